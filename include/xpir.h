@@ -1,0 +1,214 @@
+/* xpir.h — C-ABI of the B200-native Talek server hot path (arXiv 2001.08250).
+ *
+ * Drop-in boundary for the reference's PIR-server / cuckoo-table / interest-
+ * window interfaces (/root/reference/proj/include/oblog/{pir,cuckoo,notify,
+ * server}.hpp). Plain pointers and sizes only; no torch or CUDA types in the
+ * signatures (streams are passed as `void*` = cudaStream_t, NULL = the
+ * library's own stream). Every entry point returns an int status:
+ *
+ *     XPIR_OK (0)            success
+ *     XPIR_EINVAL (-1)       the reference would throw std::invalid_argument
+ *     XPIR_ECUDA (-2)        CUDA runtime / kernel error
+ *     XPIR_ENOMEM (-3)       device allocation failed
+ *     XPIR_ESTATE (-4)       internal invariant (e.g. FIFO ring overflow)
+ *
+ * and xpir_last_error() returns a thread-local message for the last failure.
+ * Functions taking host buffers are synchronous; *_dev functions take device
+ * pointers, enqueue on `stream` and return without synchronising.
+ *
+ * Bit and byte layouts are the reference's:
+ *   query vector   bit j = q[j/8] >> (j%8) & 1, ceil(N/8) bytes     (pir.hpp:14-28)
+ *   snapshot       bucket i at i*S, slot s of bucket i at (i*depth+s)*item
+ *                                                          (pir.hpp:32-41, cuckoo.cpp:23-29)
+ *   answer         B x S bytes, request-major                (pir.cpp:41-52)
+ */
+#ifndef XPIR_H
+#define XPIR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XPIR_OK 0
+#define XPIR_EINVAL (-1)
+#define XPIR_ECUDA (-2)
+#define XPIR_ENOMEM (-3)
+#define XPIR_ESTATE (-4)
+
+#define XPIR_SEED_LEN 32   /* crypto::SEED_LEN, crypto.hpp:20 */
+#define XPIR_PRF_KEY_LEN 16 /* crypto::PRF_KEY_LEN, crypto.hpp:13 */
+#define XPIR_MAX_DISPLACEMENTS 500u /* cuckoo::MAX_DISPLACEMENTS, cuckoo.hpp:15 */
+
+const char* xpir_last_error(void);
+int xpir_version(void);
+/* Number of kernel launches this process has issued through the library. */
+uint64_t xpir_launch_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Sealed snapshot shard (pir::Snapshot, pir.hpp:32-41) resident in HBM.     */
+/* A store holds buckets [lo, hi) of an N-bucket snapshot; lo and hi must be  */
+/* multiples of 8 unless hi == N (whole query bytes per shard).               */
+/* ------------------------------------------------------------------------ */
+typedef struct xpir_store xpir_store;
+
+int xpir_store_create(int device, uint32_t bucket_count, uint32_t bucket_size, uint32_t lo,
+                      uint32_t hi, xpir_store** out);
+int xpir_store_destroy(xpir_store* st);
+/* Upload (hi-lo)*S bucket-major bytes from host memory. */
+int xpir_store_upload(xpir_store* st, const uint8_t* host_buckets, uint64_t epoch);
+/* Copy (hi-lo)*S bytes from device memory (same device). */
+int xpir_store_upload_dev(xpir_store* st, const void* dev_src, uint64_t epoch, void* stream);
+/* Fill the shard with DetRng bytes: ChaCha20(key, nonce) keystream starting at byte
+ * offset lo*S — i.e. the shard's window of one Rng::fill(N*S) call (rng.cpp:25-31). */
+int xpir_store_fill_keystream(xpir_store* st, const uint8_t key[32], uint64_t nonce,
+                              uint64_t epoch, void* stream);
+int xpir_store_info(const xpir_store* st, uint32_t* bucket_count, uint32_t* bucket_size,
+                    uint32_t* lo, uint32_t* hi, uint64_t* epoch, void** dev_data);
+/* Download `len` shard bytes starting at shard byte `offset` (test helper). */
+int xpir_store_download(const xpir_store* st, uint64_t offset, uint64_t len, uint8_t* host_out);
+
+/* ------------------------------------------------------------------------ */
+/* PIR read scan — pir::answer / answer_batch (pir.cpp:29-52) + mask_answer   */
+/* (pir.cpp:65-69) + the server's answer step of answer_share (server.cpp:    */
+/* 115-127). Each request's answer is the XOR of the buckets it selects in    */
+/* this shard; with mask_seeds != NULL it is further XORed with               */
+/* prng_expand(mask_seed_r, S). q_bits must equal bucket_count (pir.cpp:30). */
+/* ------------------------------------------------------------------------ */
+int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint32_t q_bits,
+                      uint32_t batch, const uint8_t* mask_seeds, uint8_t* out);
+/* Seeded requests: q_r = prng_expand(seed_r, ceil(N/8)) expanded on device (K2). */
+int xpir_answer_batch_seeded(xpir_store* st, const uint8_t* seeds, uint32_t batch,
+                             const uint8_t* mask_seeds, uint8_t* out);
+
+/* Device-pointer variants. d_q rows hold the FULL ceil(N/8)-byte vector
+ * (the shard reads bytes [lo/8, ceil(hi/8))). d_out is batch*S bytes. */
+int xpir_answer_batch_dev(xpir_store* st, const uint8_t* d_q, uint64_t q_stride,
+                          uint32_t q_bits, uint32_t batch, const uint8_t* d_mask_seeds,
+                          uint8_t* d_out, void* stream);
+/* Expand seeds on device into the shard's query window only, then scan.
+ * d_qbuf: scratch of batch * xpir_query_window_bytes(st) bytes (or NULL to use an
+ * internal buffer). */
+int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_t batch,
+                                 const uint8_t* d_mask_seeds, uint8_t* d_out, void* stream);
+uint64_t xpir_query_window_bytes(const xpir_store* st);
+
+/* K2 alone: d_q[r*q_stride + k] = prng_expand(seed_r)[byte_lo + k], k < nbytes. */
+int xpir_expand_queries_dev(int device, const uint8_t* d_seeds, uint32_t batch, uint64_t byte_lo,
+                            uint64_t nbytes, uint8_t* d_q, uint64_t q_stride, void* stream);
+/* K3 alone: d_out[r*S..] ^= prng_expand(mask_seed_r, S). */
+int xpir_mask_dev(int device, uint8_t* d_out, const uint8_t* d_mask_seeds, uint32_t batch,
+                  uint32_t S, void* stream);
+/* K4: d_dst ^= XOR_k d_srcs[k] over `bytes` bytes; sources may be peer pointers
+ * (P2P over NVLink) — pir::reconstruct / combine_masked (pir.cpp:54-73). */
+int xpir_xor_reduce_dev(int device, uint8_t* d_dst, const uint8_t* const* d_srcs, uint32_t nsrc,
+                        uint64_t bytes, void* stream);
+
+/* Scan-kernel tuning / introspection. */
+typedef struct {
+    int kernel;        /* 0 = auto, 1 = direct select-XOR, 2 = M4RM byte tables */
+    int ctas_per_sm;   /* 0 = auto */
+    int reserved[6];
+} xpir_scan_opts;
+int xpir_set_scan_opts(const xpir_scan_opts* o);
+/* Which kernel the last scan used (1 direct, 2 M4RM, 3 byte-granular). */
+int xpir_last_scan_kernel(void);
+/* When enabled, CUDA events bracket every scan-kernel launch on its own stream;
+ * collect returns the summed kernel milliseconds and launch count since the last
+ * collect (synchronising on the recorded events). */
+int xpir_scan_timing(int enable);
+int xpir_scan_timing_collect(double* total_ms, uint32_t* launches);
+/* Microbenchmarks of the two ALU-side ceilings of the scan, measured on `device`:
+ * 32-bit LOP3 (acc ^= w & m) lane-ops per second, and LDS.128 shared-memory bytes
+ * per second, both chip-wide. */
+int xpir_measure_peaks(int device, double* lop3_per_s, double* smem_bytes_per_s,
+                       double* sm_clock_mhz);
+
+/* ------------------------------------------------------------------------ */
+/* Intra-box peer memory for the sharded reduce (CUDA IPC over NVLink).       */
+/* ------------------------------------------------------------------------ */
+#define XPIR_IPC_HANDLE_BYTES 64
+int xpir_ipc_get_handle(int device, const void* d_ptr, uint8_t handle[64]);
+/* Map a peer process's allocation; enables peer access (NVLink) lazily. */
+int xpir_ipc_open(int device, const uint8_t handle[64], void** d_ptr);
+int xpir_ipc_close(int device, void* d_ptr);
+int xpir_device_sync(int device);
+
+/* ------------------------------------------------------------------------ */
+/* Primitives on device, host buffers (parity tests and input generation).    */
+/* ------------------------------------------------------------------------ */
+/* crypto::prng_expand (crypto.cpp:35-45) */
+int xpir_prng_expand(const uint8_t seed[32], uint8_t* out, uint64_t len);
+/* DetRng::fill (rng.cpp:25-31): ChaCha20(key, nonce=LE64(nonce)) from block 0. */
+int xpir_keystream_dev(int device, const uint8_t key[32], uint64_t nonce, uint64_t byte_offset,
+                       uint8_t* d_out, uint64_t len, void* stream);
+/* Many fills, one per row: d_out[r*row_stride..+len] = ChaCha20(key, nonce0+r). */
+int xpir_keystream_rows_dev(int device, const uint8_t key[32], uint64_t nonce0, uint32_t rows,
+                            uint64_t len, uint8_t* d_out, uint64_t row_stride, void* stream);
+/* crypto::prf (crypto.cpp:17-33) for n inputs. */
+int xpir_prf_batch(const uint8_t key[16], const uint64_t* inputs, uint64_t n, uint64_t modulus,
+                   uint64_t* out);
+/* notify::make_interest (notify.cpp:30-35): out[i*h + k] */
+int xpir_make_interest_batch(uint32_t m_bits, uint32_t h, const uint8_t id[16],
+                             const uint64_t* seqs, uint64_t n, uint32_t* out);
+/* crypto::bloom_positions for one arbitrary item (crypto.cpp:146-166). */
+int xpir_bloom_positions(const uint8_t* item, uint64_t len, uint32_t h, uint32_t m_bits,
+                         uint32_t* out);
+/* crypto::digest = BLAKE2b (crypto.cpp:168-175), computed on the host side of the library. */
+int xpir_blake2b(const uint8_t* data, uint64_t len, uint32_t outlen, uint8_t* out);
+
+/* ------------------------------------------------------------------------ */
+/* Blocked cuckoo table — cuckoo::Table (cuckoo.hpp:37-84, cuckoo.cpp).       */
+/* ------------------------------------------------------------------------ */
+typedef struct xpir_table xpir_table;
+
+int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t capacity,
+                      uint64_t item_size, const uint8_t seed[32], xpir_table** out);
+int xpir_table_destroy(xpir_table* t);
+/* Table::insert (cuckoo.cpp:56-126) for n items in order; reports[4*i..] =
+ * {stored, dropped, gc_evicted, displacements} (InsertReport, cuckoo.hpp:23-28). */
+int xpir_table_insert_batch(xpir_table* t, const uint32_t* beta1, const uint32_t* beta2,
+                            const uint8_t* payload, uint64_t n, uint32_t* reports);
+int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_beta1, const uint32_t* d_beta2,
+                                const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
+                                void* stream);
+/* Table::snapshot bytes (cuckoo.cpp:128-135). */
+int xpir_table_snapshot(const xpir_table* t, uint8_t* host_out);
+/* Seal into a store covering the whole table or a bucket range of it (device copy). */
+int xpir_table_seal(const xpir_table* t, xpir_store* st, uint64_t epoch, void* stream);
+int xpir_table_meta(const xpir_table* t, uint8_t* used, uint32_t* beta1, uint32_t* beta2,
+                    uint64_t* stamp);
+int xpir_table_counters(const xpir_table* t, uint64_t* writes, uint64_t* live,
+                        uint64_t* next_stamp);
+/* Table::state_digest (cuckoo.cpp:137-149). */
+int xpir_table_state_digest(const xpir_table* t, uint8_t out[32]);
+/* Table::slot_used (cuckoo.cpp:160-163). */
+int xpir_table_slot_used(const xpir_table* t, uint32_t bucket, uint32_t slot);
+void* xpir_table_device_data(const xpir_table* t);
+
+/* ------------------------------------------------------------------------ */
+/* Interest window — notify::Window (notify.hpp:57-88, notify.cpp:54-117).    */
+/* ------------------------------------------------------------------------ */
+typedef struct xpir_window xpir_window;
+
+int xpir_window_create(int device, uint32_t m_bits, uint32_t h, uint32_t w, xpir_window** out);
+int xpir_window_destroy(xpir_window* win);
+/* Window::absorb: OR positions into the newest delta; EINVAL if any >= m_bits. */
+int xpir_window_absorb(xpir_window* win, const uint32_t* positions, uint64_t n);
+int xpir_window_absorb_dev(xpir_window* win, const uint32_t* d_positions, uint64_t n,
+                           void* stream);
+/* Fused make_interest(bp, id, seq_i) + absorb for n writes (BLAKE2b on device). */
+int xpir_window_absorb_interest(xpir_window* win, const uint8_t id[16], const uint64_t* seqs,
+                                uint64_t n);
+int xpir_window_rotate(xpir_window* win);
+int xpir_window_info(const xpir_window* win, uint64_t* size, uint64_t* base);
+int xpir_window_delta(const xpir_window* win, uint64_t i, uint64_t* out_words);
+/* Window::digest (notify.cpp:87-107). */
+int xpir_window_digest(const xpir_window* win, uint8_t out[32]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

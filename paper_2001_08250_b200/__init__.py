@@ -1,0 +1,521 @@
+"""B200-native server hot path of Talek (arXiv 2001.08250): batched XOR-PIR over a
+blocked-cuckoo-hashed store, plus the per-round write path.
+
+This module is a thin ctypes mirror of the C-ABI in ``include/xpir.h``; every
+computation happens in the sm_100a kernels of ``libxpir.so`` (built in-tree by
+``make -C paper_2001_08250_b200``). There is no CPU fallback: importing works
+anywhere, but any call fails loudly (``XpirError``) if the library is missing
+or no GPU is visible.
+
+Names mirror the reference interface (``/root/reference/proj/include/oblog``):
+
+=========================  ==================================================
+reference                  here
+=========================  ==================================================
+pir::Snapshot              ``Store`` (one shard of a sealed snapshot in HBM)
+pir::answer_batch          ``Store.answer_batch`` / ``answer_batch_dev``
+pir::mask_answer           ``mask_seeds=`` argument (fused K3)
+crypto::prng_expand        ``prng_expand`` / ``Store.answer_batch_seeded``
+pir::reconstruct           ``xor_reduce_dev`` (K4, also over NVLink peers)
+cuckoo::Table              ``Table``
+notify::Window             ``Window``
+crypto::prf                ``prf_batch``
+notify::make_interest      ``make_interest_batch``
+=========================  ==================================================
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libxpir.so")
+
+XPIR_OK, XPIR_EINVAL, XPIR_ECUDA, XPIR_ENOMEM, XPIR_ESTATE = 0, -1, -2, -3, -4
+MAX_DISPLACEMENTS = 500  # cuckoo.hpp:15
+
+
+class XpirError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"xpir error {code}: {msg}")
+        self.code = code
+
+
+class InvalidArgument(XpirError, ValueError):
+    """The reference would throw std::invalid_argument here."""
+
+
+_u8p = C.POINTER(C.c_uint8)
+_u32p = C.POINTER(C.c_uint32)
+_u64p = C.POINTER(C.c_uint64)
+_vp = C.c_void_p
+
+_lib = None
+
+
+def build(verbose: bool = False) -> str:
+    """Compile libxpir.so for sm_100a in-tree (nvcc cross-compiles without a GPU)."""
+    out = subprocess.run(["make", "-C", HERE, "-j4"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("libxpir build failed:\n" + out.stdout + out.stderr)
+    if verbose:
+        print(out.stdout)
+    return LIB_PATH
+
+
+_SIGS = {
+    "xpir_last_error": ([], C.c_char_p),
+    "xpir_version": ([], C.c_int),
+    "xpir_launch_count": ([], C.c_uint64),
+    "xpir_set_scan_opts": ([_vp], C.c_int),
+    "xpir_last_scan_kernel": ([], C.c_int),
+    "xpir_scan_timing": ([C.c_int], C.c_int),
+    "xpir_scan_timing_collect": ([C.POINTER(C.c_double), _u32p], C.c_int),
+    "xpir_measure_peaks": ([C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+    "xpir_ipc_get_handle": ([C.c_int, _vp, _u8p], C.c_int),
+    "xpir_ipc_open": ([C.c_int, _u8p, C.POINTER(_vp)], C.c_int),
+    "xpir_ipc_close": ([C.c_int, _vp], C.c_int),
+    "xpir_device_sync": ([C.c_int], C.c_int),
+    "xpir_store_create": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "xpir_store_destroy": ([_vp], C.c_int),
+    "xpir_store_upload": ([_vp, _u8p, C.c_uint64], C.c_int),
+    "xpir_store_upload_dev": ([_vp, _vp, C.c_uint64, _vp], C.c_int),
+    "xpir_store_fill_keystream": ([_vp, _u8p, C.c_uint64, C.c_uint64, _vp], C.c_int),
+    "xpir_store_info": ([_vp, _u32p, _u32p, _u32p, _u32p, _u64p, C.POINTER(_vp)], C.c_int),
+    "xpir_store_download": ([_vp, C.c_uint64, C.c_uint64, _u8p], C.c_int),
+    "xpir_answer_batch": ([_vp, _u8p, C.c_uint64, C.c_uint32, C.c_uint32, _u8p, _u8p], C.c_int),
+    "xpir_answer_batch_seeded": ([_vp, _u8p, C.c_uint32, _u8p, _u8p], C.c_int),
+    "xpir_answer_batch_dev": ([_vp, _vp, C.c_uint64, C.c_uint32, C.c_uint32, _vp, _vp, _vp], C.c_int),
+    "xpir_answer_batch_seeded_dev": ([_vp, _vp, C.c_uint32, _vp, _vp, _vp], C.c_int),
+    "xpir_query_window_bytes": ([_vp], C.c_uint64),
+    "xpir_expand_queries_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint64, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
+    "xpir_mask_dev": ([C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, _vp], C.c_int),
+    "xpir_xor_reduce_dev": ([C.c_int, _vp, _vp, C.c_uint32, C.c_uint64, _vp], C.c_int),
+    "xpir_prng_expand": ([_u8p, _u8p, C.c_uint64], C.c_int),
+    "xpir_keystream_dev": ([C.c_int, _u8p, C.c_uint64, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
+    "xpir_keystream_rows_dev": ([C.c_int, _u8p, C.c_uint64, C.c_uint32, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
+    "xpir_prf_batch": ([_u8p, _u64p, C.c_uint64, C.c_uint64, _u64p], C.c_int),
+    "xpir_make_interest_batch": ([C.c_uint32, C.c_uint32, _u8p, _u64p, C.c_uint64, _u32p], C.c_int),
+    "xpir_bloom_positions": ([_u8p, C.c_uint64, C.c_uint32, C.c_uint32, _u32p], C.c_int),
+    "xpir_blake2b": ([_u8p, C.c_uint64, C.c_uint32, _u8p], C.c_int),
+    "xpir_table_create": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _u8p, C.POINTER(_vp)], C.c_int),
+    "xpir_table_destroy": ([_vp], C.c_int),
+    "xpir_table_insert_batch": ([_vp, _u32p, _u32p, _u8p, C.c_uint64, _u32p], C.c_int),
+    "xpir_table_insert_batch_dev": ([_vp, _vp, _vp, _vp, C.c_uint64, _vp, _vp], C.c_int),
+    "xpir_table_snapshot": ([_vp, _u8p], C.c_int),
+    "xpir_table_seal": ([_vp, _vp, C.c_uint64, _vp], C.c_int),
+    "xpir_table_meta": ([_vp, _u8p, _u32p, _u32p, _u64p], C.c_int),
+    "xpir_table_counters": ([_vp, _u64p, _u64p, _u64p], C.c_int),
+    "xpir_table_state_digest": ([_vp, _u8p], C.c_int),
+    "xpir_table_slot_used": ([_vp, C.c_uint32, C.c_uint32], C.c_int),
+    "xpir_table_device_data": ([_vp], _vp),
+    "xpir_window_create": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "xpir_window_destroy": ([_vp], C.c_int),
+    "xpir_window_absorb": ([_vp, _u32p, C.c_uint64], C.c_int),
+    "xpir_window_absorb_dev": ([_vp, _vp, C.c_uint64, _vp], C.c_int),
+    "xpir_window_absorb_interest": ([_vp, _u8p, _u64p, C.c_uint64], C.c_int),
+    "xpir_window_rotate": ([_vp], C.c_int),
+    "xpir_window_info": ([_vp, _u64p, _u64p], C.c_int),
+    "xpir_window_delta": ([_vp, C.c_uint64, _u64p], C.c_int),
+    "xpir_window_digest": ([_vp, _u8p], C.c_int),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+
+def lib() -> C.CDLL:
+    """Load libxpir.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise XpirError(XPIR_ECUDA, f"{LIB_PATH} missing: run paper_2001_08250_b200.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> int:
+    if rc >= 0:
+        return rc
+    msg = lib().xpir_last_error().decode(errors="replace")
+    if rc == XPIR_EINVAL:
+        raise InvalidArgument(rc, msg)
+    raise XpirError(rc, msg)
+
+
+def _p(a: np.ndarray, t=_u8p):
+    return a.ctypes.data_as(t)
+
+
+def _u8(x) -> np.ndarray:
+    if isinstance(x, (bytes, bytearray, memoryview)):
+        return np.frombuffer(bytes(x), dtype=np.uint8).copy()
+    return np.ascontiguousarray(x, dtype=np.uint8)
+
+
+def _ptr(x) -> int | None:
+    """Device pointer of a torch tensor (or an int address)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream  # torch.cuda.Stream
+
+
+def launch_count() -> int:
+    return lib().xpir_launch_count()
+
+
+def last_scan_kernel() -> int:
+    """1 = direct select-XOR, 2 = M4RM byte tables, 3 = byte-granular."""
+    return lib().xpir_last_scan_kernel()
+
+
+class _ScanOpts(C.Structure):
+    _fields_ = [("kernel", C.c_int), ("ctas_per_sm", C.c_int), ("reserved", C.c_int * 6)]
+
+
+def set_scan_opts(kernel: int = 0, ctas_per_sm: int = 0) -> None:
+    o = _ScanOpts(kernel, ctas_per_sm)
+    _check(lib().xpir_set_scan_opts(C.byref(o)))
+
+
+def scan_timing(enable: bool) -> None:
+    _check(lib().xpir_scan_timing(1 if enable else 0))
+
+
+def scan_timing_collect() -> tuple[float, int]:
+    """(summed scan-kernel ms, launches) since the last collect."""
+    ms, n = C.c_double(), C.c_uint32()
+    _check(lib().xpir_scan_timing_collect(C.byref(ms), C.byref(n)))
+    return ms.value, n.value
+
+
+def measure_peaks(device: int = 0) -> dict:
+    """LOP3 lane-op rate and LDS.128 bandwidth of this GPU (roofline denominators)."""
+    a, b, c = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().xpir_measure_peaks(device, C.byref(a), C.byref(b), C.byref(c)))
+    return {"lop3_per_s": a.value, "smem_bytes_per_s": b.value, "sm_clock_attr_mhz": c.value}
+
+
+def ipc_handle(d_ptr, device: int = 0) -> bytes:
+    out = np.empty(64, np.uint8)
+    _check(lib().xpir_ipc_get_handle(device, _ptr(d_ptr), _p(out)))
+    return out.tobytes()
+
+
+def ipc_open(handle: bytes, device: int = 0) -> int:
+    p = _vp()
+    _check(lib().xpir_ipc_open(device, _p(_u8(handle)), C.byref(p)))
+    return p.value
+
+
+def ipc_close(d_ptr: int, device: int = 0) -> None:
+    _check(lib().xpir_ipc_close(device, d_ptr))
+
+
+def device_sync(device: int = 0) -> None:
+    _check(lib().xpir_device_sync(device))
+
+
+# ---------------------------------------------------------------------------
+# pir::Snapshot shard
+# ---------------------------------------------------------------------------
+class Store:
+    """Buckets [lo, hi) of an N-bucket sealed snapshot, resident on `device`."""
+
+    def __init__(self, bucket_count: int, bucket_size: int, lo: int = 0, hi: int | None = None,
+                 device: int = 0):
+        hi = bucket_count if hi is None else hi
+        h = _vp()
+        _check(lib().xpir_store_create(device, bucket_count, bucket_size, lo, hi, C.byref(h)))
+        self.h, self.N, self.S, self.lo, self.hi, self.device = h, bucket_count, bucket_size, lo, hi, device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xpir_store_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    @property
+    def shard_bytes(self) -> int:
+        return (self.hi - self.lo) * self.S
+
+    def upload(self, buckets: np.ndarray, epoch: int = 1) -> None:
+        b = _u8(buckets).reshape(-1)
+        if b.size != self.shard_bytes:
+            raise InvalidArgument(XPIR_EINVAL, "upload: size differs from the shard")
+        _check(lib().xpir_store_upload(self.h, _p(b), epoch))
+
+    def upload_dev(self, src, epoch: int = 1, stream=None) -> None:
+        _check(lib().xpir_store_upload_dev(self.h, _ptr(src), epoch, _stream(stream)))
+
+    def fill_keystream(self, key32: bytes, nonce: int, epoch: int = 1, stream=None) -> None:
+        """Shard window of one DetRng fill call (rng.cpp:25-31), generated on device."""
+        _check(lib().xpir_store_fill_keystream(self.h, _p(_u8(key32)), nonce, epoch, _stream(stream)))
+
+    def download(self, offset: int = 0, length: int | None = None) -> np.ndarray:
+        length = self.shard_bytes - offset if length is None else length
+        out = np.empty(max(length, 1), np.uint8)
+        _check(lib().xpir_store_download(self.h, offset, length, _p(out)))
+        return out[:length]
+
+    def device_ptr(self) -> int:
+        p = _vp()
+        _check(lib().xpir_store_info(self.h, None, None, None, None, None, C.byref(p)))
+        return p.value
+
+    @property
+    def query_window_bytes(self) -> int:
+        return lib().xpir_query_window_bytes(self.h)
+
+    # pir::answer_batch (pir.cpp:41-52) [+ mask_answer, pir.cpp:65-69]
+    def answer_batch(self, queries: np.ndarray, q_bits: int | None = None,
+                     mask_seeds: np.ndarray | None = None) -> np.ndarray:
+        q = _u8(queries)
+        if q.ndim == 1:
+            q = q.reshape(1, -1)
+        B = q.shape[0]
+        out = np.empty((B, self.S), np.uint8)
+        ms = None if mask_seeds is None else _u8(mask_seeds).reshape(B, 32)
+        _check(lib().xpir_answer_batch(self.h, _p(q) if B else None, q.shape[1] if B else 0,
+                                       self.N if q_bits is None else q_bits, B,
+                                       None if ms is None else _p(ms), _p(out) if B else None))
+        return out
+
+    def answer(self, query, q_bits: int | None = None) -> np.ndarray:
+        """pir::answer (pir.cpp:29-39)."""
+        return self.answer_batch(_u8(query).reshape(1, -1), q_bits)[0]
+
+    def answer_batch_seeded(self, seeds: np.ndarray, mask_seeds: np.ndarray | None = None) -> np.ndarray:
+        s = _u8(seeds).reshape(-1, 32)
+        B = s.shape[0]
+        out = np.empty((B, self.S), np.uint8)
+        ms = None if mask_seeds is None else _u8(mask_seeds).reshape(B, 32)
+        _check(lib().xpir_answer_batch_seeded(self.h, _p(s), B, None if ms is None else _p(ms), _p(out)))
+        return out
+
+    # device variants (torch tensors or raw pointers)
+    def answer_batch_dev(self, d_q, q_stride: int, B: int, d_out, d_mask=None, stream=None,
+                         q_bits: int | None = None) -> None:
+        _check(lib().xpir_answer_batch_dev(self.h, _ptr(d_q), q_stride, self.N if q_bits is None else q_bits,
+                                           B, _ptr(d_mask), _ptr(d_out), _stream(stream)))
+
+    def answer_batch_seeded_dev(self, d_seeds, B: int, d_out, d_mask=None, stream=None) -> None:
+        _check(lib().xpir_answer_batch_seeded_dev(self.h, _ptr(d_seeds), B, _ptr(d_mask), _ptr(d_out),
+                                                  _stream(stream)))
+
+
+def expand_queries_dev(d_seeds, B: int, byte_lo: int, nbytes: int, d_q, q_stride: int, device: int = 0,
+                       stream=None) -> None:
+    _check(lib().xpir_expand_queries_dev(device, _ptr(d_seeds), B, byte_lo, nbytes, _ptr(d_q), q_stride,
+                                         _stream(stream)))
+
+
+def mask_dev(d_out, d_mask, B: int, S: int, device: int = 0, stream=None) -> None:
+    _check(lib().xpir_mask_dev(device, _ptr(d_out), _ptr(d_mask), B, S, _stream(stream)))
+
+
+def xor_reduce_dev(d_dst, src_ptrs: list[int], nbytes: int, device: int = 0, stream=None,
+                   d_ptr_array=None) -> None:
+    """d_dst ^= XOR of the source buffers (device pointers, peers allowed).
+    `d_ptr_array` is a device buffer holding the pointer array (uint64 tensor)."""
+    _check(lib().xpir_xor_reduce_dev(device, _ptr(d_dst), _ptr(d_ptr_array), len(src_ptrs), nbytes,
+                                     _stream(stream)))
+
+
+# ---------------------------------------------------------------------------
+# primitives
+# ---------------------------------------------------------------------------
+def prng_expand(seed32: bytes, n: int) -> bytes:
+    out = np.empty(max(n, 1), np.uint8)
+    _check(lib().xpir_prng_expand(_p(_u8(seed32)), _p(out), n))
+    return out[:n].tobytes()
+
+
+def keystream_dev(key32: bytes, nonce: int, d_out, nbytes: int, byte_offset: int = 0, device: int = 0,
+                  stream=None) -> None:
+    _check(lib().xpir_keystream_dev(device, _p(_u8(key32)), nonce, byte_offset, _ptr(d_out), nbytes,
+                                    _stream(stream)))
+
+
+def keystream_rows_dev(key32: bytes, nonce0: int, rows: int, nbytes: int, d_out, row_stride: int,
+                       device: int = 0, stream=None) -> None:
+    _check(lib().xpir_keystream_rows_dev(device, _p(_u8(key32)), nonce0, rows, nbytes, _ptr(d_out),
+                                         row_stride, _stream(stream)))
+
+
+def prf_batch(key16: bytes, inputs, modulus: int) -> np.ndarray:
+    x = np.ascontiguousarray(inputs, np.uint64)
+    out = np.empty(max(len(x), 1), np.uint64)
+    _check(lib().xpir_prf_batch(_p(_u8(key16)), _p(x, _u64p), len(x), modulus, _p(out, _u64p)))
+    return out[: len(x)]
+
+
+def make_interest_batch(m_bits: int, h: int, id16: bytes, seqs) -> np.ndarray:
+    s = np.ascontiguousarray(seqs, np.uint64)
+    out = np.empty((max(len(s), 1), max(h, 1)), np.uint32)
+    _check(lib().xpir_make_interest_batch(m_bits, h, _p(_u8(id16)), _p(s, _u64p), len(s), _p(out, _u32p)))
+    return out[: len(s), :h]
+
+
+def bloom_positions(item: bytes, h: int, m_bits: int) -> list[int]:
+    it = _u8(item) if len(item) else np.zeros(1, np.uint8)
+    out = np.empty(max(h, 1), np.uint32)
+    _check(lib().xpir_bloom_positions(_p(it), len(item), h, m_bits, _p(out, _u32p)))
+    return out[:h].tolist()
+
+
+def blake2b(data: bytes, outlen: int = 32) -> bytes:
+    d = _u8(data) if len(data) else np.zeros(1, np.uint8)
+    out = np.empty(64, np.uint8)
+    _check(lib().xpir_blake2b(_p(d), len(data), outlen, _p(out)))
+    return out[:outlen].tobytes()
+
+
+# ---------------------------------------------------------------------------
+# cuckoo::Table
+# ---------------------------------------------------------------------------
+class Table:
+    def __init__(self, buckets: int, depth: int, capacity: int, item_size: int, seed32: bytes,
+                 device: int = 0):
+        h = _vp()
+        _check(lib().xpir_table_create(device, buckets, depth, capacity, item_size, _p(_u8(seed32)),
+                                       C.byref(h)))
+        self.h, self.buckets, self.depth, self.item, self.device = h, buckets, depth, item_size, device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xpir_table_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def insert_batch(self, beta1, beta2, payload) -> np.ndarray:
+        """Table::insert for each item in order; returns n x 4 InsertReport rows."""
+        b1 = np.ascontiguousarray(beta1, np.uint32)
+        b2 = np.ascontiguousarray(beta2, np.uint32)
+        n = len(b1)
+        pl = _u8(payload).reshape(-1)
+        if pl.size != n * self.item:
+            raise InvalidArgument(XPIR_EINVAL, "cuckoo: item size mismatch")
+        rep = np.zeros((max(n, 1), 4), np.uint32)
+        _check(lib().xpir_table_insert_batch(self.h, _p(b1, _u32p), _p(b2, _u32p), _p(pl), n,
+                                             _p(rep, _u32p)))
+        return rep[:n]
+
+    def insert(self, beta1: int, beta2: int, data: bytes) -> dict:
+        r = self.insert_batch([beta1], [beta2], _u8(data))[0]
+        return {"stored": bool(r[0]), "dropped": bool(r[1]), "gc_evicted": bool(r[2]),
+                "displacements": int(r[3])}
+
+    def insert_batch_dev(self, d_b1, d_b2, d_payload, n: int, d_reports=None, stream=None) -> None:
+        _check(lib().xpir_table_insert_batch_dev(self.h, _ptr(d_b1), _ptr(d_b2), _ptr(d_payload), n,
+                                                 _ptr(d_reports), _stream(stream)))
+
+    def snapshot(self) -> np.ndarray:
+        out = np.empty(self.buckets * self.depth * self.item, np.uint8)
+        _check(lib().xpir_table_snapshot(self.h, _p(out)))
+        return out
+
+    def seal(self, store: Store, epoch: int, stream=None) -> None:
+        _check(lib().xpir_table_seal(self.h, store.h, epoch, _stream(stream)))
+
+    def meta(self):
+        n = self.buckets * self.depth
+        used = np.empty(n, np.uint8)
+        b1 = np.empty(n, np.uint32)
+        b2 = np.empty(n, np.uint32)
+        st = np.empty(n, np.uint64)
+        _check(lib().xpir_table_meta(self.h, _p(used), _p(b1, _u32p), _p(b2, _u32p), _p(st, _u64p)))
+        return used, b1, b2, st
+
+    def counters(self):
+        w, l, s = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().xpir_table_counters(self.h, C.byref(w), C.byref(l), C.byref(s)))
+        return w.value, l.value, s.value
+
+    def writes_applied(self) -> int:
+        return self.counters()[0]
+
+    def live_count(self) -> int:
+        return self.counters()[1]
+
+    def state_digest(self) -> bytes:
+        out = np.empty(32, np.uint8)
+        _check(lib().xpir_table_state_digest(self.h, _p(out)))
+        return out.tobytes()
+
+    def slot_used(self, bucket: int, slot: int) -> bool:
+        return bool(_check(lib().xpir_table_slot_used(self.h, bucket, slot)))
+
+    def device_ptr(self) -> int:
+        return lib().xpir_table_device_data(self.h)
+
+
+# ---------------------------------------------------------------------------
+# notify::Window
+# ---------------------------------------------------------------------------
+class Window:
+    def __init__(self, m_bits: int, h: int, w: int, device: int = 0):
+        hd = _vp()
+        _check(lib().xpir_window_create(device, m_bits, h, w, C.byref(hd)))
+        self.h, self.m, self.nh, self.w, self.device = hd, m_bits, h, w, device
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xpir_window_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def absorb(self, positions) -> None:
+        p = np.ascontiguousarray(positions, np.uint32).reshape(-1)
+        _check(lib().xpir_window_absorb(self.h, _p(p, _u32p) if p.size else None, p.size))
+
+    def absorb_dev(self, d_pos, n: int, stream=None) -> None:
+        _check(lib().xpir_window_absorb_dev(self.h, _ptr(d_pos), n, _stream(stream)))
+
+    def absorb_interest(self, id16: bytes, seqs) -> None:
+        s = np.ascontiguousarray(seqs, np.uint64)
+        _check(lib().xpir_window_absorb_interest(self.h, _p(_u8(id16)), _p(s, _u64p), len(s)))
+
+    def rotate(self) -> None:
+        _check(lib().xpir_window_rotate(self.h))
+
+    def info(self):
+        n, b = C.c_uint64(), C.c_uint64()
+        _check(lib().xpir_window_info(self.h, C.byref(n), C.byref(b)))
+        return n.value, b.value
+
+    def size(self) -> int:
+        return self.info()[0]
+
+    def base(self) -> int:
+        return self.info()[1]
+
+    def delta(self, i: int) -> np.ndarray:
+        out = np.empty((self.m + 63) // 64, np.uint64)
+        _check(lib().xpir_window_delta(self.h, i, _p(out, _u64p)))
+        return out
+
+    def digest(self) -> bytes:
+        out = np.empty(32, np.uint8)
+        _check(lib().xpir_window_digest(self.h, _p(out)))
+        return out.tobytes()

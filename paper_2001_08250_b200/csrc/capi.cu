@@ -1,0 +1,1071 @@
+// extern "C" boundary (include/xpir.h) over the sm_100a kernels in scan.cu and
+// write.cu. Host-side bookkeeping only: argument validation with the
+// reference's error conditions, device memory ownership, kernel dispatch.
+// There is no CPU compute path: every answer, table mutation and filter update
+// is produced by a kernel, and the library fails (XPIR_ECUDA) without a GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/xpir.h"
+#include "prims.cuh"
+#include "scan.cuh"
+
+namespace xpir {
+static std::atomic<uint64_t> g_launches{0};
+void count_launches(uint64_t n) { g_launches += n; }
+}  // namespace xpir
+
+using namespace xpir;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int> g_last_kernel{0};
+xpir_scan_opts g_opts{};
+std::mutex g_opts_mu;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define XCK(expr)                                                                       \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(XPIR_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int num_sms(int dev) {
+    static int cache[64] = {0};
+    if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < 64) cache[dev] = n;
+    return n;
+}
+
+// Grow-only device scratch buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(n, size_t(256));
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+uint64_t round16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+
+// Host BLAKE2b (same algorithm as the device port in prims.cuh), incremental,
+// used for the digests that the reference computes over whole tables/windows.
+struct HostBlake2b {
+    uint64_t h[8];
+    uint64_t t = 0;
+    uint8_t buf[128];
+    size_t buflen = 0, outlen;
+    explicit HostBlake2b(size_t out) : outlen(out) {
+        for (int i = 0; i < 8; ++i) h[i] = b2_iv(i);
+        h[0] ^= 0x01010000ULL ^ out;
+    }
+    void block(bool last) {
+        uint64_t m[16];
+        for (int i = 0; i < 16; ++i) m[i] = ld64le(buf + 8 * i);
+        blake2b_compress(h, m, t, 0, last);
+    }
+    void update(const uint8_t* in, size_t len) {
+        while (len) {
+            if (buflen == 128) {
+                t += 128;
+                block(false);
+                buflen = 0;
+            }
+            size_t take = std::min(len, 128 - buflen);
+            std::memcpy(buf + buflen, in, take);
+            buflen += take;
+            in += take;
+            len -= take;
+        }
+    }
+    void update_u64be(uint64_t v) {
+        uint8_t b[8];
+        for (int i = 0; i < 8; ++i) b[i] = uint8_t(v >> (56 - 8 * i));
+        update(b, 8);
+    }
+    void final(uint8_t* out) {
+        t += buflen;
+        std::memset(buf + buflen, 0, 128 - buflen);
+        block(true);
+        uint8_t full[64];
+        for (int i = 0; i < 8; ++i)
+            for (int k = 0; k < 8; ++k) full[8 * i + k] = uint8_t(h[i] >> (8 * k));
+        std::memcpy(out, full, outlen);
+    }
+};
+
+}  // namespace
+
+// ===========================================================================
+// store
+// ===========================================================================
+struct xpir_store {
+    int device;
+    uint32_t N, S, lo, hi;
+    uint64_t epoch = 0;
+    uint8_t* data = nullptr;
+    cudaStream_t stream = nullptr;
+    DevBuf q, part, out, seeds, masks, qwin;
+    std::mutex mu;
+    uint32_t nb() const { return hi - lo; }
+    uint64_t bytes() const { return uint64_t(nb()) * S; }
+    uint64_t byte_lo() const { return lo / 8; }
+    uint64_t nbytes_window() const { return (uint64_t(hi) + 7) / 8 - lo / 8; }
+};
+
+extern "C" {
+
+const char* xpir_last_error(void) { return g_err.c_str(); }
+int xpir_version(void) { return 1; }
+uint64_t xpir_launch_count(void) { return g_launches.load(); }
+
+int xpir_set_scan_opts(const xpir_scan_opts* o) {
+    std::lock_guard<std::mutex> lk(g_opts_mu);
+    g_opts = o ? *o : xpir_scan_opts{};
+    return XPIR_OK;
+}
+int xpir_last_scan_kernel(void) { return g_last_kernel.load(); }
+
+}  // extern "C"
+
+// Scan-kernel event timing (bench.py's roofline.achieved denominator).
+namespace {
+std::mutex g_tmu;
+bool g_timing = false;
+std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+
+void timing_begin(cudaStream_t s, cudaEvent_t* a) {
+    *a = nullptr;
+    std::lock_guard<std::mutex> lk(g_tmu);
+    if (!g_timing) return;
+    cudaEventCreate(a);
+    cudaEventRecord(*a, s);
+}
+void timing_end(cudaStream_t s, cudaEvent_t a) {
+    if (!a) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, s);
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_events.emplace_back(a, b);
+}
+}  // namespace
+
+extern "C" {
+
+int xpir_scan_timing(int enable) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_timing = enable != 0;
+    return XPIR_OK;
+}
+
+int xpir_scan_timing_collect(double* total_ms, uint32_t* launches) {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    {
+        std::lock_guard<std::mutex> lk(g_tmu);
+        ev.swap(g_events);
+    }
+    double tot = 0;
+    for (auto& p : ev) {
+        float ms = 0;
+        XCK(cudaEventSynchronize(p.second));
+        XCK(cudaEventElapsedTime(&ms, p.first, p.second));
+        tot += ms;
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = uint32_t(ev.size());
+    return XPIR_OK;
+}
+
+int xpir_measure_peaks(int device, double* lop3_per_s, double* smem_bps, double* sm_clock_mhz) {
+    DeviceGuard g(device);
+    cudaStream_t s;
+    XCK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaError_t e = run_peak_kernels(num_sms(device), lop3_per_s, smem_bps, s);
+    count_launches(4);
+    cudaStreamDestroy(s);
+    XCK(e);
+    if (sm_clock_mhz) {
+        int khz = 0;
+        cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device);
+        *sm_clock_mhz = khz / 1000.0;
+    }
+    return XPIR_OK;
+}
+
+int xpir_ipc_get_handle(int device, const void* d_ptr, uint8_t handle[64]) {
+    if (!d_ptr || !handle) return fail(XPIR_EINVAL, "ipc_get_handle: null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    XCK(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+    std::memcpy(handle, &h, 64);
+    return XPIR_OK;
+}
+
+int xpir_ipc_open(int device, const uint8_t handle[64], void** d_ptr) {
+    if (!handle || !d_ptr) return fail(XPIR_EINVAL, "ipc_open: null argument");
+    DeviceGuard g(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    XCK(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return XPIR_OK;
+}
+
+int xpir_ipc_close(int device, void* d_ptr) {
+    DeviceGuard g(device);
+    XCK(cudaIpcCloseMemHandle(d_ptr));
+    return XPIR_OK;
+}
+
+int xpir_device_sync(int device) {
+    DeviceGuard g(device);
+    XCK(cudaDeviceSynchronize());
+    return XPIR_OK;
+}
+
+int xpir_store_create(int device, uint32_t N, uint32_t S, uint32_t lo, uint32_t hi,
+                      xpir_store** out) {
+    if (!out) return fail(XPIR_EINVAL, "store_create: null out");
+    if (N == 0 || S == 0) return fail(XPIR_EINVAL, "store_create: empty geometry");
+    if (lo >= hi || hi > N) return fail(XPIR_EINVAL, "store_create: bad shard range");
+    if (lo % 8 != 0 || (hi % 8 != 0 && hi != N))
+        return fail(XPIR_EINVAL, "store_create: shard bounds must be multiples of 8 buckets");
+    int ndev = 0;
+    XCK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(XPIR_EINVAL, "store_create: bad device");
+    DeviceGuard g(device);
+    auto* st = new xpir_store;
+    st->device = device;
+    st->N = N;
+    st->S = S;
+    st->lo = lo;
+    st->hi = hi;
+    cudaError_t e = cudaMalloc(&st->data, std::max<uint64_t>(st->bytes(), 16));
+    if (e != cudaSuccess) {
+        delete st;
+        return fail(XPIR_ENOMEM, std::string("store_create: ") + cudaGetErrorString(e));
+    }
+    e = cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        cudaFree(st->data);
+        delete st;
+        return fail(XPIR_ECUDA, cudaGetErrorString(e));
+    }
+    *out = st;
+    return XPIR_OK;
+}
+
+int xpir_store_destroy(xpir_store* st) {
+    if (!st) return XPIR_OK;
+    DeviceGuard g(st->device);
+    cudaStreamSynchronize(st->stream);
+    cudaFree(st->data);
+    st->q.release();
+    st->part.release();
+    st->out.release();
+    st->seeds.release();
+    st->masks.release();
+    st->qwin.release();
+    cudaStreamDestroy(st->stream);
+    delete st;
+    return XPIR_OK;
+}
+
+int xpir_store_upload(xpir_store* st, const uint8_t* host, uint64_t epoch) {
+    if (!st || !host) return fail(XPIR_EINVAL, "store_upload: null argument");
+    std::lock_guard<std::mutex> lk(st->mu);
+    DeviceGuard g(st->device);
+    XCK(cudaMemcpyAsync(st->data, host, st->bytes(), cudaMemcpyHostToDevice, st->stream));
+    XCK(cudaStreamSynchronize(st->stream));
+    st->epoch = epoch;
+    return XPIR_OK;
+}
+
+int xpir_store_upload_dev(xpir_store* st, const void* src, uint64_t epoch, void* stream) {
+    if (!st || !src) return fail(XPIR_EINVAL, "store_upload_dev: null argument");
+    DeviceGuard g(st->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
+    XCK(cudaMemcpyAsync(st->data, src, st->bytes(), cudaMemcpyDeviceToDevice, s));
+    st->epoch = epoch;
+    return XPIR_OK;
+}
+
+int xpir_store_fill_keystream(xpir_store* st, const uint8_t key[32], uint64_t nonce,
+                              uint64_t epoch, void* stream) {
+    if (!st || !key) return fail(XPIR_EINVAL, "store_fill_keystream: null argument");
+    DeviceGuard g(st->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
+    XCK(launch_keystream(key, nonce, uint64_t(st->lo) * st->S, st->data, st->bytes(), s));
+    count_launches(1);
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    st->epoch = epoch;
+    return XPIR_OK;
+}
+
+int xpir_store_info(const xpir_store* st, uint32_t* N, uint32_t* S, uint32_t* lo, uint32_t* hi,
+                    uint64_t* epoch, void** dev) {
+    if (!st) return fail(XPIR_EINVAL, "store_info: null store");
+    if (N) *N = st->N;
+    if (S) *S = st->S;
+    if (lo) *lo = st->lo;
+    if (hi) *hi = st->hi;
+    if (epoch) *epoch = st->epoch;
+    if (dev) *dev = st->data;
+    return XPIR_OK;
+}
+
+int xpir_store_download(const xpir_store* st, uint64_t offset, uint64_t len, uint8_t* host) {
+    if (!st || (len && !host)) return fail(XPIR_EINVAL, "store_download: null argument");
+    if (offset > st->bytes() || len > st->bytes() - offset)
+        return fail(XPIR_EINVAL, "store_download: range outside the shard");
+    DeviceGuard g(st->device);
+    XCK(cudaStreamSynchronize(st->stream));
+    if (len) XCK(cudaMemcpy(host, st->data + offset, len, cudaMemcpyDeviceToHost));
+    return XPIR_OK;
+}
+
+uint64_t xpir_query_window_bytes(const xpir_store* st) {
+    return st ? round16(st->nbytes_window()) + 16 : 0;
+}
+
+}  // extern "C"
+
+// Core dispatch: d_qwin rows hold the shard window (byte 0 = query byte lo/8),
+// 16-byte aligned with stride % 16 == 0 and >= round16(window) readable bytes.
+static int scan_window(xpir_store* st, const uint8_t* d_qwin, uint64_t stride, bool aligned,
+                       uint32_t B, const uint8_t* d_mask, uint8_t* d_out, cudaStream_t s) {
+    XCK(launch_init_out(d_out, B, st->S, d_mask, false, s));
+    count_launches(1);
+    if (B == 0) return XPIR_OK;
+    int kernel;
+    {
+        std::lock_guard<std::mutex> lk(g_opts_mu);
+        kernel = g_opts.kernel;
+    }
+    const bool m4_ok = (st->S % 128) == 0 && aligned;
+    if (kernel == 0) kernel = (m4_ok && B >= 96) ? 2 : 1;
+    if (kernel == 2 && !m4_ok) kernel = 1;
+    ScanArgs a{st->data, st->nb(), st->S, d_qwin, stride, B, d_out, s};
+    const int sms = num_sms(st->device);
+    if (st->S % 16 != 0) {
+        XCK(launch_scan_bytes(a));
+        count_launches(1);
+        g_last_kernel = 3;
+        return XPIR_OK;
+    }
+    if (kernel == 2) {
+        int cps;
+        {
+            std::lock_guard<std::mutex> lk(g_opts_mu);
+            cps = g_opts.ctas_per_sm;
+        }
+        cudaEvent_t ev;
+        timing_begin(s, &ev);
+        XCK(launch_scan_m4rm(a, cps, sms));
+        timing_end(s, ev);
+        count_launches(1);
+        g_last_kernel = 2;
+        return XPIR_OK;
+    }
+    // direct: partial buffer sized for up to 64 splits, capped at 256 MiB
+    const uint64_t out_bytes = uint64_t(B) * st->S;
+    uint64_t part_bytes = std::min<uint64_t>(out_bytes * 64, uint64_t(256) << 20);
+    part_bytes = std::max(part_bytes, out_bytes);
+    XCK(st->part.ensure(part_bytes));
+    uint32_t nsplit = 0;
+    cudaEvent_t ev;
+    timing_begin(s, &ev);
+    XCK(launch_scan_direct(a, st->part.as<uint8_t>(), st->part.cap, sms, &nsplit));
+    timing_end(s, ev);
+    count_launches(2);
+    g_last_kernel = 1;
+    return XPIR_OK;
+}
+
+// Full-row device queries -> aligned window (zero-copy when already aligned).
+static int scan_rows_dev(xpir_store* st, const uint8_t* d_q, uint64_t q_stride, uint32_t B,
+                         const uint8_t* d_mask, uint8_t* d_out, cudaStream_t s) {
+    const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
+    const uint8_t* qw = d_q + blo;
+    const bool aligned = (reinterpret_cast<uintptr_t>(qw) % 16) == 0 && (q_stride % 16) == 0 &&
+                         (q_stride - blo) >= round16(nbw);
+    if (aligned || (st->S % 128) != 0) return scan_window(st, qw, q_stride, aligned, B, d_mask, d_out, s);
+    const uint64_t ws = round16(nbw) + 16;
+    XCK(st->qwin.ensure(ws * B));
+    XCK(launch_repack(d_q, q_stride, blo, nbw, B, st->qwin.as<uint8_t>(), ws, s));
+    count_launches(1);
+    return scan_window(st, st->qwin.as<uint8_t>(), ws, true, B, d_mask, d_out, s);
+}
+
+extern "C" {
+
+int xpir_answer_batch_dev(xpir_store* st, const uint8_t* d_q, uint64_t q_stride, uint32_t q_bits,
+                          uint32_t B, const uint8_t* d_mask, uint8_t* d_out, void* stream) {
+    if (!st) return fail(XPIR_EINVAL, "answer_batch: null store");
+    if (q_bits != st->N) return fail(XPIR_EINVAL, "answer_batch: query length mismatch");
+    if (B && (!d_q || !d_out)) return fail(XPIR_EINVAL, "answer_batch: null buffer");
+    if (B && q_stride < (uint64_t(st->N) + 7) / 8)
+        return fail(XPIR_EINVAL, "answer_batch: query stride shorter than the vector");
+    DeviceGuard g(st->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
+    return scan_rows_dev(st, d_q, q_stride, B, d_mask, d_out, s);
+}
+
+int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_t B,
+                                 const uint8_t* d_mask, uint8_t* d_out, void* stream) {
+    if (!st) return fail(XPIR_EINVAL, "answer_batch_seeded: null store");
+    if (B && (!d_seeds || !d_out)) return fail(XPIR_EINVAL, "answer_batch_seeded: null buffer");
+    DeviceGuard g(st->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
+    const uint64_t ws = xpir_query_window_bytes(st);
+    XCK(st->qwin.ensure(ws * std::max<uint32_t>(B, 1)));
+    // K2: expand only this shard's window of every request's selection vector
+    XCK(launch_expand(d_seeds, B, st->byte_lo(), st->nbytes_window(), st->qwin.as<uint8_t>(), ws, s));
+    count_launches(1);
+    return scan_window(st, st->qwin.as<uint8_t>(), ws, true, B, d_mask, d_out, s);
+}
+
+int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint32_t q_bits,
+                      uint32_t B, const uint8_t* mask_seeds, uint8_t* out) {
+    if (!st) return fail(XPIR_EINVAL, "answer_batch: null store");
+    if (q_bits != st->N) return fail(XPIR_EINVAL, "answer_batch: query length mismatch");
+    if (B == 0) return XPIR_OK;
+    if (!q || !out) return fail(XPIR_EINVAL, "answer_batch: null buffer");
+    if (q_stride < (uint64_t(st->N) + 7) / 8)
+        return fail(XPIR_EINVAL, "answer_batch: query stride shorter than the vector");
+    std::lock_guard<std::mutex> lk(st->mu);
+    DeviceGuard g(st->device);
+    cudaStream_t s = st->stream;
+    const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
+    const uint64_t ws = round16(nbw) + 16;
+    XCK(st->q.ensure(ws * B));
+    // H2D of the shard's window of every row (pitched copy), zero padding tail
+    XCK(cudaMemsetAsync(st->q.p, 0, ws * B, s));
+    XCK(cudaMemcpy2DAsync(st->q.p, ws, q + blo, q_stride, nbw, B, cudaMemcpyHostToDevice, s));
+    const uint8_t* dm = nullptr;
+    if (mask_seeds) {
+        XCK(st->masks.ensure(uint64_t(B) * 32));
+        XCK(cudaMemcpyAsync(st->masks.p, mask_seeds, uint64_t(B) * 32, cudaMemcpyHostToDevice, s));
+        dm = st->masks.as<uint8_t>();
+    }
+    const uint64_t ob = uint64_t(B) * st->S;
+    XCK(st->out.ensure(ob));
+    int rc = scan_window(st, st->q.as<uint8_t>(), ws, true, B, dm, st->out.as<uint8_t>(), s);
+    if (rc) return rc;
+    XCK(cudaMemcpyAsync(out, st->out.p, ob, cudaMemcpyDeviceToHost, s));
+    XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_answer_batch_seeded(xpir_store* st, const uint8_t* seeds, uint32_t B,
+                             const uint8_t* mask_seeds, uint8_t* out) {
+    if (!st) return fail(XPIR_EINVAL, "answer_batch_seeded: null store");
+    if (B == 0) return XPIR_OK;
+    if (!seeds || !out) return fail(XPIR_EINVAL, "answer_batch_seeded: null buffer");
+    std::lock_guard<std::mutex> lk(st->mu);
+    DeviceGuard g(st->device);
+    cudaStream_t s = st->stream;
+    XCK(st->seeds.ensure(uint64_t(B) * 32));
+    XCK(cudaMemcpyAsync(st->seeds.p, seeds, uint64_t(B) * 32, cudaMemcpyHostToDevice, s));
+    const uint8_t* dm = nullptr;
+    if (mask_seeds) {
+        XCK(st->masks.ensure(uint64_t(B) * 32));
+        XCK(cudaMemcpyAsync(st->masks.p, mask_seeds, uint64_t(B) * 32, cudaMemcpyHostToDevice, s));
+        dm = st->masks.as<uint8_t>();
+    }
+    const uint64_t ob = uint64_t(B) * st->S;
+    XCK(st->out.ensure(ob));
+    int rc = xpir_answer_batch_seeded_dev(st, st->seeds.as<uint8_t>(), B, dm, st->out.as<uint8_t>(), s);
+    if (rc) return rc;
+    XCK(cudaMemcpyAsync(out, st->out.p, ob, cudaMemcpyDeviceToHost, s));
+    XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_expand_queries_dev(int device, const uint8_t* d_seeds, uint32_t B, uint64_t byte_lo,
+                            uint64_t nbytes, uint8_t* d_q, uint64_t q_stride, void* stream) {
+    if (B && (!d_seeds || !d_q)) return fail(XPIR_EINVAL, "expand_queries: null buffer");
+    if (q_stride < nbytes) return fail(XPIR_EINVAL, "expand_queries: stride < nbytes");
+    DeviceGuard g(device);
+    XCK(launch_expand(d_seeds, B, byte_lo, nbytes, d_q, q_stride, static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+int xpir_mask_dev(int device, uint8_t* d_out, const uint8_t* d_mask, uint32_t B, uint32_t S,
+                  void* stream) {
+    if (B && (!d_out || !d_mask)) return fail(XPIR_EINVAL, "mask: null buffer");
+    DeviceGuard g(device);
+    XCK(launch_init_out(d_out, B, S, d_mask, true, static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+int xpir_xor_reduce_dev(int device, uint8_t* d_dst, const uint8_t* const* d_srcs, uint32_t nsrc,
+                        uint64_t bytes, void* stream) {
+    if (nsrc && (!d_dst || !d_srcs)) return fail(XPIR_EINVAL, "xor_reduce: null buffer");
+    DeviceGuard g(device);
+    XCK(launch_xor_reduce(d_dst, d_srcs, nsrc, bytes, num_sms(device), static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// primitives
+// ---------------------------------------------------------------------------
+int xpir_prng_expand(const uint8_t seed[32], uint8_t* out, uint64_t len) {
+    if (!seed || (len && !out)) return fail(XPIR_EINVAL, "prng_expand: null buffer");
+    if (!len) return XPIR_OK;
+    uint8_t* d = nullptr;
+    XCK(cudaMalloc(&d, len));
+    cudaError_t e = launch_keystream(seed, 0, 0, d, len, nullptr);
+    count_launches(1);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, len, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    XCK(e);
+    return XPIR_OK;
+}
+
+int xpir_keystream_dev(int device, const uint8_t key[32], uint64_t nonce, uint64_t byte_offset,
+                       uint8_t* d_out, uint64_t len, void* stream) {
+    if (!key || (len && !d_out)) return fail(XPIR_EINVAL, "keystream: null buffer");
+    DeviceGuard g(device);
+    XCK(launch_keystream(key, nonce, byte_offset, d_out, len, static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+int xpir_keystream_rows_dev(int device, const uint8_t key[32], uint64_t nonce0, uint32_t rows,
+                            uint64_t len, uint8_t* d_out, uint64_t row_stride, void* stream) {
+    if (!key || (rows && len && !d_out)) return fail(XPIR_EINVAL, "keystream_rows: null buffer");
+    if (row_stride < len) return fail(XPIR_EINVAL, "keystream_rows: stride < len");
+    DeviceGuard g(device);
+    XCK(launch_keystream_rows(key, nonce0, rows, len, d_out, row_stride, static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+int xpir_prf_batch(const uint8_t key[16], const uint64_t* inputs, uint64_t n, uint64_t modulus,
+                   uint64_t* out) {
+    if (modulus == 0) return fail(XPIR_EINVAL, "prf: modulus must be positive");
+    if (!key || (n && (!inputs || !out))) return fail(XPIR_EINVAL, "prf: null buffer");
+    if (!n) return XPIR_OK;
+    uint64_t* d = nullptr;
+    XCK(cudaMalloc(&d, 16 * n));
+    cudaError_t e = cudaMemcpy(d, inputs, 8 * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_prf(ld64le(key), ld64le(key + 8), d, n, modulus, d + n, nullptr);
+    count_launches(1);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d + n, 8 * n, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    XCK(e);
+    return XPIR_OK;
+}
+
+int xpir_make_interest_batch(uint32_t m_bits, uint32_t h, const uint8_t id[16],
+                             const uint64_t* seqs, uint64_t n, uint32_t* out) {
+    if (m_bits == 0) return fail(XPIR_EINVAL, "bloom_positions: m_bits must be positive");
+    if (!id || (n && (!seqs || !out))) return fail(XPIR_EINVAL, "make_interest: null buffer");
+    if (!n || !h) return XPIR_OK;
+    uint64_t* ds = nullptr;
+    uint32_t* dp = nullptr;
+    XCK(cudaMalloc(&ds, 8 * n));
+    cudaError_t e = cudaMalloc(&dp, 4 * n * h);
+    if (e == cudaSuccess) e = cudaMemcpy(ds, seqs, 8 * n, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_interest(id, ds, n, h, m_bits, dp, nullptr, nullptr);
+    count_launches(1);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dp, 4 * n * h, cudaMemcpyDeviceToHost);
+    cudaFree(ds);
+    cudaFree(dp);
+    XCK(e);
+    return XPIR_OK;
+}
+
+int xpir_bloom_positions(const uint8_t* item, uint64_t len, uint32_t h, uint32_t m_bits,
+                         uint32_t* out) {
+    if (m_bits == 0) return fail(XPIR_EINVAL, "bloom_positions: m_bits must be positive");
+    if (len > 120) return fail(XPIR_EINVAL, "bloom_positions: device port takes items <= 120 bytes");
+    if ((len && !item) || (h && !out)) return fail(XPIR_EINVAL, "bloom_positions: null buffer");
+    if (!h) return XPIR_OK;
+    uint8_t* d = nullptr;
+    XCK(cudaMalloc(&d, 128 + 4 * uint64_t(h)));
+    cudaError_t e = len ? cudaMemcpy(d, item, len, cudaMemcpyHostToDevice) : cudaSuccess;
+    uint32_t* dp = reinterpret_cast<uint32_t*>(d + 128);
+    if (e == cudaSuccess) e = launch_bloom_item(d, uint32_t(len), h, m_bits, dp, nullptr);
+    count_launches(1);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dp, 4 * uint64_t(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    XCK(e);
+    return XPIR_OK;
+}
+
+int xpir_blake2b(const uint8_t* data, uint64_t len, uint32_t outlen, uint8_t* out) {
+    if (outlen < 1 || outlen > 64) return fail(XPIR_EINVAL, "blake2b: outlen must be 1..64");
+    if ((len && !data) || !out) return fail(XPIR_EINVAL, "blake2b: null buffer");
+    HostBlake2b h(outlen);
+    h.update(data, len);
+    h.final(out);
+    return XPIR_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// cuckoo table
+// ===========================================================================
+struct xpir_table {
+    int device;
+    uint8_t seed[32];
+    CuckooDev d{};
+    CuckooState h{};
+    CuckooState* dstate = nullptr;
+    uint8_t* data = nullptr;
+    cudaStream_t stream = nullptr;
+    DevBuf in_b1, in_b2, in_payload, in_reports, gather;
+    std::mutex mu;
+    uint64_t slots() const { return uint64_t(d.buckets) * d.depth; }
+};
+
+static const uint32_t DRAW_CAP = 1u << 16;
+
+static void table_free_all(xpir_table* t) {
+    cudaFree(t->d.used);
+    cudaFree(t->d.beta1);
+    cudaFree(t->d.beta2);
+    cudaFree(t->d.stamp);
+    cudaFree(t->d.origin);
+    cudaFree(t->d.touched_mark);
+    cudaFree(t->d.touched);
+    cudaFree(t->d.fifo);
+    cudaFree(t->d.draws);
+    cudaFree(t->dstate);
+    cudaFree(t->data);
+    t->in_b1.release();
+    t->in_b2.release();
+    t->in_payload.release();
+    t->in_reports.release();
+    t->gather.release();
+    if (t->stream) cudaStreamDestroy(t->stream);
+}
+
+extern "C" {
+
+int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t capacity,
+                      uint64_t item_size, const uint8_t seed[32], xpir_table** out) {
+    if (!out || !seed) return fail(XPIR_EINVAL, "table_create: null argument");
+    if (buckets == 0 || depth == 0 || item_size == 0)  // cuckoo.cpp:15-16
+        return fail(XPIR_EINVAL, "cuckoo: table dimensions must be positive");
+    if (capacity == 0 || capacity > uint64_t(buckets) * depth)  // cuckoo.cpp:17-18
+        return fail(XPIR_EINVAL, "cuckoo: capacity must be in [1, buckets*depth]");
+    if (uint64_t(buckets) * depth >= (uint64_t(1) << 32))
+        return fail(XPIR_EINVAL, "cuckoo: more than 2^32 slots");
+    int ndev = 0;
+    XCK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(XPIR_EINVAL, "table_create: bad device");
+    DeviceGuard g(device);
+    auto* t = new xpir_table;
+    t->device = device;
+    std::memcpy(t->seed, seed, 32);
+    t->d.buckets = buckets;
+    t->d.depth = depth;
+    t->d.capacity = capacity;
+    t->d.item = item_size;
+    const uint64_t slots = t->slots();
+    uint64_t fc = 1;
+    while (fc < 2 * slots + 1024) fc <<= 1;
+    t->d.fifo_cap = fc;
+    t->d.draw_cap = DRAW_CAP;
+    cudaError_t e = cudaSuccess;
+    auto M = [&](void** p, size_t n) {
+        if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(n, 16));
+        if (e == cudaSuccess) e = cudaMemset(*p, 0, std::max<size_t>(n, 16));
+    };
+    M(reinterpret_cast<void**>(&t->d.used), slots);
+    M(reinterpret_cast<void**>(&t->d.beta1), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.beta2), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.stamp), 8 * slots);
+    M(reinterpret_cast<void**>(&t->d.origin), 8 * slots);
+    M(reinterpret_cast<void**>(&t->d.touched_mark), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.touched), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.fifo), 8 * fc);
+    M(reinterpret_cast<void**>(&t->d.draws), 8 * uint64_t(DRAW_CAP));
+    M(reinterpret_cast<void**>(&t->dstate), sizeof(CuckooState));
+    M(reinterpret_cast<void**>(&t->data), slots * item_size);
+    if (e == cudaSuccess) e = cudaMemset(t->d.fifo, 0xff, 8 * fc);  // -1: no entry
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        table_free_all(t);
+        delete t;
+        return fail(e == cudaErrorMemoryAllocation ? XPIR_ENOMEM : XPIR_ECUDA,
+                    std::string("table_create: ") + cudaGetErrorString(e));
+    }
+    t->h = CuckooState{};
+    *out = t;
+    return XPIR_OK;
+}
+
+int xpir_table_destroy(xpir_table* t) {
+    if (!t) return XPIR_OK;
+    DeviceGuard g(t->device);
+    cudaStreamSynchronize(t->stream);
+    table_free_all(t);
+    delete t;
+    return XPIR_OK;
+}
+
+int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2,
+                                const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
+                                void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+    if (n == 0) return XPIR_OK;
+    if (!d_b1 || !d_b2 || !d_payload) return fail(XPIR_EINVAL, "table_insert: null buffer");
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    t->h.batch_id += 1;
+    t->h.n_touched = 0;
+    uint64_t i = 0;
+    for (int guard = 0; i < n; ++guard) {
+        if (t->h.draw_count - (t->h.rng_block - t->h.draw_base) < 1024 || guard == 0) {
+            // (re)fill the draw window starting at the next unconsumed nonce
+            t->h.draw_base = t->h.rng_block;
+            t->h.draw_count = DRAW_CAP;
+            XCK(launch_draws(t->seed, t->h.draw_base, DRAW_CAP, t->d.draws, s));
+            count_launches(1);
+        }
+        XCK(cudaMemcpyAsync(t->dstate, &t->h, sizeof(CuckooState), cudaMemcpyHostToDevice, s));
+        XCK(launch_cuckoo_walk(t->d, t->dstate, d_b1, d_b2, i, n, d_reports, s));
+        count_launches(1);
+        XCK(cudaMemcpyAsync(&t->h, t->dstate, sizeof(CuckooState), cudaMemcpyDeviceToHost, s));
+        XCK(cudaStreamSynchronize(s));
+        if (t->h.status == 2) return fail(XPIR_ESTATE, "table_insert: FIFO ring overflow");
+        if (t->h.resume_at <= i && t->h.status != 1)
+            return fail(XPIR_ESTATE, "table_insert: walk made no progress");
+        i = t->h.resume_at;
+        if (t->h.status == 1) t->h.draw_count = 0;  // force a refill
+    }
+    XCK(t->gather.ensure(uint64_t(t->h.n_touched) * t->d.item));
+    t->d.gather = t->gather.as<uint8_t>();
+    XCK(launch_cuckoo_apply(t->d, &t->h, t->data, d_payload, s));
+    count_launches(2);
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b2,
+                            const uint8_t* payload, uint64_t n, uint32_t* reports) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+    if (n == 0) return XPIR_OK;
+    if (!b1 || !b2 || !payload) return fail(XPIR_EINVAL, "table_insert: null buffer");
+    // cuckoo.cpp:57-58 — validated per item in order; items before the bad one
+    // are inserted, exactly as a loop of Table::insert calls would leave them.
+    uint64_t ok = n;
+    for (uint64_t k = 0; k < n; ++k)
+        if (b1[k] >= t->d.buckets || b2[k] >= t->d.buckets) {
+            ok = k;
+            break;
+        }
+    std::lock_guard<std::mutex> lk(t->mu);
+    DeviceGuard g(t->device);
+    cudaStream_t s = t->stream;
+    if (ok > 0) {
+        XCK(t->in_b1.ensure(4 * ok));
+        XCK(t->in_b2.ensure(4 * ok));
+        XCK(t->in_payload.ensure(ok * t->d.item));
+        XCK(t->in_reports.ensure(16 * ok));
+        XCK(cudaMemcpyAsync(t->in_b1.p, b1, 4 * ok, cudaMemcpyHostToDevice, s));
+        XCK(cudaMemcpyAsync(t->in_b2.p, b2, 4 * ok, cudaMemcpyHostToDevice, s));
+        XCK(cudaMemcpyAsync(t->in_payload.p, payload, ok * t->d.item, cudaMemcpyHostToDevice, s));
+        int rc = xpir_table_insert_batch_dev(t, t->in_b1.as<uint32_t>(), t->in_b2.as<uint32_t>(),
+                                             t->in_payload.as<uint8_t>(), ok,
+                                             t->in_reports.as<uint32_t>(), s);
+        if (rc) return rc;
+        if (reports)
+            XCK(cudaMemcpyAsync(reports, t->in_reports.p, 16 * ok, cudaMemcpyDeviceToHost, s));
+        XCK(cudaStreamSynchronize(s));
+    }
+    if (ok < n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
+    return XPIR_OK;
+}
+
+int xpir_table_snapshot(const xpir_table* t, uint8_t* host_out) {
+    if (!t || !host_out) return fail(XPIR_EINVAL, "table_snapshot: null argument");
+    DeviceGuard g(t->device);
+    XCK(cudaStreamSynchronize(t->stream));
+    XCK(cudaMemcpy(host_out, t->data, t->slots() * t->d.item, cudaMemcpyDeviceToHost));
+    return XPIR_OK;
+}
+
+void* xpir_table_device_data(const xpir_table* t) { return t ? t->data : nullptr; }
+
+int xpir_table_seal(const xpir_table* t, xpir_store* st, uint64_t epoch, void* stream) {
+    if (!t || !st) return fail(XPIR_EINVAL, "table_seal: null argument");
+    if (st->N != t->d.buckets || uint64_t(st->S) != uint64_t(t->d.depth) * t->d.item)
+        return fail(XPIR_EINVAL, "table_seal: store geometry differs from the table");
+    if (st->device != t->device) return fail(XPIR_EINVAL, "table_seal: different devices");
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    XCK(cudaMemcpyAsync(st->data, t->data + uint64_t(st->lo) * st->S, st->bytes(),
+                        cudaMemcpyDeviceToDevice, s));
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    st->epoch = epoch;
+    return XPIR_OK;
+}
+
+int xpir_table_meta(const xpir_table* t, uint8_t* used, uint32_t* b1, uint32_t* b2,
+                    uint64_t* stamp) {
+    if (!t) return fail(XPIR_EINVAL, "table_meta: null table");
+    DeviceGuard g(t->device);
+    XCK(cudaStreamSynchronize(t->stream));
+    const uint64_t n = t->slots();
+    if (used) XCK(cudaMemcpy(used, t->d.used, n, cudaMemcpyDeviceToHost));
+    if (b1) XCK(cudaMemcpy(b1, t->d.beta1, 4 * n, cudaMemcpyDeviceToHost));
+    if (b2) XCK(cudaMemcpy(b2, t->d.beta2, 4 * n, cudaMemcpyDeviceToHost));
+    if (stamp) XCK(cudaMemcpy(stamp, t->d.stamp, 8 * n, cudaMemcpyDeviceToHost));
+    return XPIR_OK;
+}
+
+int xpir_table_counters(const xpir_table* t, uint64_t* writes, uint64_t* live, uint64_t* next_stamp) {
+    if (!t) return fail(XPIR_EINVAL, "table_counters: null table");
+    if (writes) *writes = t->h.writes;
+    if (live) *live = t->h.live;
+    if (next_stamp) *next_stamp = t->h.next_stamp;
+    return XPIR_OK;
+}
+
+int xpir_table_slot_used(const xpir_table* t, uint32_t bucket, uint32_t slot) {
+    if (!t || bucket >= t->d.buckets || slot >= t->d.depth)
+        return fail(XPIR_EINVAL, "slot_used: out of range");
+    DeviceGuard g(t->device);
+    uint8_t u = 0;
+    XCK(cudaStreamSynchronize(t->stream));
+    XCK(cudaMemcpy(&u, t->d.used + uint64_t(bucket) * t->d.depth + slot, 1, cudaMemcpyDeviceToHost));
+    return u ? 1 : 0;
+}
+
+int xpir_table_state_digest(const xpir_table* t, uint8_t out[32]) {
+    if (!t || !out) return fail(XPIR_EINVAL, "state_digest: null argument");
+    const uint64_t n = t->slots();
+    std::vector<uint8_t> data(n * t->d.item), used(n);
+    std::vector<uint32_t> b1(n), b2(n);
+    std::vector<uint64_t> st(n);
+    int rc = xpir_table_snapshot(t, data.data());
+    if (rc) return rc;
+    rc = xpir_table_meta(t, used.data(), b1.data(), b2.data(), st.data());
+    if (rc) return rc;
+    HostBlake2b h(32);  // cuckoo.cpp:137-149
+    h.update_u64be(t->h.writes);
+    h.update_u64be(t->h.live);
+    h.update_u64be(t->h.next_stamp);
+    h.update(data.data(), data.size());
+    for (uint64_t f = 0; f < n; ++f) {
+        h.update_u64be(used[f] ? 1 : 0);
+        h.update_u64be(uint64_t(b1[f]) << 32 | b2[f]);
+        h.update_u64be(st[f]);
+    }
+    h.final(out);
+    return XPIR_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// interest window
+// ===========================================================================
+struct xpir_window {
+    int device;
+    uint32_t m, h, w;
+    uint64_t base = 0;
+    uint64_t words;
+    std::deque<unsigned long long*> deltas;
+    cudaStream_t stream = nullptr;
+    DevBuf pos, seqs, scratch;
+    std::mutex mu;
+};
+
+extern "C" {
+
+int xpir_window_create(int device, uint32_t m_bits, uint32_t h, uint32_t w, xpir_window** out) {
+    if (!out) return fail(XPIR_EINVAL, "window_create: null out");
+    if (w == 0) return fail(XPIR_EINVAL, "Window: need at least one delta");   // notify.cpp:55
+    if (m_bits == 0 || h == 0) return fail(XPIR_EINVAL, "Window: bad bloom params");  // :56
+    int ndev = 0;
+    XCK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(XPIR_EINVAL, "window_create: bad device");
+    DeviceGuard g(device);
+    auto* win = new xpir_window;
+    win->device = device;
+    win->m = m_bits;
+    win->h = h;
+    win->w = w;
+    win->words = (uint64_t(m_bits) + 63) / 64;
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 8 * win->words);
+    if (e == cudaSuccess) e = cudaMemset(d, 0, 8 * win->words);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&win->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        if (d) cudaFree(d);
+        delete win;
+        return fail(XPIR_ECUDA, cudaGetErrorString(e));
+    }
+    win->deltas.push_back(d);
+    *out = win;
+    return XPIR_OK;
+}
+
+int xpir_window_destroy(xpir_window* win) {
+    if (!win) return XPIR_OK;
+    DeviceGuard g(win->device);
+    cudaStreamSynchronize(win->stream);
+    for (auto* d : win->deltas) cudaFree(d);
+    win->pos.release();
+    win->seqs.release();
+    win->scratch.release();
+    cudaStreamDestroy(win->stream);
+    delete win;
+    return XPIR_OK;
+}
+
+int xpir_window_absorb_dev(xpir_window* win, const uint32_t* d_pos, uint64_t n, void* stream) {
+    if (!win) return fail(XPIR_EINVAL, "window_absorb: null window");
+    if (!n) return XPIR_OK;
+    if (!d_pos) return fail(XPIR_EINVAL, "window_absorb: null buffer");
+    DeviceGuard g(win->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : win->stream;
+    XCK(win->scratch.ensure(16));
+    XCK(launch_absorb(d_pos, n, win->m, win->deltas.back(), win->scratch.as<unsigned long long>(), s));
+    count_launches(2);
+    unsigned long long first_bad = 0;
+    XCK(cudaMemcpyAsync(&first_bad, win->scratch.p, 8, cudaMemcpyDeviceToHost, s));
+    XCK(cudaStreamSynchronize(s));
+    if (first_bad != ~0ull) return fail(XPIR_EINVAL, "Window: position out of range");
+    return XPIR_OK;
+}
+
+int xpir_window_absorb(xpir_window* win, const uint32_t* pos, uint64_t n) {
+    if (!win) return fail(XPIR_EINVAL, "window_absorb: null window");
+    if (!n) return XPIR_OK;
+    if (!pos) return fail(XPIR_EINVAL, "window_absorb: null buffer");
+    std::lock_guard<std::mutex> lk(win->mu);
+    DeviceGuard g(win->device);
+    XCK(win->pos.ensure(4 * n));
+    XCK(cudaMemcpyAsync(win->pos.p, pos, 4 * n, cudaMemcpyHostToDevice, win->stream));
+    return xpir_window_absorb_dev(win, win->pos.as<uint32_t>(), n, win->stream);
+}
+
+int xpir_window_absorb_interest(xpir_window* win, const uint8_t id[16], const uint64_t* seqs,
+                                uint64_t n) {
+    if (!win || !id) return fail(XPIR_EINVAL, "window_absorb_interest: null argument");
+    if (!n) return XPIR_OK;
+    if (!seqs) return fail(XPIR_EINVAL, "window_absorb_interest: null buffer");
+    std::lock_guard<std::mutex> lk(win->mu);
+    DeviceGuard g(win->device);
+    XCK(win->seqs.ensure(8 * n));
+    XCK(cudaMemcpyAsync(win->seqs.p, seqs, 8 * n, cudaMemcpyHostToDevice, win->stream));
+    XCK(launch_interest(id, win->seqs.as<uint64_t>(), n, win->h, win->m, nullptr, win->deltas.back(),
+                        win->stream));
+    count_launches(1);
+    XCK(cudaStreamSynchronize(win->stream));
+    return XPIR_OK;
+}
+
+int xpir_window_rotate(xpir_window* win) {  // notify.cpp:67-73
+    if (!win) return fail(XPIR_EINVAL, "window_rotate: null window");
+    std::lock_guard<std::mutex> lk(win->mu);
+    DeviceGuard g(win->device);
+    unsigned long long* d = nullptr;
+    XCK(cudaMalloc(&d, 8 * win->words));
+    XCK(cudaMemsetAsync(d, 0, 8 * win->words, win->stream));
+    win->deltas.push_back(d);
+    while (win->deltas.size() > win->w) {
+        XCK(cudaStreamSynchronize(win->stream));
+        cudaFree(win->deltas.front());
+        win->deltas.pop_front();
+        win->base++;
+    }
+    return XPIR_OK;
+}
+
+int xpir_window_info(const xpir_window* win, uint64_t* size, uint64_t* base) {
+    if (!win) return fail(XPIR_EINVAL, "window_info: null window");
+    if (size) *size = win->deltas.size();
+    if (base) *base = win->base;
+    return XPIR_OK;
+}
+
+int xpir_window_delta(const xpir_window* win, uint64_t i, uint64_t* out) {
+    if (!win || !out) return fail(XPIR_EINVAL, "window_delta: null argument");
+    if (i >= win->deltas.size()) return fail(XPIR_EINVAL, "window_delta: index out of range");
+    DeviceGuard g(win->device);
+    XCK(cudaStreamSynchronize(win->stream));
+    XCK(cudaMemcpy(out, win->deltas[i], 8 * win->words, cudaMemcpyDeviceToHost));
+    return XPIR_OK;
+}
+
+int xpir_window_digest(const xpir_window* win, uint8_t out[32]) {  // notify.cpp:87-107
+    if (!win || !out) return fail(XPIR_EINVAL, "window_digest: null argument");
+    HostBlake2b h(32);
+    const char* tag = "interest-window-v1";
+    h.update(reinterpret_cast<const uint8_t*>(tag), std::strlen(tag));
+    h.update_u64be(win->m);
+    h.update_u64be(win->h);
+    h.update_u64be(win->w);
+    h.update_u64be(win->base);
+    h.update_u64be(win->deltas.size());
+    std::vector<uint64_t> words(win->words);
+    for (uint64_t i = 0; i < win->deltas.size(); ++i) {
+        int rc = xpir_window_delta(win, i, words.data());
+        if (rc) return rc;
+        h.update(reinterpret_cast<const uint8_t*>(words.data()), 8 * words.size());  // LE words
+    }
+    h.final(out);
+    return XPIR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,638 @@
+// K1/K2/K3/K4 — the PIR read scan on sm_100a.
+//
+// Reference semantics (bit-exact target):
+//   pir::answer_batch (pir.cpp:41-52): out_r = XOR_{j < N : q_r bit j} bucket_j,
+//     bit j = q_r[j/8] >> (j%8) & 1 (pir.hpp:25); bits >= N are ignored.
+//   pir::mask_answer (pir.cpp:65-69): out_r ^= ChaCha20(mask_seed_r, nonce 0)[0:S].
+//   crypto::prng_expand (crypto.cpp:35-45) for seed-expanded query vectors.
+//   pir::reconstruct / combine_masked (pir.cpp:54-73) for the cross-shard reduce.
+//
+// Two scan kernels:
+//   k_scan_m4rm   — batches >= ~128: "four Russians" byte tables. Query byte g of
+//                   request r is exactly the 8-bit selection of buckets 8g..8g+7,
+//                   so per 128-byte column slice the CTA builds the 256-row table
+//                   T_g[x] = XOR_{i: bit i of x} bucket_{8g+i} in shared memory
+//                   (Gray-code order, one XOR per row), and every request does ONE
+//                   16-byte LDS + 4 XORs per 8 buckets instead of 8 masked XORs.
+//                   Shared-memory bandwidth (128 B/clk/SM) is the bound.
+//   k_scan_direct — small batches: stream the shard once through registers and
+//                   XOR 16-byte words under warp-uniform selection bits (HBM bound).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "prims.cuh"
+#include "scan.cuh"
+
+namespace xpir {
+
+// ---------------------------------------------------------------------------
+// small PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// 16-byte cp.async with zero-fill when src_bytes == 0.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
+                 "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(addr), "r"(v));
+}
+__device__ __forceinline__ void red_xor64(uint8_t* p, uint64_t v) {
+    atomicXor(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+}
+
+// ---------------------------------------------------------------------------
+// K1 (large batches): M4RM byte-table scan.
+//
+// CTA = NT threads. Column tile = 128 bytes (32 words) of every bucket. A
+// quarter-warp (8 lanes x 16 B) owns one 128-byte row, so one LDS.128 per
+// quarter-warp phase reads exactly one table row: conflict-free for any index.
+// Thread (warp w, quarter qq, lane8 l) accumulates RPT requests
+//   r_local(i) = (w*RPT + i)*4 + qq,   i < RPT
+// over bytes [c*128 + l*16, +16). Rc = (NT/8)*RPT requests per request tile.
+//
+// Work = (pair p = rt*n_ctiles + c) x (group g < n_groups), flattened; CTA b of a
+// persistent grid takes a contiguous slice, XOR-flushing its accumulators into
+// `out` (atomicXor) whenever it finishes a pair's slice. `out` is pre-set to the
+// mask pad or zero by k_init_out.
+//
+// Shared memory (bytes):
+//   tab [2][256][128]       double-buffered byte table          64 KiB
+//   qs  [2][Rc][16]         query bytes of 16 groups per request 2*Rc*16
+//   dbs [2][128][128]       the 128 buckets (16 groups) column slice 32 KiB
+// ---------------------------------------------------------------------------
+constexpr int M4_CHUNK_G = 16;  // groups per staged chunk
+constexpr int M4_TAB_BYTES = 256 * 128;
+constexpr int M4_DBS_BYTES = M4_CHUNK_G * 8 * 128;
+
+template <int NT, int RPT>
+struct M4Layout {
+    static constexpr int Rc = (NT / 8) * RPT;
+    static constexpr int QS_BYTES = Rc * 16;
+    static constexpr int OFF_TAB = 0;
+    static constexpr int OFF_QS = 2 * M4_TAB_BYTES;
+    static constexpr int OFF_DBS = OFF_QS + 2 * QS_BYTES;
+    static constexpr int SMEM = OFF_DBS + 2 * M4_DBS_BYTES;
+};
+
+template <int NT, int RPT>
+__global__ void __launch_bounds__(NT, 1)
+k_scan_m4rm(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ q,
+            uint64_t q_stride, uint32_t B, uint8_t* __restrict__ out, uint32_t n_ctiles,
+            uint32_t n_groups, uint64_t total_work) {
+    using L = M4Layout<NT, RPT>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int qq = lane >> 3, l8 = lane & 7;
+
+    // table-build role: word column bw, 16-row block bj (rows 16*bj .. 16*bj+15)
+    const int bw = tid & 31;
+    const int bj = (tid >> 5) & 15;  // NT >= 512 -> each (bw, bj) built once per 16 warps
+    const bool builder = tid < 512;
+    const uint32_t hm0 = 0u - ((bj >> 0) & 1u), hm1 = 0u - ((bj >> 1) & 1u);
+    const uint32_t hm2 = 0u - ((bj >> 2) & 1u), hm3 = 0u - ((bj >> 3) & 1u);
+
+    const uint64_t w0 = total_work * blockIdx.x / gridDim.x;
+    const uint64_t w1 = total_work * (blockIdx.x + 1) / gridDim.x;
+
+    uint64_t u = w0;
+    while (u < w1) {
+        const uint32_t p = uint32_t(u / n_groups);
+        const uint32_t gs = uint32_t(u - uint64_t(p) * n_groups);
+        const uint64_t pend = uint64_t(p + 1) * n_groups;
+        const uint32_t ge = uint32_t((w1 < pend ? w1 : pend) - uint64_t(p) * n_groups);
+        u = uint64_t(p) * n_groups + ge;
+        const uint32_t rt = p / n_ctiles, c = p - rt * n_ctiles;
+        const uint32_t r_base = rt * L::Rc;
+
+        uint4 acc[RPT];
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) acc[i] = make_uint4(0, 0, 0, 0);
+
+        // stage chunk kc (16 groups) into buffer b
+        auto stage = [&](uint32_t kc, int b) {
+            // query bytes: Rc rows x 16 bytes
+            const uint32_t qdst = sbase + L::OFF_QS + b * L::QS_BYTES;
+            for (int r = tid; r < L::Rc; r += NT) {
+                const uint32_t rg = r_base + r;
+                const uint8_t* src = q + (rg < B ? uint64_t(rg) * q_stride : 0) + uint64_t(kc) * 16;
+                cp_async16(qdst + r * 16, src, rg < B ? 16u : 0u);
+            }
+            // db: buckets [kc*128, kc*128+128) x 128-byte slice c
+            const uint32_t ddst = sbase + L::OFF_DBS + b * M4_DBS_BYTES;
+            for (int k = tid; k < M4_CHUNK_G * 8 * 8; k += NT) {
+                const uint32_t bl = k >> 3, part = k & 7;
+                const uint32_t bucket = kc * 128 + bl;
+                const uint8_t* src =
+                    db + (bucket < nb ? uint64_t(bucket) * S : 0) + uint64_t(c) * 128 + part * 16;
+                cp_async16(ddst + bl * 128 + part * 16, src, bucket < nb ? 16u : 0u);
+            }
+        };
+
+        const uint32_t kc0 = gs / M4_CHUNK_G, kc1 = (ge + M4_CHUNK_G - 1) / M4_CHUNK_G;
+        stage(kc0, 0);
+        cp_async_commit();
+        int tb = 0;
+        for (uint32_t kc = kc0; kc < kc1; ++kc) {
+            const int b = (kc - kc0) & 1;
+            if (kc + 1 < kc1) {
+                stage(kc + 1, b ^ 1);
+                cp_async_commit();
+                cp_async_wait<1>();
+            } else {
+                cp_async_wait<0>();
+            }
+            __syncthreads();
+            const uint32_t qbuf = sbase + L::OFF_QS + b * L::QS_BYTES;
+            const uint32_t dbuf = sbase + L::OFF_DBS + b * M4_DBS_BYTES;
+            const uint32_t glo = (gs > kc * M4_CHUNK_G ? gs : kc * M4_CHUNK_G) - kc * M4_CHUNK_G;
+            const uint32_t ghi = (ge < kc * M4_CHUNK_G + M4_CHUNK_G ? ge : kc * M4_CHUNK_G + M4_CHUNK_G) -
+                                 kc * M4_CHUNK_G;
+#pragma unroll 1
+            for (uint32_t g4 = glo & ~3u; g4 < ghi; g4 += 4) {
+                uint32_t qw[RPT];
+#pragma unroll
+                for (int i = 0; i < RPT; ++i)
+                    qw[i] = lds32(qbuf + (((warp * RPT + i) * 4 + qq) * 16) + g4);
+#pragma unroll
+                for (int gg = 0; gg < 4; ++gg) {
+                    const uint32_t gl = g4 + gg;
+                    if (gl < glo || gl >= ghi) continue;  // uniform across the CTA
+                    const uint32_t tab = sbase + L::OFF_TAB + tb * M4_TAB_BYTES;
+                    if (builder) {
+                        // T[16*bj + x] = H_bj ^ L_x, L in Gray-code order: one XOR per row.
+                        const uint32_t src = dbuf + gl * 8 * 128 + bw * 4;
+                        const uint32_t b0 = lds32(src + 0 * 128), b1 = lds32(src + 1 * 128);
+                        const uint32_t b2 = lds32(src + 2 * 128), b3 = lds32(src + 3 * 128);
+                        uint32_t h = (lds32(src + 4 * 128) & hm0) ^ (lds32(src + 5 * 128) & hm1) ^
+                                     (lds32(src + 6 * 128) & hm2) ^ (lds32(src + 7 * 128) & hm3);
+                        const uint32_t row0 = tab + (bj * 16) * 128 + bw * 4;
+                        // Gray sequence 0,1,3,2,6,7,5,4,12,13,15,14,10,11,9,8
+                        sts32(row0 + 0 * 128, h);
+                        h ^= b0; sts32(row0 + 1 * 128, h);
+                        h ^= b1; sts32(row0 + 3 * 128, h);
+                        h ^= b0; sts32(row0 + 2 * 128, h);
+                        h ^= b2; sts32(row0 + 6 * 128, h);
+                        h ^= b0; sts32(row0 + 7 * 128, h);
+                        h ^= b1; sts32(row0 + 5 * 128, h);
+                        h ^= b0; sts32(row0 + 4 * 128, h);
+                        h ^= b3; sts32(row0 + 12 * 128, h);
+                        h ^= b0; sts32(row0 + 13 * 128, h);
+                        h ^= b1; sts32(row0 + 15 * 128, h);
+                        h ^= b0; sts32(row0 + 14 * 128, h);
+                        h ^= b2; sts32(row0 + 10 * 128, h);
+                        h ^= b0; sts32(row0 + 11 * 128, h);
+                        h ^= b1; sts32(row0 + 9 * 128, h);
+                        h ^= b0; sts32(row0 + 8 * 128, h);
+                    }
+                    __syncthreads();
+                    const uint32_t rowbase = tab + l8 * 16;
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        const uint32_t idx = (qw[i] >> (8 * gg)) & 0xffu;
+                        const uint4 v = lds128(rowbase + idx * 128);
+                        acc[i].x ^= v.x;
+                        acc[i].y ^= v.y;
+                        acc[i].z ^= v.z;
+                        acc[i].w ^= v.w;
+                    }
+                    tb ^= 1;
+                }
+            }
+            __syncthreads();  // chunk buffers b are re-staged next iteration
+        }
+        // flush
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const uint32_t r = r_base + (warp * RPT + i) * 4 + qq;
+            if (r < B) {
+                uint8_t* o = out + uint64_t(r) * S + uint64_t(c) * 128 + l8 * 16;
+                red_xor64(o, uint64_t(acc[i].y) << 32 | acc[i].x);
+                red_xor64(o + 8, uint64_t(acc[i].w) << 32 | acc[i].z);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1 (small batches): direct select-XOR, 16-byte words, selection bits from
+// 32-bucket query words. Grid: x = column blocks of 128 threads x 16 B,
+// y = bucket splits, z = request tiles of RPT. Each split writes its partial
+// into part[split][B][S] (plain stores), reduced by k_reduce_parts.
+// ---------------------------------------------------------------------------
+template <int RPT>
+__global__ void __launch_bounds__(128)
+k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ q,
+              uint64_t q_stride, uint32_t B, uint8_t* __restrict__ part, uint32_t buckets_per_split) {
+    const uint32_t ncol = S / 16;
+    const uint32_t col = blockIdx.x * 128 + threadIdx.x;
+    const uint32_t split = blockIdx.y;
+    const uint32_t r0 = blockIdx.z * RPT;
+    const uint32_t j0 = split * buckets_per_split;
+    const uint32_t j1 = min(nb, j0 + buckets_per_split);
+    uint4 acc[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) acc[i] = make_uint4(0, 0, 0, 0);
+    const bool active = col < ncol;
+    const uint4* dbw = reinterpret_cast<const uint4*>(db) + col;
+    for (uint32_t jc = j0; jc < j1; jc += 32) {
+        uint32_t qw[RPT];
+        const uint32_t nvalid = min(32u, j1 - jc);
+        const uint32_t vmask = nvalid == 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            uint32_t w = 0;
+            if (r0 + i < B) {
+                const uint8_t* qp = q + uint64_t(r0 + i) * q_stride + (jc >> 3);
+                // jc is a multiple of 8 (split sizes are multiples of 32)
+                const uint32_t nbytes = (nvalid + 7) >> 3;
+#pragma unroll
+                for (uint32_t k = 0; k < 4; ++k)
+                    if (k < nbytes) w |= uint32_t(__ldg(qp + k)) << (8 * k);
+            }
+            qw[i] = w & vmask;
+        }
+        if (!active) continue;
+        uint32_t any = 0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) any |= qw[i];
+#pragma unroll 4
+        for (uint32_t jj = 0; jj < nvalid; ++jj) {
+            const uint4 v = __ldcs(dbw + uint64_t(jc + jj) * ncol);
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const uint32_t m = 0u - ((qw[i] >> jj) & 1u);
+                acc[i].x ^= v.x & m;
+                acc[i].y ^= v.y & m;
+                acc[i].z ^= v.z & m;
+                acc[i].w ^= v.w & m;
+            }
+        }
+        (void)any;
+    }
+    if (!active) return;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        if (r0 + i < B)
+            reinterpret_cast<uint4*>(part + (uint64_t(split) * B + r0 + i) * S)[col] = acc[i];
+    }
+}
+
+// Byte-granular fallback for bucket sizes that are not a multiple of 16 (the
+// reference's own tests use 1-, 8- and 12-byte buckets). One thread per
+// (request, byte).
+__global__ void k_scan_bytes(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S,
+                             const uint8_t* __restrict__ q, uint64_t q_stride, uint32_t B,
+                             uint8_t* __restrict__ out) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= uint64_t(B) * S) return;
+    const uint32_t r = uint32_t(t / S), k = uint32_t(t - uint64_t(r) * S);
+    const uint8_t* qr = q + uint64_t(r) * q_stride;
+    uint8_t acc = 0;
+    for (uint32_t j = 0; j < nb; ++j)
+        if ((qr[j >> 3] >> (j & 7)) & 1) acc ^= db[uint64_t(j) * S + k];
+    out[t] ^= acc;
+}
+
+// out ^= XOR over splits of part[split]
+__global__ void k_reduce_parts(const uint8_t* __restrict__ part, uint32_t nsplit, uint64_t bytes,
+                               uint8_t* __restrict__ out) {
+    const uint64_t n16 = bytes / 16;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint4 a = reinterpret_cast<uint4*>(out)[i];
+        for (uint32_t s = 0; s < nsplit; ++s) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(part + uint64_t(s) * bytes) + i);
+            a.x ^= v.x; a.y ^= v.y; a.z ^= v.z; a.w ^= v.w;
+        }
+        reinterpret_cast<uint4*>(out)[i] = a;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: out[r] = mask pad (prng_expand(mask_seed_r, S)) or zero — applied before
+// the scan XOR-accumulates into it, so the mask costs one write pass.
+// ---------------------------------------------------------------------------
+__global__ void k_init_out(uint8_t* __restrict__ out, uint32_t B, uint32_t S,
+                           const uint8_t* __restrict__ mask_seeds, int xor_into) {
+    const uint32_t nblk = (S + 63) / 64;
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= uint64_t(B) * nblk) return;
+    const uint32_t r = uint32_t(t / nblk), blk = uint32_t(t - uint64_t(r) * nblk);
+    uint32_t ks[16];
+    if (mask_seeds) {
+        ChaChaKey key = chacha_key(mask_seeds + uint64_t(r) * 32, 0);
+        chacha20_block(key, blk, ks);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) ks[k] = 0;
+    }
+    uint8_t* o = out + uint64_t(r) * S + uint64_t(blk) * 64;
+    const uint32_t n = min(64u, S - blk * 64);
+    if (n == 64 && (S % 16) == 0) {
+        uint4* o4 = reinterpret_cast<uint4*>(o);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint4 v = make_uint4(ks[4 * k], ks[4 * k + 1], ks[4 * k + 2], ks[4 * k + 3]);
+            if (xor_into) {
+                const uint4 a = o4[k];
+                v.x ^= a.x; v.y ^= a.y; v.z ^= a.z; v.w ^= a.w;
+            }
+            o4[k] = v;
+        }
+    } else {
+        for (uint32_t k = 0; k < n; ++k) {
+            const uint8_t b = uint8_t(ks[k >> 2] >> (8 * (k & 3)));
+            o[k] = xor_into ? uint8_t(o[k] ^ b) : b;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: query expansion. d_q[r*stride + k] = prng_expand(seed_r)[byte_lo + k].
+// One thread per 64-byte ChaCha20 block of the window.
+// ---------------------------------------------------------------------------
+__global__ void k_expand(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t byte_lo,
+                         uint64_t nbytes, uint8_t* __restrict__ qout, uint64_t stride) {
+    const uint64_t blk_lo = byte_lo / 64, blk_hi = (byte_lo + nbytes + 63) / 64;
+    const uint64_t nblk = blk_hi - blk_lo;
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= uint64_t(B) * nblk) return;
+    const uint32_t r = uint32_t(t / nblk);
+    const uint64_t blk = blk_lo + (t - uint64_t(r) * nblk);
+    ChaChaKey key = chacha_key(seeds + uint64_t(r) * 32, 0);
+    uint32_t ks[16];
+    chacha20_block(key, blk, ks);
+    const uint64_t b0 = blk * 64;
+    uint8_t* o = qout + uint64_t(r) * stride;
+    if (b0 >= byte_lo && b0 + 64 <= byte_lo + nbytes && ((b0 - byte_lo) % 16) == 0 &&
+        (stride % 16) == 0) {
+        uint4* o4 = reinterpret_cast<uint4*>(o + (b0 - byte_lo));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o4[k] = make_uint4(ks[4 * k], ks[4 * k + 1], ks[4 * k + 2], ks[4 * k + 3]);
+    } else {
+        for (int k = 0; k < 64; ++k) {
+            const uint64_t pos = b0 + k;
+            if (pos >= byte_lo && pos < byte_lo + nbytes)
+                o[pos - byte_lo] = uint8_t(ks[k >> 2] >> (8 * (k & 3)));
+        }
+    }
+}
+
+// Copy a window of query bytes into a 16-byte-aligned, padded layout.
+__global__ void k_repack_queries(const uint8_t* __restrict__ q, uint64_t q_stride, uint64_t byte_lo,
+                                 uint64_t nbytes, uint32_t B, uint8_t* __restrict__ dst,
+                                 uint64_t dst_stride) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= uint64_t(B) * dst_stride) return;
+    const uint32_t r = uint32_t(t / dst_stride);
+    const uint64_t k = t - uint64_t(r) * dst_stride;
+    dst[t] = k < nbytes ? q[uint64_t(r) * q_stride + byte_lo + k] : uint8_t(0);
+}
+
+// ---------------------------------------------------------------------------
+// K4: dst ^= XOR_k srcs[k] (srcs may be NVLink peer pointers).
+// ---------------------------------------------------------------------------
+__global__ void k_xor_reduce(uint8_t* __restrict__ dst, const uint8_t* const* __restrict__ srcs,
+                             uint32_t nsrc, uint64_t bytes) {
+    const uint64_t n16 = bytes / 16;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride) {
+        uint4 a = reinterpret_cast<uint4*>(dst)[i];
+        for (uint32_t s = 0; s < nsrc; ++s) {
+            const uint4 v = __ldcv(reinterpret_cast<const uint4*>(srcs[s]) + i);
+            a.x ^= v.x; a.y ^= v.y; a.z ^= v.z; a.w ^= v.w;
+        }
+        reinterpret_cast<uint4*>(dst)[i] = a;
+    }
+    // byte tail
+    if (blockIdx.x == 0) {
+        for (uint64_t k = n16 * 16 + threadIdx.x; k < bytes; k += blockDim.x) {
+            uint8_t a = dst[k];
+            for (uint32_t s = 0; s < nsrc; ++s) a ^= srcs[s][k];
+            dst[k] = a;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Microbenchmarks for the roofline denominators.
+// k_lop3_peak: 8 independent accumulators per thread, acc ^= w & m — exactly the
+// dense select-XOR inner op, one LOP3 each. k_lds_peak: conflict-free LDS.128.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_lop3_peak(uint32_t iters, uint32_t seed, uint32_t* sink) {
+    uint32_t a[8], w[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        a[k] = seed * (k + 1) + threadIdx.x;
+        w[k] = seed ^ (k * 0x9e3779b9u) ^ blockIdx.x;
+    }
+    uint32_t m = 0u - (threadIdx.x & 1u);
+    for (uint32_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                uint32_t out;
+                asm volatile("lop3.b32 %0, %1, %2, %3, 0x78;\n"  // a ^ (w & m)
+                             : "=r"(out)
+                             : "r"(a[k]), "r"(w[k]), "r"(m));
+                a[k] = out;
+            }
+            m = ~m;
+        }
+    }
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x ^= a[k];
+    if (x == 0x12345678u) sink[0] = x;
+}
+
+__global__ void __launch_bounds__(512) k_lds_peak(uint32_t iters, uint32_t* sink) {
+    __shared__ __align__(16) uint4 buf[2048];
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) buf[i] = make_uint4(i, i * 3, i * 5, i * 7);
+    __syncthreads();
+    const uint32_t base = smem_u32(buf) + (threadIdx.x & 7) * 16;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    uint32_t idx = threadIdx.x >> 3;
+    for (uint32_t i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const uint4 v = lds128(base + ((idx + r * 37) & 255) * 128);
+            acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+        }
+        idx += acc.x & 1;
+    }
+    if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x12345678u) sink[0] = acc.x;
+}
+
+cudaError_t run_peak_kernels(int num_sms, double* lop3_per_s, double* smem_bps, cudaStream_t s) {
+    uint32_t* sink = nullptr;
+    cudaError_t e = cudaMalloc(&sink, 16);
+    if (e != cudaSuccess) return e;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float ms = 0;
+    const uint32_t it1 = 4096;
+    const uint32_t grid1 = num_sms * 8;  // 8 x 256 threads per SM = 64 warps
+    k_lop3_peak<<<grid1, 256, 0, s>>>(64, 1, sink);  // warm-up
+    cudaEventRecord(a, s);
+    k_lop3_peak<<<grid1, 256, 0, s>>>(it1, 1, sink);
+    cudaEventRecord(b, s);
+    e = cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    if (lop3_per_s) *lop3_per_s = double(grid1) * 256 * it1 * 16 * 8 / (ms * 1e-3);
+    const uint32_t it2 = 2048, grid2 = num_sms * 2;
+    k_lds_peak<<<grid2, 512, 0, s>>>(64, sink);
+    cudaEventRecord(a, s);
+    k_lds_peak<<<grid2, 512, 0, s>>>(it2, sink);
+    cudaEventRecord(b, s);
+    if (e == cudaSuccess) e = cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    if (smem_bps) *smem_bps = double(grid2) * 512 * it2 * 16 * 16 / (ms * 1e-3);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    return e;
+}
+
+// ---------------------------------------------------------------------------
+// host-side launchers
+// ---------------------------------------------------------------------------
+template <int NT, int RPT>
+static cudaError_t launch_m4(const ScanArgs& a, int ctas_per_sm, int num_sms) {
+    using L = M4Layout<NT, RPT>;
+    cudaError_t e = cudaFuncSetAttribute(k_scan_m4rm<NT, RPT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    if (e != cudaSuccess) return e;
+    const uint32_t n_ctiles = a.S / 128;
+    const uint32_t n_rtiles = (a.B + L::Rc - 1) / L::Rc;
+    const uint32_t n_groups = (a.nb + 7) / 8;
+    const uint64_t total = uint64_t(n_ctiles) * n_rtiles * n_groups;
+    uint64_t grid = uint64_t(num_sms) * (ctas_per_sm > 0 ? ctas_per_sm : 1);
+    // at least ~8 groups of work per CTA
+    const uint64_t max_grid = (total + 7) / 8;
+    if (grid > max_grid) grid = max_grid > 0 ? max_grid : 1;
+    k_scan_m4rm<NT, RPT><<<dim3(uint32_t(grid)), NT, L::SMEM, a.stream>>>(
+        a.db, a.nb, a.S, a.q, a.q_stride, a.B, a.out, n_ctiles, n_groups, total);
+    return cudaGetLastError();
+}
+
+int m4rm_rows_per_tile(int variant) {
+    switch (variant) {
+        case 0: return M4Layout<512, 2>::Rc;
+        case 1: return M4Layout<512, 4>::Rc;
+        case 2: return M4Layout<512, 8>::Rc;
+        default: return M4Layout<512, 16>::Rc;
+    }
+}
+
+cudaError_t launch_scan_m4rm(const ScanArgs& a, int ctas_per_sm, int num_sms) {
+    // choose RPT so that one request tile covers the batch (up to Rc = 1024)
+    if (a.B <= 128) return launch_m4<512, 2>(a, ctas_per_sm, num_sms);
+    if (a.B <= 256) return launch_m4<512, 4>(a, ctas_per_sm, num_sms);
+    if (a.B <= 512) return launch_m4<512, 8>(a, ctas_per_sm, num_sms);
+    return launch_m4<512, 16>(a, ctas_per_sm, num_sms);
+}
+
+cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
+                               uint32_t* nsplit_out) {
+    constexpr int RPT = 8;
+    const uint32_t ncol = a.S / 16;
+    const uint32_t gx = (ncol + 127) / 128;
+    const uint32_t gz = (a.B + RPT - 1) / RPT;
+    // enough CTAs for ~8 per SM, split sizes a multiple of 32 buckets
+    uint64_t want = uint64_t(num_sms) * 8;
+    uint64_t per = uint64_t(gx) * gz;
+    uint32_t nsplit = uint32_t((want + per - 1) / per);
+    const uint32_t max_split = (a.nb + 31) / 32;
+    if (nsplit > max_split) nsplit = max_split;
+    if (nsplit < 1) nsplit = 1;
+    const uint64_t out_bytes = uint64_t(a.B) * a.S;
+    while (nsplit > 1 && uint64_t(nsplit) * out_bytes > part_bytes) nsplit = (nsplit + 1) / 2;
+    uint32_t bps = (a.nb + nsplit - 1) / nsplit;
+    bps = (bps + 31) & ~31u;
+    nsplit = (a.nb + bps - 1) / bps;
+    if (nsplit < 1) nsplit = 1;
+    k_scan_direct<RPT><<<dim3(gx, nsplit, gz), 128, 0, a.stream>>>(a.db, a.nb, a.S, a.q, a.q_stride,
+                                                                    a.B, part, bps);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const uint64_t n16 = out_bytes / 16;
+    uint32_t rg = uint32_t((n16 + 255) / 256);
+    if (rg > uint32_t(num_sms) * 16) rg = uint32_t(num_sms) * 16;
+    if (rg < 1) rg = 1;
+    k_reduce_parts<<<rg, 256, 0, a.stream>>>(part, nsplit, out_bytes, a.out);
+    *nsplit_out = nsplit;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan_bytes(const ScanArgs& a) {
+    const uint64_t n = uint64_t(a.B) * a.S;
+    if (n == 0) return cudaSuccess;
+    k_scan_bytes<<<uint32_t((n + 255) / 256), 256, 0, a.stream>>>(a.db, a.nb, a.S, a.q, a.q_stride,
+                                                                  a.B, a.out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_out(uint8_t* out, uint32_t B, uint32_t S, const uint8_t* mask_seeds,
+                            bool xor_into, cudaStream_t s) {
+    const uint64_t n = uint64_t(B) * ((S + 63) / 64);
+    if (n == 0) return cudaSuccess;
+    k_init_out<<<uint32_t((n + 255) / 256), 256, 0, s>>>(out, B, S, mask_seeds, xor_into ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_expand(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
+                          uint8_t* qout, uint64_t stride, cudaStream_t s) {
+    const uint64_t nblk = (byte_lo + nbytes + 63) / 64 - byte_lo / 64;
+    const uint64_t n = uint64_t(B) * nblk;
+    if (n == 0) return cudaSuccess;
+    k_expand<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qout, stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_repack(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
+                          uint32_t B, uint8_t* dst, uint64_t dst_stride, cudaStream_t s) {
+    const uint64_t n = uint64_t(B) * dst_stride;
+    if (n == 0) return cudaSuccess;
+    k_repack_queries<<<uint32_t((n + 255) / 256), 256, 0, s>>>(q, q_stride, byte_lo, nbytes, B, dst,
+                                                                dst_stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_xor_reduce(uint8_t* dst, const uint8_t* const* d_srcs, uint32_t nsrc,
+                              uint64_t bytes, int num_sms, cudaStream_t s) {
+    if (bytes == 0 || nsrc == 0) return cudaSuccess;
+    uint64_t n16 = bytes / 16 + 1;
+    uint32_t g = uint32_t((n16 + 255) / 256);
+    if (g > uint32_t(num_sms) * 8) g = uint32_t(num_sms) * 8;
+    k_xor_reduce<<<g, 256, 0, s>>>(dst, d_srcs, nsrc, bytes);
+    return cudaGetLastError();
+}
+
+}  // namespace xpir

@@ -1,0 +1,95 @@
+// Launch interfaces of the scan kernels (scan.cu) and write-path kernels (write.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace xpir {
+
+constexpr uint32_t XPIR_MAX_DISPLACEMENTS_DEV = 500;  // cuckoo.hpp:15
+
+// Count of kernels launched through the library (reported as gpu_launches).
+void count_launches(uint64_t n);
+
+struct ScanArgs {
+    const uint8_t* db;   // shard, bucket-major, nb * S bytes
+    uint32_t nb;         // buckets in the shard
+    uint32_t S;          // bucket bytes
+    const uint8_t* q;    // query rows, already offset to the shard's first byte
+    uint64_t q_stride;   // bytes between rows
+    uint32_t B;          // requests
+    uint8_t* out;        // B * S, pre-initialised (zero or mask pad); scan XORs into it
+    cudaStream_t stream;
+};
+
+cudaError_t launch_scan_m4rm(const ScanArgs& a, int ctas_per_sm, int num_sms);
+int m4rm_rows_per_tile(int variant);
+cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
+                               uint32_t* nsplit_out);
+cudaError_t launch_scan_bytes(const ScanArgs& a);
+cudaError_t launch_init_out(uint8_t* out, uint32_t B, uint32_t S, const uint8_t* mask_seeds,
+                            bool xor_into, cudaStream_t s);
+cudaError_t launch_expand(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
+                          uint8_t* qout, uint64_t stride, cudaStream_t s);
+cudaError_t launch_repack(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
+                          uint32_t B, uint8_t* dst, uint64_t dst_stride, cudaStream_t s);
+cudaError_t launch_xor_reduce(uint8_t* dst, const uint8_t* const* d_srcs, uint32_t nsrc,
+                              uint64_t bytes, int num_sms, cudaStream_t s);
+cudaError_t run_peak_kernels(int num_sms, double* lop3_per_s, double* smem_bps, cudaStream_t s);
+
+// write path / generators (write.cu)
+cudaError_t launch_keystream(const uint8_t* key_host32, uint64_t nonce, uint64_t byte_offset,
+                             uint8_t* out, uint64_t len, cudaStream_t s);
+cudaError_t launch_keystream_rows(const uint8_t* key_host32, uint64_t nonce0, uint32_t rows,
+                                  uint64_t len, uint8_t* out, uint64_t row_stride, cudaStream_t s);
+cudaError_t launch_prf(uint64_t k0, uint64_t k1, const uint64_t* in, uint64_t n, uint64_t modulus,
+                       uint64_t* out, cudaStream_t s);
+cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint64_t n, uint32_t h,
+                            uint32_t m_bits, uint32_t* pos_out, unsigned long long* words,
+                            cudaStream_t s);
+cudaError_t launch_bloom_item(const uint8_t* item_dev, uint32_t len, uint32_t h, uint32_t m_bits,
+                              uint32_t* out, cudaStream_t s);
+// scratch: 8 bytes of device memory; on return it holds the index of the first
+// out-of-range position (or ~0); positions before it are absorbed (notify.cpp:60-65).
+cudaError_t launch_absorb(const uint32_t* pos, uint64_t n, uint32_t m_bits,
+                          unsigned long long* words, unsigned long long* scratch, cudaStream_t s);
+cudaError_t launch_draws(const uint8_t* key_host32, uint64_t nonce0, uint32_t count, uint64_t* out,
+                         cudaStream_t s);
+
+// Device-resident cuckoo metadata (one per table).
+struct CuckooDev {
+    uint32_t buckets, depth;
+    uint64_t capacity, item;
+    uint8_t* used;        // [slots]
+    uint32_t* beta1;      // [slots]
+    uint32_t* beta2;      // [slots]
+    uint64_t* stamp;      // [slots]
+    int64_t* origin;      // [slots] payload source of a slot touched this batch
+    uint32_t* touched_mark;  // [slots] batch id that last touched the slot
+    uint32_t* touched;    // [slots] list of touched slots this batch
+    int64_t* fifo;        // ring [fifo_cap] stamp -> flat slot (or -1)
+    uint64_t fifo_cap;    // power of two
+    uint64_t* draws;      // [draw_cap] precomputed DetRng::next_u64 values
+    uint32_t draw_cap;
+    uint8_t* gather;      // [slots*item] staging for moved pre-existing payloads
+};
+
+// Scalars the walk reads and advances (device memory, one struct).
+struct CuckooState {
+    uint64_t writes, live, next_stamp, fifo_head;
+    uint64_t rng_block;       // DetRng fill counter (= next draw's nonce)
+    uint64_t draw_base;       // nonce of draws[0]
+    uint32_t draw_count;      // valid draws in the buffer
+    uint32_t n_touched;
+    uint32_t batch_id;
+    uint32_t status;          // 0 ok, 1 need more draws (resume_at valid), 2 fifo overflow
+    uint64_t resume_at;       // first insert not yet processed
+};
+
+cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32_t* beta1,
+                               const uint32_t* beta2, uint64_t i0, uint64_t n, uint32_t* reports,
+                               cudaStream_t s);
+cudaError_t launch_cuckoo_apply(const CuckooDev& d, const CuckooState* st_host_copy,
+                                uint8_t* table, const uint8_t* payload, cudaStream_t s);
+
+}  // namespace xpir

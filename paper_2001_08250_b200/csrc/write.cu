@@ -1,0 +1,433 @@
+// Write path (K5-K7) and keystream generators on sm_100a.
+//
+//   K5 k_prf          crypto::prf (crypto.cpp:17-33)            SipHash-2-4 + rejection
+//   K6 k_cuckoo_walk  cuckoo::Table::insert (cuckoo.cpp:56-126) sequential metadata walk
+//      k_cuckoo_*     payload gather/scatter of the round          parallel
+//   K7 k_interest     notify::make_interest (notify.cpp:30-35) + Window::absorb
+//                     (notify.cpp:60-65): BLAKE2b positions OR-ed into the delta
+//   k_keystream*      DetRng::fill / prng_expand keystream (rng.cpp:25-31)
+//   k_draws           DetRng::next_u64 of consecutive fill calls (rng.hpp:31-37)
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "prims.cuh"
+#include "scan.cuh"
+
+namespace xpir {
+
+// ---------------------------------------------------------------------------
+// keystream generators
+// ---------------------------------------------------------------------------
+__global__ void k_keystream(ChaChaKey key, uint64_t byte_offset, uint8_t* __restrict__ out,
+                            uint64_t len) {
+    const uint64_t blk_lo = byte_offset / 64;
+    const uint64_t nblk = (byte_offset + len + 63) / 64 - blk_lo;
+    const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nblk; t += stride) {
+        const uint64_t blk = blk_lo + t;
+        uint32_t ks[16];
+        chacha20_block(key, blk, ks);
+        const uint64_t b0 = blk * 64;
+        if (b0 >= byte_offset && b0 + 64 <= byte_offset + len && ((b0 - byte_offset) & 15) == 0 &&
+            (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+            uint4* o4 = reinterpret_cast<uint4*>(out + (b0 - byte_offset));
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                __stcs(o4 + k, make_uint4(ks[4 * k], ks[4 * k + 1], ks[4 * k + 2], ks[4 * k + 3]));
+        } else {
+            for (int k = 0; k < 64; ++k) {
+                const uint64_t p = b0 + k;
+                if (p >= byte_offset && p < byte_offset + len)
+                    out[p - byte_offset] = uint8_t(ks[k >> 2] >> (8 * (k & 3)));
+            }
+        }
+    }
+}
+
+__global__ void k_keystream_rows(ChaChaKey key, uint64_t nonce0, uint32_t rows, uint64_t len,
+                                 uint8_t* __restrict__ out, uint64_t row_stride) {
+    const uint64_t nblk = (len + 63) / 64;
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= uint64_t(rows) * nblk) return;
+    const uint32_t r = uint32_t(t / nblk);
+    const uint64_t blk = t - uint64_t(r) * nblk;
+    ChaChaKey k = key;
+    const uint64_t nonce = nonce0 + r;
+    k.n[0] = uint32_t(nonce);
+    k.n[1] = uint32_t(nonce >> 32);
+    uint32_t ks[16];
+    chacha20_block(k, blk, ks);
+    uint8_t* o = out + uint64_t(r) * row_stride + blk * 64;
+    const uint64_t n = (len - blk * 64) < 64 ? (len - blk * 64) : 64;
+    for (uint64_t i = 0; i < n; ++i) o[i] = uint8_t(ks[i >> 2] >> (8 * (i & 3)));
+}
+
+__global__ void k_draws(ChaChaKey key, uint64_t nonce0, uint32_t count, uint64_t* __restrict__ out) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    ChaChaKey k = key;
+    const uint64_t nonce = nonce0 + t;
+    k.n[0] = uint32_t(nonce);
+    k.n[1] = uint32_t(nonce >> 32);
+    uint32_t ks[16];
+    chacha20_block(k, 0, ks);
+    out[t] = uint64_t(ks[0]) | uint64_t(ks[1]) << 32;
+}
+
+// ---------------------------------------------------------------------------
+// K5 PRF, K7 interest / absorb
+// ---------------------------------------------------------------------------
+__global__ void k_prf(uint64_t k0, uint64_t k1, const uint64_t* __restrict__ in, uint64_t n,
+                      uint64_t modulus, uint64_t* __restrict__ out) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = prf(k0, k1, in[t], modulus);
+}
+
+struct Id16 {
+    uint8_t b[16];
+};
+
+__global__ void k_interest(Id16 id, const uint64_t* __restrict__ seqs, uint64_t n, uint32_t h,
+                           uint32_t m_bits, uint32_t* __restrict__ pos_out,
+                           unsigned long long* __restrict__ words) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n * h) return;
+    const uint64_t w = t / h;
+    const uint32_t k = uint32_t(t - w * h);
+    uint8_t item[24];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) item[i] = id.b[i];
+    const uint64_t seq = seqs[w];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) item[16 + i] = uint8_t(seq >> (56 - 8 * i));  // BE64 (notify.cpp:33)
+    const uint32_t pos = bloom_position(item, 24, k, m_bits);
+    if (pos_out) pos_out[t] = pos;
+    if (words) atomicOr(words + (pos >> 6), 1ull << (pos & 63));
+}
+
+__global__ void k_bloom_item(const uint8_t* __restrict__ item, uint32_t len, uint32_t h,
+                             uint32_t m_bits, uint32_t* __restrict__ out) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < h) out[t] = bloom_position(item, len, t, m_bits);
+}
+
+__global__ void k_absorb_check(const uint32_t* __restrict__ pos, uint64_t n, uint32_t m_bits,
+                               unsigned long long* __restrict__ first_bad) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < n && pos[t] >= m_bits) atomicMin(first_bad, (unsigned long long)t);
+}
+
+__global__ void k_absorb(const uint32_t* __restrict__ pos, uint64_t n,
+                         const unsigned long long* __restrict__ limit,
+                         unsigned long long* __restrict__ words) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < n && t < *limit) atomicOr(words + (pos[t] >> 6), 1ull << (pos[t] & 63));
+}
+
+// ---------------------------------------------------------------------------
+// K6: cuckoo insertion walk. One thread executes the reference's sequential
+// semantics exactly (cuckoo.cpp:56-126); the rest of the CTA mirrors the
+// occupancy bitmap into shared memory first so the common path (free slot in
+// beta1/beta2) never waits on global memory. Payload bytes are not moved here:
+// each touched slot records where its final content comes from (origin) and
+// k_cuckoo_gather/scatter move the bytes in parallel afterwards.
+//   origin >= 0   : payload row `origin` of this batch
+//   origin == -1  : cleared (zero)
+//   origin <= -2  : the pre-batch content of flat slot (-origin - 2)
+// ---------------------------------------------------------------------------
+constexpr uint32_t WALK_SMEM_MAX_SLOTS = 96 * 1024 * 8;  // bit-packed: 96 KiB each map
+constexpr uint32_t WALK_MIN_DRAWS = 640;  // >= 1 + 500 draws of one insert, with slack
+
+__global__ void __launch_bounds__(256)
+k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __restrict__ beta1,
+              const uint32_t* __restrict__ beta2, uint64_t i0, uint64_t n,
+              uint32_t* __restrict__ reports, int use_smem) {
+    extern __shared__ uint32_t sm[];
+    const uint64_t slots = uint64_t(d.buckets) * d.depth;
+    const uint32_t words = uint32_t((slots + 31) / 32);
+    uint32_t* used_bits = sm;
+    uint32_t* touch_bits = sm + words;
+    CuckooState s = *gst;
+    if (use_smem) {
+        for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
+            uint32_t v = 0;
+            for (uint32_t b = 0; b < 32; ++b) {
+                const uint64_t f = uint64_t(w) * 32 + b;
+                if (f < slots && d.used[f]) v |= 1u << b;
+            }
+            used_bits[w] = v;
+            touch_bits[w] = 0;
+        }
+        __syncthreads();
+        for (uint32_t k = threadIdx.x; k < s.n_touched; k += blockDim.x) {
+            const uint32_t f = d.touched[k];
+            atomicOr(&touch_bits[f >> 5], 1u << (f & 31));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+
+    const uint64_t fmask = d.fifo_cap - 1;
+    auto is_used = [&](uint32_t f) -> bool {
+        return use_smem ? ((used_bits[f >> 5] >> (f & 31)) & 1u) : d.used[f] != 0;
+    };
+    auto is_touched = [&](uint32_t f) -> bool {
+        return use_smem ? ((touch_bits[f >> 5] >> (f & 31)) & 1u) : d.touched_mark[f] == s.batch_id;
+    };
+    auto touch = [&](uint32_t f, int64_t org) {
+        if (!is_touched(f)) {
+            if (use_smem) touch_bits[f >> 5] |= 1u << (f & 31);
+            d.touched_mark[f] = s.batch_id;
+            d.touched[s.n_touched++] = f;
+        }
+        d.origin[f] = org;
+    };
+    auto origin_of = [&](uint32_t f) -> int64_t {
+        return is_touched(f) ? d.origin[f] : -int64_t(f) - 2;
+    };
+    auto free_slot = [&](uint32_t b) -> int {  // cuckoo.cpp:31-35
+        for (uint32_t sl = 0; sl < d.depth; ++sl)
+            if (!is_used(b * d.depth + sl)) return int(sl);
+        return -1;
+    };
+    auto place = [&](uint32_t f, uint32_t b1, uint32_t b2, uint64_t stamp, int64_t org) {  // :37-46
+        if (use_smem) used_bits[f >> 5] |= 1u << (f & 31);
+        d.used[f] = 1;
+        d.beta1[f] = b1;
+        d.beta2[f] = b2;
+        d.stamp[f] = stamp;
+        d.fifo[stamp & fmask] = int64_t(f);
+        touch(f, org);
+        s.live++;
+    };
+    auto clear = [&](uint32_t f) {  // :48-54
+        if (use_smem) used_bits[f >> 5] &= ~(1u << (f & 31));
+        d.fifo[d.stamp[f] & fmask] = -1;
+        d.used[f] = 0;
+        d.beta1[f] = 0;
+        d.beta2[f] = 0;
+        d.stamp[f] = 0;
+        touch(f, -1);
+        s.live--;
+    };
+    auto uniform = [&](uint64_t bound) -> uint64_t {  // rng.cpp:9-16 over DetRng::fill draws
+        const uint64_t tail = (~uint64_t(0) % bound + 1) % bound;
+        for (;;) {
+            const uint64_t v = d.draws[s.rng_block - s.draw_base];
+            s.rng_block++;
+            if (tail == 0 || v <= ~uint64_t(0) - tail) return v % bound;
+        }
+    };
+
+    s.status = 0;
+    uint64_t i = i0;
+    uint32_t nb1 = i < n ? beta1[i] : 0, nb2 = i < n ? beta2[i] : 0;
+    for (; i < n; ++i) {
+        const uint32_t b1 = nb1, b2 = nb2;
+        if (i + 1 < n) {  // prefetch the next item's buckets
+            nb1 = beta1[i + 1];
+            nb2 = beta2[i + 1];
+        }
+        if (s.draw_count - (s.rng_block - s.draw_base) < WALK_MIN_DRAWS) {
+            s.status = 1;  // host refills draws from nonce s.rng_block and resumes at i
+            break;
+        }
+        uint32_t stored = 0, dropped = 0, gc = 0, disp = 0;
+        s.writes++;                                 // :62
+        if (s.live == d.capacity) {                 // :64-69 FIFO GC of the oldest entry
+            while (d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
+            clear(uint32_t(d.fifo[s.fifo_head & fmask]));
+            gc = 1;
+        }
+        const uint64_t stamp = s.next_stamp++;     // :71
+        if (stamp - s.fifo_head >= d.fifo_cap) {
+            s.status = 2;
+            break;
+        }
+        int fs = free_slot(b1);                     // :73-84
+        if (fs >= 0) {
+            place(b1 * d.depth + fs, b1, b2, stamp, int64_t(i));
+            stored = 1;
+        } else if ((fs = free_slot(b2)) >= 0) {
+            place(b2 * d.depth + fs, b1, b2, stamp, int64_t(i));
+            stored = 1;
+        } else {                                    // :86-125 random-walk eviction
+            uint32_t be = uniform(2) == 0 ? b1 : b2;
+            uint32_t c1 = b1, c2 = b2;
+            uint64_t cst = stamp;
+            int64_t corg = int64_t(i);
+            bool carry_incoming = true, incoming_stored = false, done = false;
+            for (uint32_t hops = 0;; ++hops) {
+                const int f2 = free_slot(be);
+                if (f2 >= 0) {
+                    place(be * d.depth + f2, c1, c2, cst, corg);
+                    if (carry_incoming) incoming_stored = true;
+                    stored = incoming_stored;
+                    disp = hops;
+                    done = true;
+                    break;
+                }
+                if (hops == XPIR_MAX_DISPLACEMENTS_DEV) break;
+                const uint32_t vs = uint32_t(uniform(d.depth));
+                const uint32_t vf = be * d.depth + vs;
+                const uint32_t v1 = d.beta1[vf], v2 = d.beta2[vf];
+                const uint64_t vst = d.stamp[vf];
+                const int64_t vorg = origin_of(vf);
+                clear(vf);
+                place(vf, c1, c2, cst, corg);
+                if (carry_incoming) incoming_stored = true;
+                c1 = v1;
+                c2 = v2;
+                cst = vst;
+                corg = vorg;
+                carry_incoming = false;
+                be = v1 == be ? v2 : v1;            // :118
+            }
+            if (!done) {                            // :122-125
+                disp = XPIR_MAX_DISPLACEMENTS_DEV;
+                dropped = 1;
+                stored = incoming_stored;
+            }
+        }
+        if (reports) {
+            uint4 r = make_uint4(stored, dropped, gc, disp);
+            reinterpret_cast<uint4*>(reports)[i] = r;
+        }
+    }
+    s.resume_at = i;
+    *gst = s;
+}
+
+// phase 1: stage pre-existing payloads that moved (origin <= -2) into d.gather[k]
+__global__ void k_cuckoo_gather(CuckooDev d, uint32_t n_touched, const uint8_t* __restrict__ table) {
+    const uint32_t k = blockIdx.x;
+    if (k >= n_touched) return;
+    const uint32_t f = d.touched[k];
+    const int64_t o = d.origin[f];
+    if (o > -2) return;
+    const uint64_t src = uint64_t(-o - 2);
+    const uint8_t* s = table + src * d.item;
+    uint8_t* g = d.gather + uint64_t(k) * d.item;
+    if ((d.item & 15) == 0) {
+        for (uint64_t b = threadIdx.x * 16; b < d.item; b += blockDim.x * 16)
+            *reinterpret_cast<uint4*>(g + b) = *reinterpret_cast<const uint4*>(s + b);
+    } else {
+        for (uint64_t b = threadIdx.x; b < d.item; b += blockDim.x) g[b] = s[b];
+    }
+}
+
+// phase 2: write each touched slot's final content
+__global__ void k_cuckoo_scatter(CuckooDev d, uint32_t n_touched, uint8_t* __restrict__ table,
+                                 const uint8_t* __restrict__ payload) {
+    const uint32_t k = blockIdx.x;
+    if (k >= n_touched) return;
+    const uint32_t f = d.touched[k];
+    const int64_t o = d.origin[f];
+    uint8_t* dst = table + uint64_t(f) * d.item;
+    const uint8_t* src = o >= 0 ? payload + uint64_t(o) * d.item
+                        : o == -1 ? nullptr
+                                  : d.gather + uint64_t(k) * d.item;
+    if ((d.item & 15) == 0) {
+        for (uint64_t b = threadIdx.x * 16; b < d.item; b += blockDim.x * 16)
+            *reinterpret_cast<uint4*>(dst + b) =
+                src ? *reinterpret_cast<const uint4*>(src + b) : make_uint4(0, 0, 0, 0);
+    } else {
+        for (uint64_t b = threadIdx.x; b < d.item; b += blockDim.x) dst[b] = src ? src[b] : 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static ChaChaKey host_key(const uint8_t* key32, uint64_t nonce) { return chacha_key(key32, nonce); }
+
+cudaError_t launch_keystream(const uint8_t* key_host32, uint64_t nonce, uint64_t byte_offset,
+                             uint8_t* out, uint64_t len, cudaStream_t s) {
+    if (len == 0) return cudaSuccess;
+    const uint64_t nblk = (byte_offset + len + 63) / 64 - byte_offset / 64;
+    uint64_t g = (nblk + 255) / 256;
+    if (g > 148 * 64) g = 148 * 64;
+    k_keystream<<<uint32_t(g), 256, 0, s>>>(host_key(key_host32, nonce), byte_offset, out, len);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_keystream_rows(const uint8_t* key_host32, uint64_t nonce0, uint32_t rows,
+                                  uint64_t len, uint8_t* out, uint64_t row_stride, cudaStream_t s) {
+    const uint64_t n = uint64_t(rows) * ((len + 63) / 64);
+    if (n == 0) return cudaSuccess;
+    k_keystream_rows<<<uint32_t((n + 127) / 128), 128, 0, s>>>(host_key(key_host32, 0), nonce0, rows,
+                                                               len, out, row_stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_draws(const uint8_t* key_host32, uint64_t nonce0, uint32_t count, uint64_t* out,
+                         cudaStream_t s) {
+    if (!count) return cudaSuccess;
+    k_draws<<<(count + 127) / 128, 128, 0, s>>>(host_key(key_host32, 0), nonce0, count, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prf(uint64_t k0, uint64_t k1, const uint64_t* in, uint64_t n, uint64_t modulus,
+                       uint64_t* out, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    k_prf<<<uint32_t((n + 127) / 128), 128, 0, s>>>(k0, k1, in, n, modulus, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint64_t n, uint32_t h,
+                            uint32_t m_bits, uint32_t* pos_out, unsigned long long* words,
+                            cudaStream_t s) {
+    const uint64_t t = n * h;
+    if (!t) return cudaSuccess;
+    Id16 id;
+    std::memcpy(id.b, id16_host, 16);
+    k_interest<<<uint32_t((t + 127) / 128), 128, 0, s>>>(id, seqs, n, h, m_bits, pos_out, words);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bloom_item(const uint8_t* item_dev, uint32_t len, uint32_t h, uint32_t m_bits,
+                              uint32_t* out, cudaStream_t s) {
+    if (!h) return cudaSuccess;
+    k_bloom_item<<<(h + 127) / 128, 128, 0, s>>>(item_dev, len, h, m_bits, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_absorb(const uint32_t* pos, uint64_t n, uint32_t m_bits,
+                          unsigned long long* words, unsigned long long* first_bad, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    const unsigned long long init = ~0ull;
+    cudaError_t e = cudaMemcpyAsync(first_bad, &init, 8, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    const uint32_t g = uint32_t((n + 255) / 256);
+    k_absorb_check<<<g, 256, 0, s>>>(pos, n, m_bits, first_bad);
+    k_absorb<<<g, 256, 0, s>>>(pos, n, first_bad, words);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32_t* beta1,
+                               const uint32_t* beta2, uint64_t i0, uint64_t n, uint32_t* reports,
+                               cudaStream_t s) {
+    const uint64_t slots = uint64_t(d.buckets) * d.depth;
+    const bool use_smem = slots <= WALK_SMEM_MAX_SLOTS;
+    const size_t smem = use_smem ? 2 * ((slots + 31) / 32) * 4 : 0;
+    if (use_smem && smem > 48 * 1024) {
+        cudaError_t e =
+            cudaFuncSetAttribute(k_cuckoo_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    k_cuckoo_walk<<<1, 256, smem, s>>>(d, st, beta1, beta2, i0, n, reports, use_smem ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cuckoo_apply(const CuckooDev& d, const CuckooState* st, uint8_t* table,
+                                const uint8_t* payload, cudaStream_t s) {
+    if (!st->n_touched) return cudaSuccess;
+    const uint32_t thr = d.item >= 1024 ? 64 : 32;
+    k_cuckoo_gather<<<st->n_touched, thr, 0, s>>>(d, st->n_touched, table);
+    k_cuckoo_scatter<<<st->n_touched, thr, 0, s>>>(d, st->n_touched, table, payload);
+    return cudaGetLastError();
+}
+
+}  // namespace xpir

@@ -1,0 +1,110 @@
+"""Bucket-range sharding of one logical PIR server over the GPUs of one box
+(the paper defers this).
+
+One process per GPU (torchrun). Rank g holds buckets [lo_g, hi_g) (multiples of
+8, so every shard reads whole query bytes) and produces a partial answer for
+every request; answers are XOR-linear, so the full answer is the XOR of the
+partials — the reference's ``pir::reconstruct`` / leader ``contribute``
+semantics (pir.cpp:54-73, node.cpp:350-378). NCCL has no XOR reduction, so the
+exchange is our own: every rank maps its peers' partial buffers through CUDA IPC
+(NVLink / NVSwitch peer loads) and the K4 kernel XOR-reduces the rows it owns
+(reduce-scatter: rank g owns requests [g*B/G, (g+1)*B/G)). The mask pad (K3) is
+applied exactly once, after the reduce, by the owner.
+
+Control plane (handle exchange, barriers) goes through ``torch.distributed``; the
+data plane is peer memory only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """Contiguous bucket ranges and request-row ownership for G shards."""
+
+    buckets: int
+    world: int
+
+    def bucket_range(self, rank: int) -> tuple[int, int]:
+        groups = (self.buckets + 7) // 8
+        lo = (groups * rank // self.world) * 8
+        hi = (groups * (rank + 1) // self.world) * 8
+        return lo, min(hi, self.buckets)
+
+    def row_range(self, rank: int, batch: int) -> tuple[int, int]:
+        return batch * rank // self.world, batch * (rank + 1) // self.world
+
+    def ranges(self):
+        return [self.bucket_range(r) for r in range(self.world)]
+
+
+def xor_reduce_scatter_reference(partials: list[np.ndarray], plan: ShardPlan, rank: int) -> np.ndarray:
+    """Host model of what rank `rank` ends with after the exchange (used by the
+    CPU gloo tests to check the plan; never called on the product path)."""
+    B = partials[0].shape[0]
+    r0, r1 = plan.row_range(rank, B)
+    acc = partials[rank][r0:r1].copy()
+    for g, p in enumerate(partials):
+        if g != rank:
+            acc ^= p[r0:r1]
+    return acc
+
+
+class ShardedScan:
+    """Per-rank driver: local shard scan + peer XOR reduce-scatter (+ mask)."""
+
+    def __init__(self, xp, torch, dist, N: int, S: int, B: int, device: int):
+        self.xp, self.torch, self.dist = xp, torch, dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.plan = ShardPlan(N, self.world)
+        self.N, self.S, self.B, self.device = N, S, B, device
+        lo, hi = self.plan.bucket_range(self.rank)
+        self.store = xp.Store(N, S, lo, hi, device=device)
+        self.partial = torch.empty((B, S), dtype=torch.uint8, device=f"cuda:{device}")
+        self.r0, self.r1 = self.plan.row_range(self.rank, B)
+        self.peers: list[int] = []
+        self.src_ptrs = None
+        self._exchange_handles()
+
+    def _exchange_handles(self):
+        xp, torch, dist = self.xp, self.torch, self.dist
+        h = xp.ipc_handle(self.partial.data_ptr(), self.device)
+        handles: list = [None] * self.world
+        dist.all_gather_object(handles, h)
+        self.peer_base = []
+        for g, hg in enumerate(handles):
+            if g == self.rank:
+                continue
+            self.peer_base.append(xp.ipc_open(hg, self.device))
+        row = self.r0 * self.S
+        ptrs = [p + row for p in self.peer_base]
+        self.src_ptrs = torch.tensor(ptrs if ptrs else [0], dtype=torch.int64, device=f"cuda:{self.device}")
+        self.nsrc = len(ptrs)
+
+    def close(self):
+        for p in self.peer_base:
+            self.xp.ipc_close(p, self.device)
+        self.peer_base = []
+        self.store.close()
+
+    def step(self, d_seeds, stream=None, d_mask=None):
+        """One batch: partial scan of this shard, barrier, reduce own rows from
+        peers, barrier. Returns the view of this rank's final rows."""
+        xp, torch, dist = self.xp, self.torch, self.dist
+        self.store.answer_batch_seeded_dev(d_seeds, self.B, self.partial, stream=stream)
+        own = self.partial[self.r0:self.r1]
+        if self.world > 1:
+            torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
+            dist.barrier()
+            xp.xor_reduce_dev(own, [0] * self.nsrc, (self.r1 - self.r0) * self.S, device=self.device,
+                              stream=stream, d_ptr_array=self.src_ptrs)
+        if d_mask is not None:
+            xp.mask_dev(own, d_mask[self.r0:self.r1], self.r1 - self.r0, self.S, device=self.device,
+                        stream=stream)
+        if self.world > 1:
+            torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
+            dist.barrier()  # peers finished reading our partial before it is overwritten
+        return own

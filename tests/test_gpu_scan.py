@@ -1,0 +1,243 @@
+"""GPU parity: the sm_100a scan path (K1 direct + M4RM, K2 expansion, K3 mask,
+K4 XOR reduce) against the oracle and the golden fixtures written from the
+unmodified reference. Integer work: every comparison is bit-exact."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import recipes
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def rand(g, *shape):
+    return g.integers(0, 256, shape, dtype=np.uint8)
+
+
+@pytest.fixture(autouse=True)
+def _auto_kernel(xp):
+    xp.set_scan_opts(0)
+    yield
+    xp.set_scan_opts(0)
+
+
+# --- reference unit-test known answers (test_pir.cpp) -----------------------------
+def test_tiny_known_db(xp, cuda):
+    st = xp.Store(3, 1)
+    st.upload(np.array([0x0F, 0xF0, 0xAA], np.uint8))
+    out = st.answer_batch(np.array([[0b101], [0], [0b10]], np.uint8))
+    assert out[:, 0].tolist() == [0xA5, 0x00, 0xF0]
+    with pytest.raises(xp.InvalidArgument):
+        st.answer_batch(np.array([[0]], np.uint8), q_bits=4)  # test_pir.cpp:107-108
+
+
+def test_full_retrieval_every_target(xp, port, cuda):
+    # test_pir.cpp:117-131 on a 64 x 12-byte DB, and acceptance #1 shapes
+    for N, S in ((64, 12), (8, 1), (256, 4), (64, 16)):
+        g = port.detrng(23)
+        db = np.frombuffer(g.fill(N * S), np.uint8)
+        st = xp.Store(N, S)
+        st.upload(db)
+        for beta in range(N):
+            qs = g.gen_queries(beta, N, 3)
+            ans = st.answer_batch(qs)
+            assert np.array_equal(ans, port.answer_batch(db, N, S, qs, 3))
+            assert np.array_equal(np.bitwise_xor.reduce(ans, axis=0), db.reshape(N, S)[beta])
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("N,S,B", [
+    (8, 128, 1), (9, 128, 3), (1000, 256, 97), (1024, 4096, 64), (777, 512, 130),
+    (4096, 128, 1), (2048, 1024, 513), (4000, 2048, 1025), (256, 32768, 40), (12345, 128, 300),
+])
+def test_scan_matches_oracle(xp, port, cuda, kernel, N, S, B):
+    g = np.random.default_rng(N * 7 + S + B)
+    db = rand(g, N * S)
+    q = rand(g, B, (N + 7) // 8)
+    xp.set_scan_opts(kernel)
+    st = xp.Store(N, S)
+    st.upload(db)
+    got = st.answer_batch(q)
+    want = port.answer_batch(db, N, S, q, B)
+    assert np.array_equal(got, want)
+    if kernel == 2 and S % 128 == 0:
+        assert xp.last_scan_kernel() == 2
+
+
+def test_dirty_trailing_bits_are_ignored(xp, port, cuda):
+    # pir::answer only reads bits j < N (pir.cpp:33-34)
+    N, S, B = 1001, 256, 200
+    g = np.random.default_rng(5)
+    db = rand(g, N * S)
+    q = rand(g, B, (N + 7) // 8)
+    q[:, -1] |= 0xFE
+    st = xp.Store(N, S)
+    st.upload(db)
+    for k in (1, 2):
+        xp.set_scan_opts(k)
+        assert np.array_equal(st.answer_batch(q), port.answer_batch(db, N, S, q, B))
+
+
+def test_empty_and_zero_queries(xp, cuda):
+    st = xp.Store(64, 128)
+    st.upload(np.full(64 * 128, 0xAB, np.uint8))
+    assert st.answer_batch(np.zeros((0, 8), np.uint8)).shape == (0, 128)
+    assert not st.answer_batch(np.zeros((300, 8), np.uint8)).any()
+    ones = st.answer_batch(np.full((300, 8), 0xFF, np.uint8))
+    assert not ones.any()  # 64 identical buckets XOR to zero
+
+
+def test_mask_fused(xp, port, cuda):
+    N, S, B = 2048, 512, 257
+    g = np.random.default_rng(9)
+    db, q, ms = rand(g, N * S), rand(g, B, N // 8), rand(g, B, 32)
+    st = xp.Store(N, S)
+    st.upload(db)
+    plain = port.answer_batch(db, N, S, q, B)
+    for k in (1, 2):
+        xp.set_scan_opts(k)
+        got = st.answer_batch(q, mask_seeds=ms)
+        for r in range(0, B, 37):
+            assert got[r].tobytes() == port.mask_answer(plain[r].tobytes(), ms[r].tobytes())
+
+
+def test_seeded_expansion(xp, port, cuda):
+    N, S, B = 4096, 1024, 150
+    g = np.random.default_rng(11)
+    db, seeds = rand(g, N * S), rand(g, B, 32)
+    q = np.stack([np.frombuffer(port.prng_expand(s.tobytes(), N // 8), np.uint8) for s in seeds])
+    st = xp.Store(N, S)
+    st.upload(db)
+    assert np.array_equal(st.answer_batch_seeded(seeds), port.answer_batch(db, N, S, q, B))
+
+
+def test_primitives(xp, port, golden, cuda):
+    P = golden["primitives"]
+    for e in P["prng_expand"]:
+        assert xp.prng_expand(bytes.fromhex(e["seed"]), e["n"]).hex() == e["out"]
+    for e in P["prf"]:
+        assert xp.prf_batch(bytes.fromhex(e["key"]), e["x"], e["m"]).tolist() == e["out"]
+    for e in P["bloom"]:
+        assert xp.bloom_positions(bytes.fromhex(e["item"]), e["h"], e["m"]) == e["out"]
+    for e in P["interest"]:
+        got = xp.make_interest_batch(e["m"], e["h"], bytes.fromhex(e["id"]), [e["seq"]])
+        assert got[0].tolist() == e["out"]
+    for e in P["blake2b"]:
+        assert xp.blake2b(bytes.fromhex(e["in"]), e["outlen"]).hex() == e["out"]
+
+
+def test_keystream_generators(xp, port, cuda):
+    torch = cuda
+    key = bytes(range(32))
+    for off, n in ((0, 1), (5, 100), (64, 4096), (1000, 777)):
+        d = torch.empty(n, dtype=torch.uint8, device="cuda")
+        xp.keystream_dev(key, 9, d, n, byte_offset=off)
+        torch.cuda.synchronize()
+        want = port.chacha20(key, (9).to_bytes(8, "little"), off + n)[off:]
+        assert d.cpu().numpy().tobytes() == want
+    rows = torch.zeros((7, 48), dtype=torch.uint8, device="cuda")
+    xp.keystream_rows_dev(key, 3, 7, 40, rows, 48)
+    torch.cuda.synchronize()
+    g = port.detrng(key)
+    for r in range(3):
+        g.fill(0)
+    for r in range(7):
+        assert rows[r, :40].cpu().numpy().tobytes() == g.fill(40)
+        assert not rows[r, 40:].cpu().numpy().any()
+
+
+def test_config1_golden(xp, port, golden, cuda):
+    db, q = recipes.config1(port)
+    st = xp.Store(1024, 4096)
+    st.upload(db)
+    for k in (0, 1, 2):
+        xp.set_scan_opts(k)
+        out = st.answer_batch(q)
+        assert out[0, :8].tobytes().hex() == "877147f881293508"
+        assert sha(out) == golden["config1"]["out_sha256"]
+
+
+def test_config2_three_server_round(xp, port, golden, cuda):
+    db, betas, shares = recipes.config2(port)
+    G = golden["config2"]
+    assert sha(db) == G["db_sha256"] and sha(shares) == G["shares_sha256"]
+    st = xp.Store(32768, 4096)
+    st.upload(db)
+    outs = [st.answer_batch(shares[s]) for s in range(3)]
+    for s in range(3):
+        assert sha(outs[s]) == G["out_sha256"][s]
+    assert np.array_equal(outs[0] ^ outs[1] ^ outs[2], db.reshape(32768, 4096)[betas])
+
+
+def test_virtual_shards_xor_reduce(xp, port, cuda):
+    """Bucket-range shards on one GPU + the K4 XOR reduce == the unsharded scan."""
+    torch = cuda
+    N, S, B = 8192, 512, 333
+    g = np.random.default_rng(21)
+    db, q = rand(g, N * S), rand(g, B, N // 8)
+    want = port.answer_batch(db, N, S, q, B)
+    dq = torch.from_numpy(q).cuda()
+    for G in (2, 3, 8):
+        bounds = [((N // 8) * k // G) * 8 for k in range(G)] + [N]
+        parts = []
+        for k in range(G):
+            lo, hi = bounds[k], bounds[k + 1]
+            st = xp.Store(N, S, lo, hi)
+            st.upload(db[lo * S: hi * S])
+            o = torch.empty((B, S), dtype=torch.uint8, device="cuda")
+            st.answer_batch_dev(dq, N // 8, B, o)
+            torch.cuda.synchronize()
+            parts.append((st, o))
+        acc = parts[0][1].clone()
+        ptrs = torch.tensor([p[1].data_ptr() for p in parts[1:]], dtype=torch.int64, device="cuda")
+        xp.xor_reduce_dev(acc, [p[1].data_ptr() for p in parts[1:]], B * S, d_ptr_array=ptrs)
+        torch.cuda.synchronize()
+        assert np.array_equal(acc.cpu().numpy(), want)
+
+
+def test_linearity_large(xp, cuda):
+    """Size-independent property at 1 GiB: answer(a ^ b) == answer(a) ^ answer(b)."""
+    torch = cuda
+    N, S, B = 1 << 18, 4096, 256
+    st = xp.Store(N, S)
+    st.fill_keystream(bytes(range(32)), 1)
+    g = np.random.default_rng(3)
+    a, b = rand(g, B, N // 8), rand(g, B, N // 8)
+    qa = st.answer_batch(a)
+    qb = st.answer_batch(b)
+    qab = st.answer_batch(a ^ b)
+    assert np.array_equal(qab, qa ^ qb)
+    # unit vectors read buckets back exactly
+    e = np.zeros((4, N // 8), np.uint8)
+    idx = [0, 1, N - 1, 123457]
+    for r, j in enumerate(idx):
+        e[r, j // 8] |= 1 << (j % 8)
+    got = st.answer_batch(e)
+    full = st.download().reshape(N, S)
+    for r, j in enumerate(idx):
+        assert np.array_equal(got[r], full[j])
+
+
+@pytest.mark.slow
+def test_config4_sample_golden(xp, port, golden, cuda):
+    """Full 4 GiB store generated on device; first 8 seeded requests vs the
+    reference outputs in golden.json; store windows spot-checked."""
+    torch = cuda
+    N, S = recipes.C4["N"], recipes.C4["S"]
+    key = xp.blake2b((3).to_bytes(8, "little"), 32)
+    st = xp.Store(N, S)
+    st.fill_keystream(key, 0)
+    G = golden["config4"]
+    for w in G["store_windows"]:
+        assert sha(st.download(w["off"], 65536)) == w["sha256"]
+    seeds = np.stack([np.frombuffer(bytes.fromhex(h), np.uint8) for h in G["seeds_hex"]])
+    assert np.array_equal(seeds, recipes.config4_seeds(port, 8))
+    for k in (1, 2):
+        xp.set_scan_opts(k)
+        out = st.answer_batch_seeded(seeds)
+        assert [sha(out[r]) for r in range(8)] == G["out_rows_sha256"]

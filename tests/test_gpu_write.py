@@ -1,0 +1,158 @@
+"""GPU parity of the write path: cuckoo insertion/eviction/GC/drop (K6), PRF (K5)
+and the interest-window Bloom update (K7) against the reference digests."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import recipes
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _compare_tables(T, P):
+    used, b1, b2, st = T.meta()
+    pu, pb1, pb2, pst = P.meta()
+    assert np.array_equal(used, pu)
+    assert np.array_equal(b1, pb1) and np.array_equal(b2, pb2) and np.array_equal(st, pst)
+    assert np.array_equal(T.snapshot(), P.data())
+    assert T.counters() == P.counters()
+    assert T.state_digest() == P.state_digest()
+
+
+def test_config3_write_round(xp, port, golden, cuda):
+    n = recipes.C3["n"]
+    d = recipes.config3(port, n)
+    G = golden["config3"][str(n)]
+    T = xp.Table(32768, 4, 32768 * 4, 1024, d["s_cuckoo"])
+    rep = T.insert_batch(d["b1"], d["b2"], d["payload"])
+    assert sha(rep) == G["reports_sha256"]
+    assert T.state_digest().hex() == G["state_digest"]
+    assert sha(T.snapshot()) == G["table_sha256"]
+    W = xp.Window(1 << 20, 23, 1)
+    W.absorb(d["pos"].ravel())
+    assert W.digest().hex() == G["window_digest"]
+    # fused make_interest + absorb on device gives the same filter
+    W2 = xp.Window(1 << 20, 23, 1)
+    W2.absorb_interest(d["lid"], d["xs"])
+    assert W2.digest().hex() == G["window_digest"]
+    # beta computation on device (K5)
+    assert np.array_equal(xp.prf_batch(d["k1"], d["xs"], 32768).astype(np.uint32), d["b1"])
+    assert np.array_equal(xp.prf_batch(d["k2"], d["xs"], 32768).astype(np.uint32), d["b2"])
+
+
+def test_config3_95pct_load(xp, port, golden, cuda):
+    n = recipes.C3["n95"]
+    d = recipes.config3(port, n)
+    G = golden["config3"][str(n)]
+    T = xp.Table(32768, 4, 32768 * 4, 1024, d["s_cuckoo"])
+    rep = T.insert_batch(d["b1"], d["b2"], d["payload"])
+    assert int(rep[:, 3].sum()) == G["displacements"]
+    assert sha(rep) == G["reports_sha256"]
+    assert T.state_digest().hex() == G["state_digest"]
+
+
+def test_multi_batch_rounds_match_single_pass(xp, port, golden, cuda):
+    """Rounds of writes (draw-window refills, resumed walks, moved pre-existing
+    payloads) leave exactly the state of one long insert sequence."""
+    n = recipes.C3["n95"]
+    d = recipes.config3(port, n)
+    T = xp.Table(32768, 4, 32768 * 4, 1024, d["s_cuckoo"])
+    cuts = [0, 1, 5000, 32000, 90000, 100001, n]
+    for a, b in zip(cuts, cuts[1:]):
+        T.insert_batch(d["b1"][a:b], d["b2"][a:b], d["payload"][a:b])
+    assert T.state_digest().hex() == golden["config3"][str(n)]["state_digest"]
+
+
+def test_adversarial_gc_and_drops(xp, port, golden, cuda):
+    for e in golden["cuckoo_adversarial"]:
+        g = port.detrng(e["rng_seed"])
+        s = g.fill(32)
+        n, nb = e["n"], e["buckets"]
+        b1 = np.array([g.uniform(nb) for _ in range(n)], np.uint32)
+        b2 = np.array([g.uniform(nb) for _ in range(n)], np.uint32)
+        pl = np.frombuffer(g.fill(n * 8), np.uint8).reshape(n, 8)
+        T = xp.Table(nb, e["depth"], e["capacity"], 8, s)
+        P = port.table(nb, e["depth"], e["capacity"], 8, s)
+        # one item per call and all-at-once must agree with the reference
+        rep = np.concatenate([T.insert_batch(b1[i:i + 1], b2[i:i + 1], pl[i:i + 1]) for i in range(n)])
+        P.insert_batch(b1, b2, pl)
+        assert rep.tolist() == e["reports"]
+        assert T.state_digest().hex() == e["state_digest"]
+        _compare_tables(T, P)
+
+
+def test_random_tables_vs_oracle(xp, port, cuda):
+    g = np.random.default_rng(77)
+    for nb, depth, cap, n, item in ((5, 2, 10, 300, 16), (64, 4, 200, 2000, 32), (7, 3, 21, 500, 12),
+                                    (1000, 8, 8000, 9000, 64)):
+        seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+        b1 = g.integers(0, nb, n).astype(np.uint32)
+        b2 = g.integers(0, nb, n).astype(np.uint32)
+        pl = g.integers(0, 256, (n, item), dtype=np.uint8)
+        T, P = xp.Table(nb, depth, cap, item, seed), port.table(nb, depth, cap, item, seed)
+        for a in range(0, n, 97):
+            assert np.array_equal(T.insert_batch(b1[a:a + 97], b2[a:a + 97], pl[a:a + 97]),
+                                  P.insert_batch(b1[a:a + 97], b2[a:a + 97], pl[a:a + 97]))
+        _compare_tables(T, P)
+
+
+def test_cuckoo_reference_unit_cases(xp, cuda):
+    z = bytes(32)
+    # test_cuckoo.cpp:42-59 — beta1 wins ties, lowest free slot first
+    T = xp.Table(4, 2, 8, 4, z)
+    T.insert(1, 2, b"aaaa")
+    T.insert(1, 2, b"bbbb")
+    assert T.slot_used(1, 0) and T.slot_used(1, 1) and not T.slot_used(2, 0)
+    T.insert(1, 2, b"cccc")
+    assert T.slot_used(2, 0)
+    snap = T.snapshot().reshape(4, 2, 4)
+    assert bytes(snap[1, 0]) == b"aaaa" and bytes(snap[1, 1]) == b"bbbb" and bytes(snap[2, 0]) == b"cccc"
+    # test_cuckoo.cpp:82-89 — no GC below capacity; empty slots are zero (177-193)
+    assert not snap[0].any() and not snap[3].any()
+    # out-of-range bucket: items before the bad one are applied, then EINVAL
+    with pytest.raises(xp.InvalidArgument):
+        T.insert_batch([0, 9], [0, 0], np.zeros(8, np.uint8))
+    assert T.writes_applied() == 4
+    with pytest.raises(xp.InvalidArgument):
+        T.insert_batch([0], [0], np.zeros(5, np.uint8))  # item size mismatch
+
+
+def test_window_rotate_and_range(xp, port, cuda):
+    for w in (1, 2, 3):
+        A, B = xp.Window(1000, 3, w), port.window(1000, 3, w)
+        g = np.random.default_rng(w)
+        for step in range(7):
+            pos = g.integers(0, 1000, 20).astype(np.uint32)
+            A.absorb(pos)
+            B.absorb(pos)
+            if step % 2:
+                A.rotate()
+                B.rotate()
+            assert A.digest() == B.digest()
+            assert A.size() == B.size()
+        with pytest.raises(xp.InvalidArgument):
+            A.absorb([5, 1000, 7])
+        with pytest.raises(ValueError):
+            B.absorb([5, 1000, 7])
+        assert A.digest() == B.digest()  # prefix before the bad position absorbed, as the reference
+
+
+def test_seal_into_store_and_read(xp, port, cuda):
+    """apply_write rounds then seal (server.cpp:58-81) and read it back via PIR."""
+    d = recipes.config3(port, 2000)
+    T = xp.Table(32768, 4, 32768 * 4, 1024, d["s_cuckoo"])
+    T.insert_batch(d["b1"], d["b2"], d["payload"])
+    st = xp.Store(32768, 4096)
+    T.seal(st, epoch=1)
+    snap = T.snapshot().reshape(32768, 4096)
+    q = np.zeros((3, 4096), np.uint8)
+    for r, b in enumerate(d["b1"][:3]):
+        q[r, b // 8] |= 1 << (b % 8)
+    got = st.answer_batch(q)
+    for r, b in enumerate(d["b1"][:3]):
+        assert np.array_equal(got[r], snap[b])

@@ -1,0 +1,204 @@
+"""CPU tests: pin the C restatement (oracle/xpir_oracle.c) against the reference's
+own known answers and against tests/golden/golden.json (written from the
+unmodified reference build), and — where the reference build loads — against
+the reference directly on fresh seeded inputs."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import recipes
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# --- SURVEY.md Appendix A anchors ----------------------------------------------
+def test_anchor_chacha(port):
+    assert port.prng_expand(b"\0" * 32, 32).hex() == \
+        "76b8e0ada0f13d90405d6ae55386bd28bdd219b8a08ded1aa836efcc8b770dc7"
+    assert port.prng_expand(b"\0" * 32, 128)[64:96].hex() == \
+        "9f07e7be5551387a98ba977c732d080dcb0f29a048e3656912c6533e32ee7aed"
+
+
+def test_anchor_detrng(port):
+    assert port.blake2b((0).to_bytes(8, "little")).hex() == \
+        "81e47a19e6b29b0a65b9591762ce5143ed30d0261e5d24a3201752506b20f15c"
+    g = port.detrng(0)
+    assert g.fill(32).hex() == "e4396463ea1d616ac0810110d26bf1c6b524e5524e88e920dc9c0007b4f69678"
+    assert g.fill(16).hex() == "658960f18e9c1a4411a1f7804a36a4f5"
+
+
+def test_anchor_prf_bloom(port):
+    k = bytes(range(16))
+    assert port.prf(k, 1, 32768) == 28290
+    assert port.prf(k, 2, 1000) == 70
+    assert port.prf(k, 0, 2**64 - 1) == 10998023115641288449
+    assert port.bloom_positions(b"item", 4, 2**20) == [1000919, 291022, 880130, 102005]
+
+
+# --- golden primitives ------------------------------------------------------------
+def test_golden_primitives(port, golden):
+    P = golden["primitives"]
+    for e in P["prng_expand"]:
+        assert port.prng_expand(bytes.fromhex(e["seed"]), e["n"]).hex() == e["out"]
+    for e in P["blake2b"]:
+        assert port.blake2b(bytes.fromhex(e["in"]), e["outlen"]).hex() == e["out"]
+    for e in P["prf"]:
+        key = bytes.fromhex(e["key"])
+        assert [port.prf(key, x, e["m"]) for x in e["x"]] == e["out"]
+    for e in P["bloom"]:
+        assert port.bloom_positions(bytes.fromhex(e["item"]), e["h"], e["m"]) == e["out"]
+    for e in P["interest"]:
+        assert port.make_interest(e["m"], e["h"], bytes.fromhex(e["id"]), e["seq"]).tolist() == e["out"]
+    for e in P["detrng"]:
+        assert recipes.detrng_key(port, e["seed"]).hex() == e["key"]
+        g = port.detrng(e["seed"])
+        assert g.fill(32).hex() == e["fill32"]
+        assert g.fill(16).hex() == e["fill16"]
+        assert g.next_u64() == e["u64"]
+        assert [g.uniform(b) for b in (2, 3, 4, 1000, 32768)] == e["uniform"]
+    bh = golden["bloom_hash_count"]
+    assert port.bloom_hash_count(bh["m"], bh["n"]) == bh["h"] == 23
+
+
+# --- pir (test_pir.cpp known answers) ------------------------------------------------
+def test_tiny_known_db(port, golden):
+    db = np.array([0x0F, 0xF0, 0xAA], np.uint8)
+    q = np.array([[0b101], [0], [0b10]], np.uint8)
+    out = port.answer_batch(db, 3, 1, q, 3)
+    assert out[:, 0].tolist() == [0xA5, 0x00, 0xF0]
+    assert bytes(out[0]).hex() == golden["tiny"]["q02"]
+    with pytest.raises(ValueError):
+        port.answer_batch(db, 3, 1, q, 3, q_bits=4)  # test_pir.cpp:107-108
+
+
+def test_query_bit_layout(port):
+    # test_pir.cpp:33-43: set(0), set(9) -> {0x01, 0x02}; a 16-bucket one-byte DB
+    db = np.arange(16, dtype=np.uint8)
+    out = port.answer_batch(db, 16, 1, np.array([[0x01, 0x02]], np.uint8), 1)
+    assert out[0, 0] == 0 ^ 9
+
+
+def test_gen_queries_xor_to_unit(port):
+    g = port.detrng(5)
+    for b in (3, 8, 64, 129):
+        for l in (2, 3, 5):
+            qs = g.gen_queries(b // 2, b, l)
+            acc = np.bitwise_xor.reduce(qs, axis=0)
+            bits = np.unpackbits(acc, bitorder="little")[:b]
+            assert bits.tolist() == [int(j == b // 2) for j in range(b)]
+    with pytest.raises(ValueError):
+        g.gen_queries(5, 4, 3)
+
+
+def test_config1_golden(port, golden):
+    db, q = recipes.config1(port)
+    G = golden["config1"]
+    assert sha(db) == G["db_sha256"] and sha(q) == G["q_sha256"]
+    out = port.answer_batch(db, 1024, 4096, q, 64)
+    assert out[0, :8].tobytes().hex() == G["out0_first8"] == "877147f881293508"
+    assert sha(out) == G["out_sha256"]
+
+
+def test_config2_golden_subset(port, golden):
+    db, betas, shares = recipes.config2(port, B=16)
+    G = golden["config2"]
+    assert sha(db) == G["db_sha256"]
+    assert betas[:8].tolist() == G["betas_first8"]
+    outs = [port.answer_batch(db, 32768, 4096, shares[s], 16) for s in range(3)]
+    for s in range(3):
+        assert [sha(outs[s][r]) for r in range(16)] == G["out_rows_sha256_first16"][s]
+    assert np.array_equal(outs[0] ^ outs[1] ^ outs[2], db.reshape(32768, 4096)[betas])
+
+
+def test_mask_roundtrip(port):
+    g = port.detrng(37)
+    ans = g.fill(2048)
+    seed = g.fill(32)
+    m = port.mask_answer(ans, seed)
+    assert port.mask_answer(m, seed) == ans
+    assert m != ans
+
+
+# --- cuckoo + window (config 3) -----------------------------------------------------
+def test_config3_golden(port, golden):
+    n = recipes.C3["n"]
+    d = recipes.config3(port, n)
+    G = golden["config3"][str(n)]
+    T = port.table(32768, 4, 32768 * 4, 1024, d["s_cuckoo"])
+    W = port.window(1 << 20, 23, 1)
+    rep = T.insert_batch(d["b1"], d["b2"], d["payload"])
+    W.absorb(d["pos"].ravel())
+    assert T.state_digest().hex() == G["state_digest"]
+    assert W.digest().hex() == G["window_digest"]
+    assert sha(rep) == G["reports_sha256"]
+
+
+@pytest.mark.slow
+def test_config3_95pct_golden(port, golden):
+    n = recipes.C3["n95"]
+    d = recipes.config3(port, n)
+    G = golden["config3"][str(n)]
+    T = port.table(32768, 4, 32768 * 4, 1024, d["s_cuckoo"])
+    rep = T.insert_batch(d["b1"], d["b2"], d["payload"])
+    assert int(rep[:, 3].sum()) == G["displacements"] == 115607
+    assert T.state_digest().hex() == G["state_digest"]
+
+
+def test_cuckoo_adversarial_golden(port, golden):
+    for e in golden["cuckoo_adversarial"]:
+        g = port.detrng(e["rng_seed"])
+        s = g.fill(32)
+        n, nb = e["n"], e["buckets"]
+        b1 = np.array([g.uniform(nb) for _ in range(n)], np.uint32)
+        b2 = np.array([g.uniform(nb) for _ in range(n)], np.uint32)
+        pl = np.frombuffer(g.fill(n * 8), np.uint8).reshape(n, 8)
+        T = port.table(nb, e["depth"], e["capacity"], 8, s)
+        rep = T.insert_batch(b1, b2, pl)
+        assert rep.tolist() == e["reports"]
+        assert T.state_digest().hex() == e["state_digest"]
+        assert T.data().tobytes().hex() == e["data"]
+    # the set exercises GC and the 500-displacement drop
+    allrep = np.concatenate([np.array(e["reports"]) for e in golden["cuckoo_adversarial"]])
+    assert allrep[:, 2].sum() > 0 and allrep[:, 1].sum() > 0 and (allrep[:, 3] == 500).any()
+
+
+def test_window_rotation_matches_reference(port, ref):
+    for w in (1, 2, 3):
+        A, B = port.window(1000, 3, w), ref.window(1000, 3, w)
+        g = np.random.default_rng(w)
+        for step in range(7):
+            pos = g.integers(0, 1000, 20).astype(np.uint32)
+            A.absorb(pos)
+            B.absorb(pos)
+            if step % 2:
+                A.rotate()
+                B.rotate()
+            assert A.digest() == B.digest()
+        with pytest.raises(ValueError):
+            A.absorb([1000])
+        with pytest.raises(ValueError):
+            B.absorb([1000])
+
+
+# --- restatement vs the reference on fresh random inputs --------------------------------
+def test_port_vs_reference_scan(port, ref):
+    g = np.random.default_rng(1)
+    for N, S, B in ((1, 1, 1), (3, 1, 3), (64, 12, 7), (1000, 16, 33), (257, 40, 5)):
+        db = g.integers(0, 256, N * S, dtype=np.uint8)
+        q = g.integers(0, 256, (B, (N + 7) // 8), dtype=np.uint8)
+        assert np.array_equal(port.answer_batch(db, N, S, q, B), ref.answer_batch(db, N, S, q, B))
+
+
+def test_port_vs_reference_cuckoo(port, ref):
+    g = np.random.default_rng(2)
+    for nb, depth, cap, n in ((5, 2, 10, 80), (32, 4, 100, 400), (7, 3, 21, 90)):
+        seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+        b1 = g.integers(0, nb, n).astype(np.uint32)
+        b2 = g.integers(0, nb, n).astype(np.uint32)
+        pl = g.integers(0, 256, (n, 16), dtype=np.uint8)
+        A, B = port.table(nb, depth, cap, 16, seed), ref.table(nb, depth, cap, 16, seed)
+        assert np.array_equal(A.insert_batch(b1, b2, pl), B.insert_batch(b1, b2, pl))
+        assert A.state_digest() == B.state_digest()
