@@ -170,6 +170,7 @@ def run_reference(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 def main():
+    global N_BUCKETS
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -179,7 +180,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 direct, 2 m4rm")
+    ap.add_argument("--buckets", type=int, default=N_BUCKETS,
+                    help="store buckets (profiling runs only; the bench line uses config 4)")
+    ap.add_argument("--quick", action="store_true", help="timed steps only (for ncu)")
     args = ap.parse_args()
+    N_BUCKETS = args.buckets
     if args.impl == "reference":
         return run_reference(args)
 
@@ -201,7 +206,8 @@ def main():
     from paper_2001_08250_b200.sharded import ShardedScan, ShardPlan
 
     plan = ShardPlan(N_BUCKETS, world)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a real stream handle (not the legacy default stream)
+    torch.cuda.set_stream(stream)
     if world > 1:
         sh = ShardedScan(xp, torch, dist, N_BUCKETS, BUCKET_BYTES, B, local)
         store = sh.store
@@ -252,6 +258,12 @@ def main():
     ms_per_step = ms / args.steps
     value = B / (ms_per_step * 1e-3)
 
+    if args.quick:
+        if rank == 0:
+            print(json.dumps({"quick": True, "ms_per_step": ms_per_step, "value": value,
+                              "scan_ms_per_launch": scan_ms / max(scan_launches, 1),
+                              "kernel": xp.last_scan_kernel(), "buckets": N_BUCKETS}), flush=True)
+        return 0
     # e2e through the C-ABI host call (host seeds -> device -> host answers)
     e2e = None
     if world == 1:

@@ -172,9 +172,10 @@ def _ptr(x) -> int | None:
 def _stream(s) -> int | None:
     if s is None:
         return None
-    if isinstance(s, int):
-        return s
-    return s.cuda_stream  # torch.cuda.Stream
+    h = s if isinstance(s, int) else s.cuda_stream  # torch.cuda.Stream
+    # handle 0 is the legacy default stream; NULL would select the library's own
+    # stream, so pass cudaStreamLegacy (0x1) to keep ordering with the caller.
+    return h if h else 1
 
 
 def launch_count() -> int:

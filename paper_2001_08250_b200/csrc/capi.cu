@@ -772,7 +772,7 @@ int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint3
     t->h.n_touched = 0;
     uint64_t i = 0;
     for (int guard = 0; i < n; ++guard) {
-        if (t->h.draw_count - (t->h.rng_block - t->h.draw_base) < 1024 || guard == 0) {
+        if (t->h.rng_block + 1024 > t->h.draw_base + t->h.draw_count || guard == 0) {
             // (re)fill the draw window starting at the next unconsumed nonce
             t->h.draw_base = t->h.rng_block;
             t->h.draw_count = DRAW_CAP;

@@ -230,7 +230,7 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
             nb1 = beta1[i + 1];
             nb2 = beta2[i + 1];
         }
-        if (s.draw_count - (s.rng_block - s.draw_base) < WALK_MIN_DRAWS) {
+        if (s.rng_block + WALK_MIN_DRAWS > s.draw_base + s.draw_count) {
             s.status = 1;  // host refills draws from nonce s.rng_block and resumes at i
             break;
         }
