@@ -378,41 +378,49 @@ uint64_t xpir_query_window_bytes(const xpir_store* st) {
 
 }  // extern "C"
 
-// Core dispatch: d_qwin rows hold the shard window (byte 0 = query byte lo/8),
-// 16-byte aligned with stride % 16 == 0 and >= round16(window) readable bytes.
-static int scan_window(xpir_store* st, const uint8_t* d_qwin, uint64_t stride, bool aligned,
-                       uint32_t B, const uint8_t* d_mask, uint8_t* d_out, cudaStream_t s) {
-    XCK(launch_init_out(d_out, B, st->S, d_mask, false, s));
-    count_launches(1);
-    if (B == 0) return XPIR_OK;
-    int kernel;
+// ---------------------------------------------------------------------------
+// Scan dispatch. Kernel choice: 2 = M4RM (S % 128 == 0, B >= 128; group-major
+// queries), 1 = direct select-XOR (S % 16 == 0; row-major query window),
+// 3 = byte-granular (any S).
+// ---------------------------------------------------------------------------
+static int choose_kernel(const xpir_store* st, uint32_t B) {
+    int k;
     {
         std::lock_guard<std::mutex> lk(g_opts_mu);
-        kernel = g_opts.kernel;
+        k = g_opts.kernel;
     }
-    const bool m4_ok = (st->S % 128) == 0 && aligned;
-    if (kernel == 0) kernel = (m4_ok && B >= 96) ? 2 : 1;
-    if (kernel == 2 && !m4_ok) kernel = 1;
-    ScanArgs a{st->data, st->nb(), st->S, d_qwin, stride, B, d_out, s};
-    const int sms = num_sms(st->device);
-    if (st->S % 16 != 0) {
+    if (st->S % 16 != 0) return 3;
+    const bool m4_ok = (st->S % 128) == 0;
+    if (k == 0) k = (m4_ok && B >= 128) ? 2 : 1;
+    if (k == 2 && !m4_ok) k = 1;
+    return k;
+}
+
+static int run_m4(xpir_store* st, const uint8_t* qT, uint64_t qstride, uint32_t B, uint8_t* d_out,
+                  cudaStream_t s) {
+    int cps;
+    {
+        std::lock_guard<std::mutex> lk(g_opts_mu);
+        cps = g_opts.ctas_per_sm;
+    }
+    M4Args a{st->data, st->nb(), st->S, qT, qstride, B, d_out, s};
+    cudaEvent_t ev;
+    timing_begin(s, &ev);
+    XCK(launch_scan_m4rm(a, cps, num_sms(st->device)));
+    timing_end(s, ev);
+    count_launches(1);
+    g_last_kernel = 2;
+    return XPIR_OK;
+}
+
+// qwin: row-major query rows already offset to the shard's first byte.
+static int run_rows(xpir_store* st, int kernel, const uint8_t* qwin, uint64_t stride, uint32_t B,
+                    uint8_t* d_out, cudaStream_t s) {
+    ScanArgs a{st->data, st->nb(), st->S, qwin, stride, B, d_out, s};
+    if (kernel == 3) {
         XCK(launch_scan_bytes(a));
         count_launches(1);
         g_last_kernel = 3;
-        return XPIR_OK;
-    }
-    if (kernel == 2) {
-        int cps;
-        {
-            std::lock_guard<std::mutex> lk(g_opts_mu);
-            cps = g_opts.ctas_per_sm;
-        }
-        cudaEvent_t ev;
-        timing_begin(s, &ev);
-        XCK(launch_scan_m4rm(a, cps, sms));
-        timing_end(s, ev);
-        count_launches(1);
-        g_last_kernel = 2;
         return XPIR_OK;
     }
     // direct: partial buffer sized for up to 64 splits, capped at 256 MiB
@@ -423,26 +431,27 @@ static int scan_window(xpir_store* st, const uint8_t* d_qwin, uint64_t stride, b
     uint32_t nsplit = 0;
     cudaEvent_t ev;
     timing_begin(s, &ev);
-    XCK(launch_scan_direct(a, st->part.as<uint8_t>(), st->part.cap, sms, &nsplit));
+    XCK(launch_scan_direct(a, st->part.as<uint8_t>(), st->part.cap, num_sms(st->device), &nsplit));
     timing_end(s, ev);
     count_launches(2);
     g_last_kernel = 1;
     return XPIR_OK;
 }
 
-// Full-row device queries -> aligned window (zero-copy when already aligned).
-static int scan_rows_dev(xpir_store* st, const uint8_t* d_q, uint64_t q_stride, uint32_t B,
-                         const uint8_t* d_mask, uint8_t* d_out, cudaStream_t s) {
-    const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
-    const uint8_t* qw = d_q + blo;
-    const bool aligned = (reinterpret_cast<uintptr_t>(qw) % 16) == 0 && (q_stride % 16) == 0 &&
-                         (q_stride - blo) >= round16(nbw);
-    if (aligned || (st->S % 128) != 0) return scan_window(st, qw, q_stride, aligned, B, d_mask, d_out, s);
-    const uint64_t ws = round16(nbw) + 16;
-    XCK(st->qwin.ensure(ws * B));
-    XCK(launch_repack(d_q, q_stride, blo, nbw, B, st->qwin.as<uint8_t>(), ws, s));
+// Row-major query rows (device; `rows` points at row 0 byte 0 of the FULL vector).
+static int scan_rows(xpir_store* st, const uint8_t* rows, uint64_t stride, uint32_t B,
+                     const uint8_t* d_mask, uint8_t* d_out, cudaStream_t s) {
+    XCK(launch_init_out(d_out, B, st->S, d_mask, false, s));
     count_launches(1);
-    return scan_window(st, st->qwin.as<uint8_t>(), ws, true, B, d_mask, d_out, s);
+    if (B == 0) return XPIR_OK;
+    const int k = choose_kernel(st, B);
+    const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
+    if (k != 2) return run_rows(st, k, rows + blo, stride, B, d_out, s);
+    const uint64_t qs = m4rm_qstride(B);
+    XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
+    XCK(launch_transpose_q(rows, stride, blo, nbw, B, st->qwin.as<uint8_t>(), qs, s));
+    count_launches(1);
+    return run_m4(st, st->qwin.as<uint8_t>(), qs, B, d_out, s);
 }
 
 extern "C" {
@@ -456,7 +465,7 @@ int xpir_answer_batch_dev(xpir_store* st, const uint8_t* d_q, uint64_t q_stride,
         return fail(XPIR_EINVAL, "answer_batch: query stride shorter than the vector");
     DeviceGuard g(st->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
-    return scan_rows_dev(st, d_q, q_stride, B, d_mask, d_out, s);
+    return scan_rows(st, d_q, q_stride, B, d_mask, d_out, s);
 }
 
 int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_t B,
@@ -465,12 +474,25 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
     if (B && (!d_seeds || !d_out)) return fail(XPIR_EINVAL, "answer_batch_seeded: null buffer");
     DeviceGuard g(st->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
-    const uint64_t ws = xpir_query_window_bytes(st);
-    XCK(st->qwin.ensure(ws * std::max<uint32_t>(B, 1)));
-    // K2: expand only this shard's window of every request's selection vector
-    XCK(launch_expand(d_seeds, B, st->byte_lo(), st->nbytes_window(), st->qwin.as<uint8_t>(), ws, s));
+    XCK(launch_init_out(d_out, B, st->S, d_mask, false, s));
     count_launches(1);
-    return scan_window(st, st->qwin.as<uint8_t>(), ws, true, B, d_mask, d_out, s);
+    if (B == 0) return XPIR_OK;
+    const int k = choose_kernel(st, B);
+    const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
+    // K2: expand only this shard's window of every request's selection vector,
+    // straight into the layout the chosen scan kernel reads.
+    if (k == 2) {
+        const uint64_t qs = m4rm_qstride(B);
+        XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
+        XCK(launch_expand_T(d_seeds, B, blo, nbw, st->qwin.as<uint8_t>(), qs, s));
+        count_launches(1);
+        return run_m4(st, st->qwin.as<uint8_t>(), qs, B, d_out, s);
+    }
+    const uint64_t ws = xpir_query_window_bytes(st);
+    XCK(st->qwin.ensure(ws * B));
+    XCK(launch_expand(d_seeds, B, blo, nbw, st->qwin.as<uint8_t>(), ws, s));
+    count_launches(1);
+    return run_rows(st, k, st->qwin.as<uint8_t>(), ws, B, d_out, s);
 }
 
 int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint32_t q_bits,
@@ -487,8 +509,7 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
     const uint64_t ws = round16(nbw) + 16;
     XCK(st->q.ensure(ws * B));
-    // H2D of the shard's window of every row (pitched copy), zero padding tail
-    XCK(cudaMemsetAsync(st->q.p, 0, ws * B, s));
+    // H2D of the shard's window of every row (pitched copy); rows start at byte 0
     XCK(cudaMemcpy2DAsync(st->q.p, ws, q + blo, q_stride, nbw, B, cudaMemcpyHostToDevice, s));
     const uint8_t* dm = nullptr;
     if (mask_seeds) {
@@ -498,7 +519,20 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
     }
     const uint64_t ob = uint64_t(B) * st->S;
     XCK(st->out.ensure(ob));
-    int rc = scan_window(st, st->q.as<uint8_t>(), ws, true, B, dm, st->out.as<uint8_t>(), s);
+    uint8_t* dout = st->out.as<uint8_t>();
+    XCK(launch_init_out(dout, B, st->S, dm, false, s));
+    count_launches(1);
+    const int k = choose_kernel(st, B);
+    int rc;
+    if (k == 2) {
+        const uint64_t qs = m4rm_qstride(B);
+        XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
+        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s));
+        count_launches(1);
+        rc = run_m4(st, st->qwin.as<uint8_t>(), qs, B, dout, s);
+    } else {
+        rc = run_rows(st, k, st->q.as<uint8_t>(), ws, B, dout, s);
+    }
     if (rc) return rc;
     XCK(cudaMemcpyAsync(out, st->out.p, ob, cudaMemcpyDeviceToHost, s));
     XCK(cudaStreamSynchronize(s));

@@ -62,181 +62,6 @@ __device__ __forceinline__ void red_xor64(uint8_t* p, uint64_t v) {
 }
 
 // ---------------------------------------------------------------------------
-// K1 (large batches): M4RM byte-table scan.
-//
-// CTA = NT threads. Column tile = 128 bytes (32 words) of every bucket. A
-// quarter-warp (8 lanes x 16 B) owns one 128-byte row, so one LDS.128 per
-// quarter-warp phase reads exactly one table row: conflict-free for any index.
-// Thread (warp w, quarter qq, lane8 l) accumulates RPT requests
-//   r_local(i) = (w*RPT + i)*4 + qq,   i < RPT
-// over bytes [c*128 + l*16, +16). Rc = (NT/8)*RPT requests per request tile.
-//
-// Work = (pair p = rt*n_ctiles + c) x (group g < n_groups), flattened; CTA b of a
-// persistent grid takes a contiguous slice, XOR-flushing its accumulators into
-// `out` (atomicXor) whenever it finishes a pair's slice. `out` is pre-set to the
-// mask pad or zero by k_init_out.
-//
-// Shared memory (bytes):
-//   tab [2][256][128]       double-buffered byte table          64 KiB
-//   qs  [2][Rc][16]         query bytes of 16 groups per request 2*Rc*16
-//   dbs [2][128][128]       the 128 buckets (16 groups) column slice 32 KiB
-// ---------------------------------------------------------------------------
-constexpr int M4_CHUNK_G = 16;  // groups per staged chunk
-constexpr int M4_TAB_BYTES = 256 * 128;
-constexpr int M4_DBS_BYTES = M4_CHUNK_G * 8 * 128;
-
-template <int NT, int RPT>
-struct M4Layout {
-    static constexpr int Rc = (NT / 8) * RPT;
-    static constexpr int QS_BYTES = Rc * 16;
-    static constexpr int OFF_TAB = 0;
-    static constexpr int OFF_QS = 2 * M4_TAB_BYTES;
-    static constexpr int OFF_DBS = OFF_QS + 2 * QS_BYTES;
-    static constexpr int SMEM = OFF_DBS + 2 * M4_DBS_BYTES;
-};
-
-template <int NT, int RPT>
-__global__ void __launch_bounds__(NT, 1)
-k_scan_m4rm(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ q,
-            uint64_t q_stride, uint32_t B, uint8_t* __restrict__ out, uint32_t n_ctiles,
-            uint32_t n_groups, uint64_t total_work) {
-    using L = M4Layout<NT, RPT>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    const uint32_t sbase = smem_u32(smem);
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int qq = lane >> 3, l8 = lane & 7;
-
-    // table-build role: word column bw, 16-row block bj (rows 16*bj .. 16*bj+15)
-    const int bw = tid & 31;
-    const int bj = (tid >> 5) & 15;  // NT >= 512 -> each (bw, bj) built once per 16 warps
-    const bool builder = tid < 512;
-    const uint32_t hm0 = 0u - ((bj >> 0) & 1u), hm1 = 0u - ((bj >> 1) & 1u);
-    const uint32_t hm2 = 0u - ((bj >> 2) & 1u), hm3 = 0u - ((bj >> 3) & 1u);
-
-    const uint64_t w0 = total_work * blockIdx.x / gridDim.x;
-    const uint64_t w1 = total_work * (blockIdx.x + 1) / gridDim.x;
-
-    uint64_t u = w0;
-    while (u < w1) {
-        const uint32_t p = uint32_t(u / n_groups);
-        const uint32_t gs = uint32_t(u - uint64_t(p) * n_groups);
-        const uint64_t pend = uint64_t(p + 1) * n_groups;
-        const uint32_t ge = uint32_t((w1 < pend ? w1 : pend) - uint64_t(p) * n_groups);
-        u = uint64_t(p) * n_groups + ge;
-        const uint32_t rt = p / n_ctiles, c = p - rt * n_ctiles;
-        const uint32_t r_base = rt * L::Rc;
-
-        uint4 acc[RPT];
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) acc[i] = make_uint4(0, 0, 0, 0);
-
-        // stage chunk kc (16 groups) into buffer b
-        auto stage = [&](uint32_t kc, int b) {
-            // query bytes: Rc rows x 16 bytes
-            const uint32_t qdst = sbase + L::OFF_QS + b * L::QS_BYTES;
-            for (int r = tid; r < L::Rc; r += NT) {
-                const uint32_t rg = r_base + r;
-                const uint8_t* src = q + (rg < B ? uint64_t(rg) * q_stride : 0) + uint64_t(kc) * 16;
-                cp_async16(qdst + r * 16, src, rg < B ? 16u : 0u);
-            }
-            // db: buckets [kc*128, kc*128+128) x 128-byte slice c
-            const uint32_t ddst = sbase + L::OFF_DBS + b * M4_DBS_BYTES;
-            for (int k = tid; k < M4_CHUNK_G * 8 * 8; k += NT) {
-                const uint32_t bl = k >> 3, part = k & 7;
-                const uint32_t bucket = kc * 128 + bl;
-                const uint8_t* src =
-                    db + (bucket < nb ? uint64_t(bucket) * S : 0) + uint64_t(c) * 128 + part * 16;
-                cp_async16(ddst + bl * 128 + part * 16, src, bucket < nb ? 16u : 0u);
-            }
-        };
-
-        const uint32_t kc0 = gs / M4_CHUNK_G, kc1 = (ge + M4_CHUNK_G - 1) / M4_CHUNK_G;
-        stage(kc0, 0);
-        cp_async_commit();
-        int tb = 0;
-        for (uint32_t kc = kc0; kc < kc1; ++kc) {
-            const int b = (kc - kc0) & 1;
-            if (kc + 1 < kc1) {
-                stage(kc + 1, b ^ 1);
-                cp_async_commit();
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
-            __syncthreads();
-            const uint32_t qbuf = sbase + L::OFF_QS + b * L::QS_BYTES;
-            const uint32_t dbuf = sbase + L::OFF_DBS + b * M4_DBS_BYTES;
-            const uint32_t glo = (gs > kc * M4_CHUNK_G ? gs : kc * M4_CHUNK_G) - kc * M4_CHUNK_G;
-            const uint32_t ghi = (ge < kc * M4_CHUNK_G + M4_CHUNK_G ? ge : kc * M4_CHUNK_G + M4_CHUNK_G) -
-                                 kc * M4_CHUNK_G;
-#pragma unroll 1
-            for (uint32_t g4 = glo & ~3u; g4 < ghi; g4 += 4) {
-                uint32_t qw[RPT];
-#pragma unroll
-                for (int i = 0; i < RPT; ++i)
-                    qw[i] = lds32(qbuf + (((warp * RPT + i) * 4 + qq) * 16) + g4);
-#pragma unroll
-                for (int gg = 0; gg < 4; ++gg) {
-                    const uint32_t gl = g4 + gg;
-                    if (gl < glo || gl >= ghi) continue;  // uniform across the CTA
-                    const uint32_t tab = sbase + L::OFF_TAB + tb * M4_TAB_BYTES;
-                    if (builder) {
-                        // T[16*bj + x] = H_bj ^ L_x, L in Gray-code order: one XOR per row.
-                        const uint32_t src = dbuf + gl * 8 * 128 + bw * 4;
-                        const uint32_t b0 = lds32(src + 0 * 128), b1 = lds32(src + 1 * 128);
-                        const uint32_t b2 = lds32(src + 2 * 128), b3 = lds32(src + 3 * 128);
-                        uint32_t h = (lds32(src + 4 * 128) & hm0) ^ (lds32(src + 5 * 128) & hm1) ^
-                                     (lds32(src + 6 * 128) & hm2) ^ (lds32(src + 7 * 128) & hm3);
-                        const uint32_t row0 = tab + (bj * 16) * 128 + bw * 4;
-                        // Gray sequence 0,1,3,2,6,7,5,4,12,13,15,14,10,11,9,8
-                        sts32(row0 + 0 * 128, h);
-                        h ^= b0; sts32(row0 + 1 * 128, h);
-                        h ^= b1; sts32(row0 + 3 * 128, h);
-                        h ^= b0; sts32(row0 + 2 * 128, h);
-                        h ^= b2; sts32(row0 + 6 * 128, h);
-                        h ^= b0; sts32(row0 + 7 * 128, h);
-                        h ^= b1; sts32(row0 + 5 * 128, h);
-                        h ^= b0; sts32(row0 + 4 * 128, h);
-                        h ^= b3; sts32(row0 + 12 * 128, h);
-                        h ^= b0; sts32(row0 + 13 * 128, h);
-                        h ^= b1; sts32(row0 + 15 * 128, h);
-                        h ^= b0; sts32(row0 + 14 * 128, h);
-                        h ^= b2; sts32(row0 + 10 * 128, h);
-                        h ^= b0; sts32(row0 + 11 * 128, h);
-                        h ^= b1; sts32(row0 + 9 * 128, h);
-                        h ^= b0; sts32(row0 + 8 * 128, h);
-                    }
-                    __syncthreads();
-                    const uint32_t rowbase = tab + l8 * 16;
-#pragma unroll
-                    for (int i = 0; i < RPT; ++i) {
-                        const uint32_t idx = (qw[i] >> (8 * gg)) & 0xffu;
-                        const uint4 v = lds128(rowbase + idx * 128);
-                        acc[i].x ^= v.x;
-                        acc[i].y ^= v.y;
-                        acc[i].z ^= v.z;
-                        acc[i].w ^= v.w;
-                    }
-                    tb ^= 1;
-                }
-            }
-            __syncthreads();  // chunk buffers b are re-staged next iteration
-        }
-        // flush
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            const uint32_t r = r_base + (warp * RPT + i) * 4 + qq;
-            if (r < B) {
-                uint8_t* o = out + uint64_t(r) * S + uint64_t(c) * 128 + l8 * 16;
-                red_xor64(o, uint64_t(acc[i].y) << 32 | acc[i].x);
-                red_xor64(o + 8, uint64_t(acc[i].w) << 32 | acc[i].z);
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
 // K1 (small batches): direct select-XOR, 16-byte words, selection bits from
 // 32-bucket query words. Grid: x = column blocks of 128 threads x 16 B,
 // y = bucket splits, z = request tiles of RPT. Each split writes its partial
@@ -523,42 +348,6 @@ cudaError_t run_peak_kernels(int num_sms, double* lop3_per_s, double* smem_bps, 
 // ---------------------------------------------------------------------------
 // host-side launchers
 // ---------------------------------------------------------------------------
-template <int NT, int RPT>
-static cudaError_t launch_m4(const ScanArgs& a, int ctas_per_sm, int num_sms) {
-    using L = M4Layout<NT, RPT>;
-    cudaError_t e = cudaFuncSetAttribute(k_scan_m4rm<NT, RPT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-    if (e != cudaSuccess) return e;
-    const uint32_t n_ctiles = a.S / 128;
-    const uint32_t n_rtiles = (a.B + L::Rc - 1) / L::Rc;
-    const uint32_t n_groups = (a.nb + 7) / 8;
-    const uint64_t total = uint64_t(n_ctiles) * n_rtiles * n_groups;
-    uint64_t grid = uint64_t(num_sms) * (ctas_per_sm > 0 ? ctas_per_sm : 1);
-    // at least ~8 groups of work per CTA
-    const uint64_t max_grid = (total + 7) / 8;
-    if (grid > max_grid) grid = max_grid > 0 ? max_grid : 1;
-    k_scan_m4rm<NT, RPT><<<dim3(uint32_t(grid)), NT, L::SMEM, a.stream>>>(
-        a.db, a.nb, a.S, a.q, a.q_stride, a.B, a.out, n_ctiles, n_groups, total);
-    return cudaGetLastError();
-}
-
-int m4rm_rows_per_tile(int variant) {
-    switch (variant) {
-        case 0: return M4Layout<512, 2>::Rc;
-        case 1: return M4Layout<512, 4>::Rc;
-        case 2: return M4Layout<512, 8>::Rc;
-        default: return M4Layout<512, 16>::Rc;
-    }
-}
-
-cudaError_t launch_scan_m4rm(const ScanArgs& a, int ctas_per_sm, int num_sms) {
-    // choose RPT so that one request tile covers the batch (up to Rc = 1024)
-    if (a.B <= 128) return launch_m4<512, 2>(a, ctas_per_sm, num_sms);
-    if (a.B <= 256) return launch_m4<512, 4>(a, ctas_per_sm, num_sms);
-    if (a.B <= 512) return launch_m4<512, 8>(a, ctas_per_sm, num_sms);
-    return launch_m4<512, 16>(a, ctas_per_sm, num_sms);
-}
-
 cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
                                uint32_t* nsplit_out) {
     constexpr int RPT = 8;

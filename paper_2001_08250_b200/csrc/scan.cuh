@@ -22,8 +22,23 @@ struct ScanArgs {
     cudaStream_t stream;
 };
 
-cudaError_t launch_scan_m4rm(const ScanArgs& a, int ctas_per_sm, int num_sms);
-int m4rm_rows_per_tile(int variant);
+// M4RM scan (m4rm.cu): queries in the group-major layout qT[g*qstride + r].
+struct M4Args {
+    const uint8_t* db;
+    uint32_t nb, S;
+    const uint8_t* qT;
+    uint64_t qstride;    // multiple of 16, >= B
+    uint32_t B;
+    uint8_t* out;
+    cudaStream_t stream;
+};
+cudaError_t launch_scan_m4rm(const M4Args& a, int ctas_per_sm, int num_sms);
+uint64_t m4rm_qstride(uint32_t B);
+uint64_t m4rm_qrows(uint64_t n_groups);  // rows to allocate (staging reads 16-row chunks)
+cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
+                            uint8_t* qT, uint64_t qstride, cudaStream_t s);
+cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
+                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s);
 cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
                                uint32_t* nsplit_out);
 cudaError_t launch_scan_bytes(const ScanArgs& a);
