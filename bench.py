@@ -97,7 +97,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference's pir::answer_batch on host cores (oracle/_ref)
 # ---------------------------------------------------------------------------
-def cpu_reference_sample(target_s: float = 15.0, max_per_thread: int = 8):
+def cpu_reference_sample(target_s: float = 15.0, max_per_thread: int = 256):
     """Times the unmodified reference answer_batch (one thread per host core, each
     on a disjoint slice of the requests, shared immutable Snapshot) on a bounded
     sample of config-4 requests. Returns (req/s, threads, sample description)."""

@@ -125,6 +125,9 @@ int xpir_scan_timing_collect(double* total_ms, uint32_t* launches);
  * per second, both chip-wide. */
 int xpir_measure_peaks(int device, double* lop3_per_s, double* smem_bytes_per_s,
                        double* sm_clock_mhz);
+/* tcgen05.ld (TMEM -> registers) bytes per SM clock with warp-uniform random
+ * columns; variant 0..4 = {x1, 4 warps}, {x1, 16}, {x2, 16}, {x4, 16}, {x4, 8}. */
+int xpir_probe_tmem(int device, int variant, double* bytes_per_clk_sm);
 
 /* ------------------------------------------------------------------------ */
 /* Intra-box peer memory for the sharded reduce (CUDA IPC over NVLink).       */

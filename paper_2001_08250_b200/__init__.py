@@ -75,6 +75,7 @@ _SIGS = {
     "xpir_scan_timing": ([C.c_int], C.c_int),
     "xpir_scan_timing_collect": ([C.POINTER(C.c_double), _u32p], C.c_int),
     "xpir_measure_peaks": ([C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+    "xpir_probe_tmem": ([C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "xpir_ipc_get_handle": ([C.c_int, _vp, _u8p], C.c_int),
     "xpir_ipc_open": ([C.c_int, _u8p, C.POINTER(_vp)], C.c_int),
     "xpir_ipc_close": ([C.c_int, _vp], C.c_int),
@@ -212,6 +213,13 @@ def measure_peaks(device: int = 0) -> dict:
     a, b, c = C.c_double(), C.c_double(), C.c_double()
     _check(lib().xpir_measure_peaks(device, C.byref(a), C.byref(b), C.byref(c)))
     return {"lop3_per_s": a.value, "smem_bytes_per_s": b.value, "sm_clock_attr_mhz": c.value}
+
+
+def probe_tmem(variant: int, device: int = 0) -> float:
+    """tcgen05.ld bytes per SM clock (diagnostic microbenchmark)."""
+    v = C.c_double()
+    _check(lib().xpir_probe_tmem(device, variant, C.byref(v)))
+    return v.value
 
 
 def ipc_handle(d_ptr, device: int = 0) -> bytes:

@@ -240,6 +240,14 @@ int xpir_measure_peaks(int device, double* lop3_per_s, double* smem_bps, double*
     return XPIR_OK;
 }
 
+int xpir_probe_tmem(int device, int variant, double* bytes_per_clk_sm) {
+    DeviceGuard g(device);
+    XCK(run_tmem_probe(variant, num_sms(device), bytes_per_clk_sm));
+    XCK(cudaDeviceSynchronize());
+    count_launches(2);
+    return XPIR_OK;
+}
+
 int xpir_ipc_get_handle(int device, const void* d_ptr, uint8_t handle[64]) {
     if (!d_ptr || !handle) return fail(XPIR_EINVAL, "ipc_get_handle: null argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");

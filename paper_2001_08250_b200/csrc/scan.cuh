@@ -51,6 +51,7 @@ cudaError_t launch_repack(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo,
 cudaError_t launch_xor_reduce(uint8_t* dst, const uint8_t* const* d_srcs, uint32_t nsrc,
                               uint64_t bytes, int num_sms, cudaStream_t s);
 cudaError_t run_peak_kernels(int num_sms, double* lop3_per_s, double* smem_bps, cudaStream_t s);
+cudaError_t run_tmem_probe(int variant, int num_sms, double* bytes_per_clk_sm);
 
 // write path / generators (write.cu)
 cudaError_t launch_keystream(const uint8_t* key_host32, uint64_t nonce, uint64_t byte_offset,
