@@ -97,60 +97,76 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference's pir::answer_batch on host cores (oracle/_ref)
 # ---------------------------------------------------------------------------
-def cpu_reference_sample(target_s: float = 15.0, max_per_thread: int = 256):
-    """Times the unmodified reference answer_batch (one thread per host core, each
-    on a disjoint slice of the requests, shared immutable Snapshot) on a bounded
-    sample of config-4 requests. Returns (req/s, threads, sample description)."""
-    import oracle
-    from oracle import recipes
+class CpuReference:
+    """The unmodified reference pir::answer_batch (oracle/_ref; the C restatement
+    when the reference build is absent) on the host cores: one thread per core,
+    each on a disjoint slice of the requests over ONE shared immutable Snapshot
+    (concurrent answers are allowed by the reference contract)."""
 
-    o = oracle.best()
-    threads = os.cpu_count() or 1
-    g = o.detrng(STORE_SEED)
-    if o.kind == "reference":
-        snap = o.snapshot_detrng(g, N_BUCKETS, BUCKET_BYTES)
-    else:
-        db = np.frombuffer(g.fill(N_BUCKETS * BUCKET_BYTES), np.uint8)
-    per = 1
-    best = None
-    while True:
-        B = threads * per
-        seeds = recipes.config4_seeds(o, B)
-        q = np.stack([np.frombuffer(o.prng_expand(s.tobytes(), N_BUCKETS // 8), np.uint8) for s in seeds])
-        if o.kind == "reference":
-            _, secs = snap.answer_batch(q, B, threads)
+    def __init__(self):
+        import oracle
+
+        self.o = oracle.best()
+        self.kind = self.o.kind
+        self.threads = os.cpu_count() or 1
+        g = self.o.detrng(STORE_SEED)  # call 0 = the 4 GiB store
+        if self.kind == "reference":
+            self.snap = self.o.snapshot_detrng(g, N_BUCKETS, BUCKET_BYTES)
         else:
-            t0 = time.perf_counter()
-            o.answer_batch(db, N_BUCKETS, BUCKET_BYTES, q, B, threads=threads)
-            secs = time.perf_counter() - t0
-        best = (B / secs, B, secs)
-        if secs >= target_s / 3 or per >= max_per_thread:
-            break
-        per = min(max_per_thread, max(per * 2, int(per * target_s / max(secs, 1e-3))))
-    rate, B, secs = best
-    desc = (f"{B} of the 8192 config-4 requests (seeds = DetRng(3) calls 1..{B}) over the full 4 GiB store, "
-            f"{threads} threads x answer_batch slices, {secs:.1f} s")
-    return rate, threads, desc, o.kind
+            self.db = np.frombuffer(g.fill(N_BUCKETS * BUCKET_BYTES), np.uint8)
+        self.q = {}
+
+    def queries(self, B):
+        from oracle import recipes
+
+        if B not in self.q:
+            seeds = recipes.config4_seeds(self.o, B)
+            self.q[B] = np.stack([np.frombuffer(self.o.prng_expand(s.tobytes(), N_BUCKETS // 8), np.uint8)
+                                  for s in seeds])
+        return self.q[B]
+
+    def time(self, B) -> float:
+        q = self.queries(B)
+        if self.kind == "reference":
+            return self.snap.answer_batch(q, B, self.threads)[1]
+        t0 = time.perf_counter()
+        self.o.answer_batch(self.db, N_BUCKETS, BUCKET_BYTES, q, B, threads=self.threads)
+        return time.perf_counter() - t0
+
+    def calibrate(self, target_s: float, max_per_thread: int = 256) -> int:
+        """Requests per sample so one sample takes about target_s."""
+        per = 1
+        while True:
+            secs = self.time(self.threads * per)
+            if secs >= target_s / 2 or per >= max_per_thread:
+                return self.threads * per
+            per = min(max_per_thread, max(per * 2, int(per * target_s / max(secs, 1e-3))))
+
+    def describe(self, B, secs) -> str:
+        return (f"{B} of the 8192 config-4 requests (seeds = DetRng(3) calls 1..{B}) over the full 4 GiB "
+                f"store, {self.threads} threads x answer_batch slices, {secs:.1f} s per sample")
+
+
+def cpu_reference_sample(target_s: float = 15.0):
+    ref = CpuReference()
+    B = ref.calibrate(target_s)
+    secs = ref.time(B)
+    return B / secs, ref.threads, ref.describe(B, secs), ref.kind
 
 
 def run_reference(args):
     rank = env_int("RANK", 0)
     if rank != 0:
         return 0
-    import oracle
-
-    if not oracle.ref_available():
-        kind = "port"
-    else:
-        kind = "reference"
-    rates = []
-    desc = ""
-    threads = os.cpu_count() or 1
+    ref = CpuReference()
+    B = ref.calibrate(args.ref_step_seconds)
+    times = []
     for i in range(args.warmup + args.steps):
-        r, threads, desc, kind = cpu_reference_sample(target_s=args.ref_step_seconds, max_per_thread=4)
+        secs = ref.time(B)
         if i >= args.warmup:
-            rates.append(r)
-    value = statistics.median(rates)
+            times.append(secs)
+    secs = statistics.median(times)
+    value = B / secs
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * BATCH / value,
@@ -158,8 +174,10 @@ def run_reference(args):
         "data": "synthetic (DetRng / ChaCha20 recipe of SURVEY.md §8(d))",
         "config": {"workload": "config4: 4 GiB store (1,048,576 buckets x 4096 B), 8192 seeded requests",
                    "store_bytes": N_BUCKETS * BUCKET_BYTES, "batch": BATCH,
-                   "parallelism": f"host threads={threads}", "l2": "store larger than L2"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": desc},
+                   "parallelism": f"host threads={ref.threads}", "l2": "store larger than L2",
+                   "step": f"a bounded sample of {B} requests per step; ms_per_step scaled to the 8192 batch"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.threads, "kind": ref.kind,
+                         "sample": ref.describe(B, secs)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
