@@ -98,6 +98,9 @@ uint64_t xpir_query_window_bytes(const xpir_store* st);
 /* K2 alone: d_q[r*q_stride + k] = prng_expand(seed_r)[byte_lo + k], k < nbytes. */
 int xpir_expand_queries_dev(int device, const uint8_t* d_seeds, uint32_t batch, uint64_t byte_lo,
                             uint64_t nbytes, uint8_t* d_q, uint64_t q_stride, void* stream);
+/* pir::mask_answer (pir.cpp:65-69) for one host answer: out = ans ^ prng_expand(seed, len),
+ * the pad generated and applied on device. */
+int xpir_mask_answer(const uint8_t* ans, uint64_t len, const uint8_t seed[32], uint8_t* out);
 /* K3 alone: d_out[r*S..] ^= prng_expand(mask_seed_r, S). */
 int xpir_mask_dev(int device, uint8_t* d_out, const uint8_t* d_mask_seeds, uint32_t batch,
                   uint32_t S, void* stream);

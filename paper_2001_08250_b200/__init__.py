@@ -93,6 +93,7 @@ _SIGS = {
     "xpir_answer_batch_seeded_dev": ([_vp, _vp, C.c_uint32, _vp, _vp, _vp], C.c_int),
     "xpir_query_window_bytes": ([_vp], C.c_uint64),
     "xpir_expand_queries_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint64, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
+    "xpir_mask_answer": ([_u8p, C.c_uint64, _u8p, _u8p], C.c_int),
     "xpir_mask_dev": ([C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, _vp], C.c_int),
     "xpir_xor_reduce_dev": ([C.c_int, _vp, _vp, C.c_uint32, C.c_uint64, _vp], C.c_int),
     "xpir_prng_expand": ([_u8p, _u8p, C.c_uint64], C.c_int),
@@ -335,6 +336,14 @@ def expand_queries_dev(d_seeds, B: int, byte_lo: int, nbytes: int, d_q, q_stride
                        stream=None) -> None:
     _check(lib().xpir_expand_queries_dev(device, _ptr(d_seeds), B, byte_lo, nbytes, _ptr(d_q), q_stride,
                                          _stream(stream)))
+
+
+def mask_answer(ans: bytes, seed32: bytes) -> bytes:
+    """pir::mask_answer (pir.cpp:65-69), pad generated and applied on device."""
+    a = _u8(ans) if len(ans) else np.zeros(1, np.uint8)
+    out = np.empty(max(len(ans), 1), np.uint8)
+    _check(lib().xpir_mask_answer(_p(a), len(ans), _p(_u8(seed32)), _p(out)))
+    return out[: len(ans)].tobytes()
 
 
 def mask_dev(d_out, d_mask, B: int, S: int, device: int = 0, stream=None) -> None:

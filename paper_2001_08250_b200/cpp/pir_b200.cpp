@@ -1,0 +1,174 @@
+// Drop-in replacement for the reference's src/pir.cpp
+// (/root/reference/proj/src/pir.cpp): the same declarations from
+// oblog/pir.hpp, with the server-side scan (answer, answer_batch — pir.cpp:29-52)
+// and the answer mask (mask_answer — pir.cpp:65-69) executed by the B200 kernels
+// behind include/xpir.h. Link this TU instead of pir.cpp.
+//
+// Client-side helpers (gen_queries, reconstruct, combine_masked, unmask) are not
+// on the server hot path; they keep their host implementation here so the TU is
+// a complete replacement.
+//
+// Snapshot residency: a sealed pir::Snapshot is immutable by contract
+// (server.hpp:70-71). The first answer against a snapshot uploads
+// it to HBM; later calls reuse the device copy, keyed by (data pointer, size,
+// geometry, epoch, content fingerprint). Thread-safe.
+#include <cstring>
+#include <list>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "oblog/pir.hpp"
+#include "xpir.h"
+
+namespace {
+
+void xpir_check(int rc, const char* what) {
+    if (rc == XPIR_OK) return;
+    std::string msg = std::string(what) + ": " + xpir_last_error();
+    if (rc == XPIR_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+uint64_t fingerprint(const oblog::pir::Snapshot& s) {
+    // FNV-1a over 8-byte words: every word for stores up to 16 MiB, an
+    // evenly strided sample of 64 Ki words beyond that (sealed snapshots are
+    // immutable; the sample guards against address reuse).
+    const uint8_t* p = s.data.data();
+    const size_t n = s.data.size();
+    uint64_t h = 1469598103934665603ULL ^ n;
+    auto mix = [&](uint64_t w) { h = (h ^ w) * 1099511628211ULL; };
+    const size_t words = n / 8;
+    const size_t step = n <= (16u << 20) ? 1 : std::max<size_t>(1, words / 65536);
+    for (size_t i = 0; i < words; i += step) {
+        uint64_t w;
+        std::memcpy(&w, p + 8 * i, 8);
+        mix(w);
+    }
+    for (size_t i = words * 8; i < n; ++i) mix(p[i]);
+    return h;
+}
+
+struct Resident {
+    const void* ptr;
+    size_t size;
+    uint32_t buckets, bucket_size;
+    uint64_t epoch, fp;
+    xpir_store* st;
+    ~Resident() { xpir_store_destroy(st); }
+};
+
+class StoreCache {
+public:
+    std::shared_ptr<Resident> get(const oblog::pir::Snapshot& s) {
+        const uint64_t fp = fingerprint(s);
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto it = lru_.begin(); it != lru_.end(); ++it) {
+            const auto& r = **it;
+            if (r.ptr == s.data.data() && r.size == s.data.size() && r.buckets == s.bucket_count &&
+                r.bucket_size == s.bucket_size && r.epoch == s.epoch && r.fp == fp) {
+                lru_.splice(lru_.begin(), lru_, it);
+                return lru_.front();
+            }
+        }
+        xpir_store* st = nullptr;
+        xpir_check(xpir_store_create(0, s.bucket_count, s.bucket_size, 0, s.bucket_count, &st),
+                   "pir: store_create");
+        auto r = std::make_shared<Resident>(Resident{s.data.data(), s.data.size(), s.bucket_count,
+                                                     s.bucket_size, s.epoch, fp, st});
+        xpir_check(xpir_store_upload(st, s.data.data(), s.epoch), "pir: store_upload");
+        lru_.push_front(r);
+        while (lru_.size() > kMax) lru_.pop_back();
+        return r;
+    }
+
+private:
+    static constexpr size_t kMax = 4;
+    std::mutex mu_;
+    std::list<std::shared_ptr<Resident>> lru_;
+};
+
+StoreCache& cache() {
+    static StoreCache c;
+    return c;
+}
+
+}  // namespace
+
+namespace oblog::pir {
+
+// pir.cpp:7-27 (client side)
+std::vector<QueryVector> gen_queries(uint32_t beta, uint32_t bucket_count, uint32_t servers,
+                                     Rng& rng) {
+    if (bucket_count == 0) throw std::invalid_argument("gen_queries: no buckets");
+    if (servers < 2) throw std::invalid_argument("gen_queries: need at least 2 servers");
+    if (beta >= bucket_count) throw std::invalid_argument("gen_queries: target out of range");
+    std::vector<QueryVector> qs(servers, QueryVector::zero(bucket_count));
+    const size_t nb = qs[0].data.size();
+    for (uint32_t i = 0; i + 1 < servers; ++i) {
+        rng.fill(qs[i].data.data(), nb);
+        if (bucket_count % 8) qs[i].data[nb - 1] &= uint8_t(0xffu >> (8 - bucket_count % 8));
+    }
+    QueryVector& last = qs.back();
+    last.set(beta);
+    for (uint32_t i = 0; i + 1 < servers; ++i) xor_into(last.data.data(), qs[i].data.data(), nb);
+    return qs;
+}
+
+std::vector<bytes> answer_batch(const Snapshot& snap, const std::vector<QueryVector>& qs) {
+    for (const QueryVector& q : qs)
+        if (q.bit_count != snap.bucket_count)
+            throw std::invalid_argument("answer_batch: query length mismatch");
+    std::vector<bytes> out(qs.size(), bytes(snap.bucket_size, 0));
+    if (qs.empty() || snap.bucket_count == 0 || snap.bucket_size == 0) return out;
+    auto res = cache().get(snap);
+    const size_t nb = (snap.bucket_count + 7) / 8;
+    bytes rows(qs.size() * nb), flat(qs.size() * size_t(snap.bucket_size));
+    for (size_t r = 0; r < qs.size(); ++r) std::memcpy(rows.data() + r * nb, qs[r].data.data(), nb);
+    xpir_check(xpir_answer_batch(res->st, rows.data(), nb, snap.bucket_count, uint32_t(qs.size()), nullptr,
+                                 flat.data()),
+               "answer_batch");
+    for (size_t r = 0; r < qs.size(); ++r)
+        std::memcpy(out[r].data(), flat.data() + r * snap.bucket_size, snap.bucket_size);
+    return out;
+}
+
+bytes answer(const Snapshot& snap, const QueryVector& q) {
+    if (q.bit_count != snap.bucket_count) throw std::invalid_argument("answer: query length mismatch");
+    return answer_batch(snap, {q}).front();
+}
+
+// pir.cpp:54-63 (client / leader side)
+bytes reconstruct(const std::vector<bytes>& answers) {
+    if (answers.empty()) throw std::invalid_argument("reconstruct: no answers");
+    bytes out = answers[0];
+    for (size_t i = 1; i < answers.size(); ++i) {
+        if (answers[i].size() != out.size())
+            throw std::invalid_argument("reconstruct: answer length mismatch");
+        xor_into(out.data(), answers[i].data(), out.size());
+    }
+    return out;
+}
+
+// pir.cpp:65-69 — server side: pad generated and applied on device
+bytes mask_answer(byte_view answer, const crypto::Seed& seed) {
+    bytes out(answer.size());
+    if (!answer.empty())
+        xpir_check(xpir_mask_answer(answer.data(), answer.size(), seed.data(), out.data()), "mask_answer");
+    return out;
+}
+
+bytes combine_masked(const std::vector<bytes>& masked) { return reconstruct(masked); }
+
+// pir.cpp:75-82 (client side)
+bytes unmask(byte_view combined, const std::vector<crypto::Seed>& seeds) {
+    bytes out(combined.begin(), combined.end());
+    for (const crypto::Seed& s : seeds) {
+        bytes pad = crypto::prng_expand(s, out.size());
+        xor_into(out.data(), pad.data(), out.size());
+    }
+    return out;
+}
+
+}  // namespace oblog::pir

@@ -582,6 +582,23 @@ int xpir_expand_queries_dev(int device, const uint8_t* d_seeds, uint32_t B, uint
     return XPIR_OK;
 }
 
+int xpir_mask_answer(const uint8_t* ans, uint64_t len, const uint8_t seed[32], uint8_t* out) {
+    if (!seed || (len && (!ans || !out))) return fail(XPIR_EINVAL, "mask_answer: null buffer");
+    if (!len) return XPIR_OK;
+    if (len > 0xffffffffull) return fail(XPIR_EINVAL, "mask_answer: answer too long");
+    uint8_t* d = nullptr;
+    XCK(cudaMalloc(&d, len + 32));
+    cudaError_t e = cudaMemcpy(d, ans, len, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d + len, seed, 32, cudaMemcpyHostToDevice);
+    // one "request" of S = len bytes: out = ans ^ pad
+    if (e == cudaSuccess) e = launch_init_out(d, 1, uint32_t(len), d + len, true, nullptr);
+    count_launches(1);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, len, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    XCK(e);
+    return XPIR_OK;
+}
+
 int xpir_mask_dev(int device, uint8_t* d_out, const uint8_t* d_mask, uint32_t B, uint32_t S,
                   void* stream) {
     if (B && (!d_out || !d_mask)) return fail(XPIR_EINVAL, "mask: null buffer");
