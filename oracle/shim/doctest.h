@@ -175,6 +175,8 @@ int main(int argc, char** argv) {
     }
     std::printf("[doctest-shim] test cases: %d | %d passed | %d failed | checks: %ld | %ld failed\n", run,
                 run - failed, failed, doctest::stats().checks, doctest::stats().failed_checks);
+    std::fflush(stdout);
+    std::fflush(stderr);
     return failed ? 1 : 0;
 }
 #endif

@@ -30,8 +30,8 @@ void xpir_check(int rc, const char* what) {
 
 std::mutex g_mu;
 std::unordered_map<const void*, xpir_table*>& tables() {
-    static std::unordered_map<const void*, xpir_table*> m;
-    return m;
+    static auto* m = new std::unordered_map<const void*, xpir_table*>;  // leaked on purpose
+    return *m;
 }
 
 xpir_table* dev(const void* self) {

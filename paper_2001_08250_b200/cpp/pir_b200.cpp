@@ -90,8 +90,10 @@ private:
 };
 
 StoreCache& cache() {
-    static StoreCache c;
-    return c;
+    // Intentionally leaked: device stores must not be freed from a static
+    // destructor that may run after the CUDA runtime has shut down.
+    static StoreCache* c = new StoreCache;
+    return *c;
 }
 
 }  // namespace
