@@ -136,6 +136,10 @@ int xpir_probe_tmem(int device, int variant, double* bytes_per_clk_sm);
 /* Intra-box peer memory for the sharded reduce (CUDA IPC over NVLink).       */
 /* ------------------------------------------------------------------------ */
 #define XPIR_IPC_HANDLE_BYTES 64
+/* Whole device allocations (IPC handles map allocation bases, so buffers shared
+ * with peers are allocated here rather than sub-allocated by a caching allocator). */
+int xpir_dev_alloc(int device, uint64_t bytes, void** d_ptr);
+int xpir_dev_free(int device, void* d_ptr);
 int xpir_ipc_get_handle(int device, const void* d_ptr, uint8_t handle[64]);
 /* Map a peer process's allocation; enables peer access (NVLink) lazily. */
 int xpir_ipc_open(int device, const uint8_t handle[64], void** d_ptr);

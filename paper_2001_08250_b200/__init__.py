@@ -76,6 +76,8 @@ _SIGS = {
     "xpir_scan_timing_collect": ([C.POINTER(C.c_double), _u32p], C.c_int),
     "xpir_measure_peaks": ([C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "xpir_probe_tmem": ([C.c_int, C.c_int, C.POINTER(C.c_double)], C.c_int),
+    "xpir_dev_alloc": ([C.c_int, C.c_uint64, C.POINTER(_vp)], C.c_int),
+    "xpir_dev_free": ([C.c_int, _vp], C.c_int),
     "xpir_ipc_get_handle": ([C.c_int, _vp, _u8p], C.c_int),
     "xpir_ipc_open": ([C.c_int, _u8p, C.POINTER(_vp)], C.c_int),
     "xpir_ipc_close": ([C.c_int, _vp], C.c_int),
@@ -221,6 +223,25 @@ def probe_tmem(variant: int, device: int = 0) -> float:
     v = C.c_double()
     _check(lib().xpir_probe_tmem(device, variant, C.byref(v)))
     return v.value
+
+
+class DeviceBuffer:
+    """A whole cudaMalloc allocation (IPC-shareable), exposed to torch through
+    __cuda_array_interface__ (``torch.as_tensor(buf, device=...)`` is zero-copy)."""
+
+    def __init__(self, nbytes: int, device: int = 0):
+        p = _vp()
+        _check(lib().xpir_dev_alloc(device, nbytes, C.byref(p)))
+        self.ptr, self.nbytes, self.device = p.value, nbytes, device
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            lib().xpir_dev_free(self.device, self.ptr)
+            self.ptr = None
+
+    __del__ = close
 
 
 def ipc_handle(d_ptr, device: int = 0) -> bytes:

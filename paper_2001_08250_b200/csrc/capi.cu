@@ -248,6 +248,20 @@ int xpir_probe_tmem(int device, int variant, double* bytes_per_clk_sm) {
     return XPIR_OK;
 }
 
+int xpir_dev_alloc(int device, uint64_t bytes, void** d_ptr) {
+    if (!d_ptr) return fail(XPIR_EINVAL, "dev_alloc: null out");
+    DeviceGuard g(device);
+    cudaError_t e = cudaMalloc(d_ptr, std::max<uint64_t>(bytes, 16));
+    if (e != cudaSuccess) return fail(XPIR_ENOMEM, std::string("dev_alloc: ") + cudaGetErrorString(e));
+    return XPIR_OK;
+}
+
+int xpir_dev_free(int device, void* d_ptr) {
+    DeviceGuard g(device);
+    XCK(cudaFree(d_ptr));
+    return XPIR_OK;
+}
+
 int xpir_ipc_get_handle(int device, const void* d_ptr, uint8_t handle[64]) {
     if (!d_ptr || !handle) return fail(XPIR_EINVAL, "ipc_get_handle: null argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");

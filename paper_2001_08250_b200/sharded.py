@@ -63,7 +63,9 @@ class ShardedScan:
         self.N, self.S, self.B, self.device = N, S, B, device
         lo, hi = self.plan.bucket_range(self.rank)
         self.store = xp.Store(N, S, lo, hi, device=device)
-        self.partial = torch.empty((B, S), dtype=torch.uint8, device=f"cuda:{device}")
+        # a whole allocation: peers map it through CUDA IPC (handles name allocation bases)
+        self._pbuf = xp.DeviceBuffer(B * S, device)
+        self.partial = torch.as_tensor(self._pbuf, device=f"cuda:{device}").view(B, S)
         self.r0, self.r1 = self.plan.row_range(self.rank, B)
         self.peers: list[int] = []
         self.src_ptrs = None
@@ -89,6 +91,8 @@ class ShardedScan:
             self.xp.ipc_close(p, self.device)
         self.peer_base = []
         self.store.close()
+        self.partial = None
+        self._pbuf.close()
 
     def step(self, d_seeds, stream=None, d_mask=None):
         """One batch: partial scan of this shard, barrier, reduce own rows from
