@@ -51,12 +51,17 @@ uint64_t fingerprint(const oblog::pir::Snapshot& s) {
 }
 
 struct Resident {
-    const void* ptr;
-    size_t size;
-    uint32_t buckets, bucket_size;
-    uint64_t epoch, fp;
-    xpir_store* st;
-    ~Resident() { xpir_store_destroy(st); }
+    const void* ptr = nullptr;
+    size_t size = 0;
+    uint32_t buckets = 0, bucket_size = 0;
+    uint64_t epoch = 0, fp = 0;
+    xpir_store* st = nullptr;
+    Resident() = default;
+    Resident(const Resident&) = delete;
+    Resident& operator=(const Resident&) = delete;
+    ~Resident() {
+        if (st) xpir_store_destroy(st);
+    }
 };
 
 class StoreCache {
@@ -72,12 +77,16 @@ public:
                 return lru_.front();
             }
         }
-        xpir_store* st = nullptr;
-        xpir_check(xpir_store_create(0, s.bucket_count, s.bucket_size, 0, s.bucket_count, &st),
+        auto r = std::make_shared<Resident>();
+        xpir_check(xpir_store_create(0, s.bucket_count, s.bucket_size, 0, s.bucket_count, &r->st),
                    "pir: store_create");
-        auto r = std::make_shared<Resident>(Resident{s.data.data(), s.data.size(), s.bucket_count,
-                                                     s.bucket_size, s.epoch, fp, st});
-        xpir_check(xpir_store_upload(st, s.data.data(), s.epoch), "pir: store_upload");
+        r->ptr = s.data.data();
+        r->size = s.data.size();
+        r->buckets = s.bucket_count;
+        r->bucket_size = s.bucket_size;
+        r->epoch = s.epoch;
+        r->fp = fp;
+        xpir_check(xpir_store_upload(r->st, s.data.data(), s.epoch), "pir: store_upload");
         lru_.push_front(r);
         while (lru_.size() > kMax) lru_.pop_back();
         return r;

@@ -49,7 +49,7 @@ struct M4Layout {
     static constexpr int Rc = NW * 4 * RPT;
     static constexpr int QS_BYTES = M4_CHUNK_G * Rc;
     static constexpr int OFF_TAB = 0;
-    static constexpr int OFF_QS = 2 * M4_TAB_BYTES;
+    static constexpr int OFF_QS = 4 * M4_TAB_BYTES;  // [2 phases][2 tables]
     static constexpr int OFF_DBS = OFF_QS + 2 * QS_BYTES;
     static constexpr int SMEM = OFF_DBS + 2 * M4_DBS_BYTES;
 };
@@ -84,7 +84,7 @@ k_scan_m4rm(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8
             uint64_t qstride, uint32_t B, uint8_t* __restrict__ out, uint32_t n_ctiles,
             uint32_t n_groups, uint64_t total_work) {
     using L = M4Layout<NT, RPT>;
-    static_assert(L::NW >= M4_BUILD_WARPS, "need 8 builder warps");
+    static_assert(L::NW >= 2 * M4_BUILD_WARPS, "need 8 builder warps per table of a pair");
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const int tid = threadIdx.x;
@@ -93,7 +93,7 @@ k_scan_m4rm(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8
     const int slot0 = (warp * 4 + qq) * RPT;  // first request slot of this thread
 
     // builder role (warps 0..7): word column `lane`, rows [32*warp, 32*warp+32)
-    const bool builder = warp < M4_BUILD_WARPS;
+    const bool builder = warp < 2 * M4_BUILD_WARPS;
     const uint32_t hm5 = 0u - ((warp >> 0) & 1u), hm6 = 0u - ((warp >> 1) & 1u),
                    hm7 = 0u - ((warp >> 2) & 1u);
 
@@ -154,17 +154,22 @@ k_scan_m4rm(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8
             const uint32_t g0 = kc * M4_CHUNK_G;
             const uint32_t glo = (gs > g0 ? gs : g0) - g0;
             const uint32_t ghi = (ge < g0 + M4_CHUNK_G ? ge : g0 + M4_CHUNK_G) - g0;
+            // Groups are processed in pairs: warps 0..7 build T_g, warps 8..15 build
+            // T_{g+1}, one barrier, then every request does two lookups folded with
+            // one 3-input XOR per word (acc ^= T_g[x] ^ T_{g+1}[y]).
 #pragma unroll 1
-            for (uint32_t gl = glo; gl < ghi; ++gl) {
-                const uint32_t tab = sbase + L::OFF_TAB + tb * M4_TAB_BYTES;
-                if (builder) {
-                    const uint32_t src = dbuf + gl * 8 * 128 + lane * 4;
+            for (uint32_t gl = glo; gl < ghi; gl += 2) {
+                const bool pair = gl + 1 < ghi;  // uniform across the CTA
+                const uint32_t tabA = sbase + L::OFF_TAB + tb * 2 * M4_TAB_BYTES;
+                if (builder && (warp < M4_BUILD_WARPS || pair)) {
+                    const uint32_t g = gl + (warp >> 3);
+                    const uint32_t src = dbuf + g * 8 * 128 + lane * 4;
                     uint32_t bk[5];
 #pragma unroll
                     for (int k = 0; k < 5; ++k) bk[k] = lds32(src + k * 128);
                     uint32_t h = (lds32(src + 5 * 128) & hm5) ^ (lds32(src + 6 * 128) & hm6) ^
                                  (lds32(src + 7 * 128) & hm7);
-                    const uint32_t row0 = tab + (warp * 32) * 128 + lane * 4;
+                    const uint32_t row0 = tabA + (warp >> 3) * M4_TAB_BYTES + ((warp & 7) * 32) * 128 + lane * 4;
                     sts32(row0, h);
 #pragma unroll
                     for (int k = 1; k < 32; ++k) {
@@ -174,17 +179,34 @@ k_scan_m4rm(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8
                 }
                 __syncthreads();
                 if (active) {
-                    IdxVec<RPT> iv;
-                    iv.load(qbuf + gl * L::Rc + slot0);
-                    const uint32_t rowbase = tab + l8 * 16;
+                    const uint32_t rowA = tabA + l8 * 16;
+                    IdxVec<RPT> ia;
+                    ia.load(qbuf + gl * L::Rc + slot0);
+                    if (pair) {
+                        const uint32_t rowB = rowA + M4_TAB_BYTES;
+                        IdxVec<RPT> ib;
+                        ib.load(qbuf + (gl + 1) * L::Rc + slot0);
 #pragma unroll
-                    for (int i = 0; i < RPT; ++i) {
-                        const uint32_t idx = (iv.w[i >> 2] >> (8 * (i & 3))) & 0xffu;
-                        const uint4 v = lds128(rowbase + idx * 128);
-                        acc[i].x ^= v.x;
-                        acc[i].y ^= v.y;
-                        acc[i].z ^= v.z;
-                        acc[i].w ^= v.w;
+                        for (int i = 0; i < RPT; ++i) {
+                            const uint32_t xa = (ia.w[i >> 2] >> (8 * (i & 3))) & 0xffu;
+                            const uint32_t xb = (ib.w[i >> 2] >> (8 * (i & 3))) & 0xffu;
+                            const uint4 va = lds128(rowA + xa * 128);
+                            const uint4 vb = lds128(rowB + xb * 128);
+                            acc[i].x ^= va.x ^ vb.x;
+                            acc[i].y ^= va.y ^ vb.y;
+                            acc[i].z ^= va.z ^ vb.z;
+                            acc[i].w ^= va.w ^ vb.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < RPT; ++i) {
+                            const uint32_t xa = (ia.w[i >> 2] >> (8 * (i & 3))) & 0xffu;
+                            const uint4 va = lds128(rowA + xa * 128);
+                            acc[i].x ^= va.x;
+                            acc[i].y ^= va.y;
+                            acc[i].z ^= va.z;
+                            acc[i].w ^= va.w;
+                        }
                     }
                 }
                 tb ^= 1;
