@@ -241,3 +241,31 @@ def test_config4_sample_golden(xp, port, golden, cuda):
         xp.set_scan_opts(k)
         out = st.answer_batch_seeded(seeds)
         assert [sha(out[r]) for r in range(8)] == G["out_rows_sha256"]
+
+
+@pytest.mark.slow
+def test_config5_shapes_golden(xp, golden, cuda):
+    """Config 5: every (slot, depth) shape over the same 1 GiB DetRng(5) store,
+    4 DetRng(55) requests each, vs the reference outputs; both scan kernels."""
+    torch = cuda
+    G = golden["config5"]
+    key = xp.blake2b((5).to_bytes(8, "little"), 32)
+    qkey = xp.blake2b((55).to_bytes(8, "little"), 32)
+    nonce = 0
+    for e in G["shapes"]:
+        N, S = e["N"], e["S"]
+        st = xp.Store(N, S)
+        st.fill_keystream(key, 0)
+        q = torch.zeros((4, N // 8), dtype=torch.uint8, device="cuda")
+        xp.keystream_rows_dev(qkey, nonce, 4, N // 8, q, N // 8)
+        nonce += 4
+        torch.cuda.synchronize()
+        assert sha(q.cpu().numpy()) == e["q_sha256"]
+        for k in (1, 2):
+            xp.set_scan_opts(k)
+            out = torch.empty((4, S), dtype=torch.uint8, device="cuda")
+            st.answer_batch_dev(q, N // 8, 4, out)
+            torch.cuda.synchronize()
+            o = out.cpu().numpy()
+            assert [sha(o[r]) for r in range(4)] == e["out_rows_sha256"], (e["slot"], e["depth"], k)
+        st.close()
