@@ -1,0 +1,159 @@
+// K1 (small batches, B < ~96): direct select-XOR — pir::answer_batch
+// (pir.cpp:41-52) streamed once from HBM.
+//
+// For small batches the scan is HBM-bound (B <~ 11) or bound by the dense
+// masked-XOR rate (one LOP3 per request x 32-bit word x bucket). Each CTA
+// (256 threads) owns a bucket range; a thread owns one 16-byte column of the
+// bucket and a contiguous run of buckets ("phase"), so each warp load is a
+// coalesced slice of one bucket (or of several buckets when S < 512 B) and every
+// thread has a long, independent, unrolled stream of 16-byte loads in flight.
+// Selection bits come from 32-bucket query words, bit-reversed so each bucket's
+// all-ones/zero mask is one arithmetic shift. Phases are XOR-reduced in shared
+// memory and each CTA writes its partial answers to part[split] (plain stores;
+// k_reduce_parts XORs the splits into `out` — deterministic, no atomics).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "scan.cuh"
+
+namespace xpir {
+
+constexpr int DIRECT_NT = 256;
+
+template <int RPT>
+__global__ void __launch_bounds__(DIRECT_NT)
+k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ q,
+              uint64_t q_stride, uint32_t B, uint8_t* __restrict__ part, uint32_t bpc, uint32_t cw) {
+    constexpr int RB = RPT < 8 ? RPT : 8;  // requests reduced per shared-memory round
+    __shared__ uint4 red[DIRECT_NT * RB];
+    const uint32_t ncol = S / 16;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t phases = DIRECT_NT / cw;
+    const uint32_t p = tid / cw;
+    const uint32_t c = blockIdx.y * cw + (tid - p * cw);
+    const bool active = p < phases && c < ncol;
+    // grid: x = request tile (fastest, so the tiles reading the same bucket range run
+    // together and share it through L2), y = column block, z = bucket split
+    const uint32_t split = blockIdx.z;
+    const uint32_t r0 = blockIdx.x * RPT;
+    const uint32_t L = bpc / phases;  // multiple of 32
+    const uint32_t jb = split * bpc + p * L;
+    const uint32_t je = min(nb, jb + L);
+
+    uint4 acc[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) acc[i] = make_uint4(0, 0, 0, 0);
+
+    if (active) {
+        const uint4* col = reinterpret_cast<const uint4*>(db) + c;
+        for (uint32_t jc = jb; jc < je; jc += 32) {
+            const uint32_t n = min(32u, je - jc);
+            uint32_t qw[RPT];
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                uint32_t w = 0;
+                if (r0 + i < B) {
+                    const uint8_t* qp = q + uint64_t(r0 + i) * q_stride + (jc >> 3);
+#pragma unroll
+                    for (uint32_t k = 0; k < 4; ++k)
+                        if (8 * k < n) w |= uint32_t(__ldg(qp + k)) << (8 * k);
+                }
+                if (n < 32) w &= (1u << n) - 1u;
+                qw[i] = __brev(w);  // bucket jc+jj -> bit 31-jj
+            }
+            if (n == 32) {
+#pragma unroll 8
+                for (uint32_t jj = 0; jj < 32; ++jj) {
+                    const uint4 v = __ldcs(col + uint64_t(jc + jj) * ncol);
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        const uint32_t m = uint32_t(int32_t(qw[i]) >> 31);
+                        qw[i] <<= 1;
+                        acc[i].x ^= v.x & m;
+                        acc[i].y ^= v.y & m;
+                        acc[i].z ^= v.z & m;
+                        acc[i].w ^= v.w & m;
+                    }
+                }
+            } else {
+                for (uint32_t jj = 0; jj < n; ++jj) {
+                    const uint4 v = __ldcs(col + uint64_t(jc + jj) * ncol);
+#pragma unroll
+                    for (int i = 0; i < RPT; ++i) {
+                        const uint32_t m = uint32_t(int32_t(qw[i]) >> 31);
+                        qw[i] <<= 1;
+                        acc[i].x ^= v.x & m;
+                        acc[i].y ^= v.y & m;
+                        acc[i].z ^= v.z & m;
+                        acc[i].w ^= v.w & m;
+                    }
+                }
+            }
+        }
+    }
+    // XOR-reduce the phases that share a column, then one plain store per (request, column)
+    if (phases > 1) {
+#pragma unroll
+        for (int i0 = 0; i0 < RPT; i0 += RB) {
+#pragma unroll
+            for (int i = 0; i < RB; ++i) red[i * DIRECT_NT + tid] = acc[i0 + i];
+            __syncthreads();
+            if (p == 0 && active) {
+                for (uint32_t ph = 1; ph < phases; ++ph)
+#pragma unroll
+                    for (int i = 0; i < RB; ++i) {
+                        const uint4 v = red[i * DIRECT_NT + ph * cw + tid];
+                        acc[i0 + i].x ^= v.x; acc[i0 + i].y ^= v.y;
+                        acc[i0 + i].z ^= v.z; acc[i0 + i].w ^= v.w;
+                    }
+            }
+            __syncthreads();
+        }
+    }
+    if (p == 0 && active) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+            if (r0 + i < B) reinterpret_cast<uint4*>(part + (uint64_t(split) * B + r0 + i) * S)[c] = acc[i];
+    }
+}
+
+template <int RPT>
+static cudaError_t launch_direct_t(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
+                                   uint32_t* nsplit_out) {
+    const uint32_t ncol = a.S / 16;
+    const uint32_t cw = ncol >= DIRECT_NT ? DIRECT_NT : ncol;  // columns per CTA
+    const uint32_t phases = DIRECT_NT / cw;
+    const uint32_t gx = (ncol + cw - 1) / cw;
+    const uint32_t gz = (a.B + RPT - 1) / RPT;
+    const uint64_t out_bytes = uint64_t(a.B) * a.S;
+    // ~8 CTAs per SM; each phase gets a multiple of 32 buckets
+    const uint64_t per = uint64_t(gx) * gz;
+    uint64_t nsplit = (uint64_t(num_sms) * 8 + per - 1) / per;
+    const uint64_t unit = 32ull * phases;
+    const uint64_t max_split = (a.nb + unit - 1) / unit;
+    if (nsplit > max_split) nsplit = max_split;
+    while (nsplit > 1 && nsplit * out_bytes > part_bytes) nsplit = (nsplit + 1) / 2;
+    if (nsplit < 1) nsplit = 1;
+    uint64_t bpc = (a.nb + nsplit - 1) / nsplit;
+    bpc = (bpc + unit - 1) / unit * unit;
+    nsplit = (a.nb + bpc - 1) / bpc;
+    if (nsplit < 1) nsplit = 1;
+    k_scan_direct<RPT><<<dim3(gz, gx, uint32_t(nsplit)), DIRECT_NT, 0, a.stream>>>(
+        a.db, a.nb, a.S, a.q, a.q_stride, a.B, part, uint32_t(bpc), cw);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    *nsplit_out = uint32_t(nsplit);
+    return launch_reduce_parts(part, uint32_t(nsplit), out_bytes, a.out, num_sms, a.stream);
+}
+
+cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
+                               uint32_t* nsplit_out) {
+    if (a.B <= 1) return launch_direct_t<1>(a, part, part_bytes, num_sms, nsplit_out);
+    if (a.B <= 2) return launch_direct_t<2>(a, part, part_bytes, num_sms, nsplit_out);
+    if (a.B <= 4) return launch_direct_t<4>(a, part, part_bytes, num_sms, nsplit_out);
+    if (a.B <= 8) return launch_direct_t<8>(a, part, part_bytes, num_sms, nsplit_out);
+    return launch_direct_t<16>(a, part, part_bytes, num_sms, nsplit_out);
+}
+
+}  // namespace xpir

@@ -61,70 +61,6 @@ __device__ __forceinline__ void red_xor64(uint8_t* p, uint64_t v) {
     atomicXor(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
 }
 
-// ---------------------------------------------------------------------------
-// K1 (small batches): direct select-XOR, 16-byte words, selection bits from
-// 32-bucket query words. Grid: x = column blocks of 128 threads x 16 B,
-// y = bucket splits, z = request tiles of RPT. Each split writes its partial
-// into part[split][B][S] (plain stores), reduced by k_reduce_parts.
-// ---------------------------------------------------------------------------
-template <int RPT>
-__global__ void __launch_bounds__(128)
-k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ q,
-              uint64_t q_stride, uint32_t B, uint8_t* __restrict__ part, uint32_t buckets_per_split) {
-    const uint32_t ncol = S / 16;
-    const uint32_t col = blockIdx.x * 128 + threadIdx.x;
-    const uint32_t split = blockIdx.y;
-    const uint32_t r0 = blockIdx.z * RPT;
-    const uint32_t j0 = split * buckets_per_split;
-    const uint32_t j1 = min(nb, j0 + buckets_per_split);
-    uint4 acc[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[i] = make_uint4(0, 0, 0, 0);
-    const bool active = col < ncol;
-    const uint4* dbw = reinterpret_cast<const uint4*>(db) + col;
-    for (uint32_t jc = j0; jc < j1; jc += 32) {
-        uint32_t qw[RPT];
-        const uint32_t nvalid = min(32u, j1 - jc);
-        const uint32_t vmask = nvalid == 32 ? 0xffffffffu : ((1u << nvalid) - 1u);
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            uint32_t w = 0;
-            if (r0 + i < B) {
-                const uint8_t* qp = q + uint64_t(r0 + i) * q_stride + (jc >> 3);
-                // jc is a multiple of 8 (split sizes are multiples of 32)
-                const uint32_t nbytes = (nvalid + 7) >> 3;
-#pragma unroll
-                for (uint32_t k = 0; k < 4; ++k)
-                    if (k < nbytes) w |= uint32_t(__ldg(qp + k)) << (8 * k);
-            }
-            qw[i] = w & vmask;
-        }
-        if (!active) continue;
-        uint32_t any = 0;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) any |= qw[i];
-#pragma unroll 4
-        for (uint32_t jj = 0; jj < nvalid; ++jj) {
-            const uint4 v = __ldcs(dbw + uint64_t(jc + jj) * ncol);
-#pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-                const uint32_t m = 0u - ((qw[i] >> jj) & 1u);
-                acc[i].x ^= v.x & m;
-                acc[i].y ^= v.y & m;
-                acc[i].z ^= v.z & m;
-                acc[i].w ^= v.w & m;
-            }
-        }
-        (void)any;
-    }
-    if (!active) return;
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-        if (r0 + i < B)
-            reinterpret_cast<uint4*>(part + (uint64_t(split) * B + r0 + i) * S)[col] = acc[i];
-    }
-}
-
 // Byte-granular fallback for bucket sizes that are not a multiple of 16 (the
 // reference's own tests use 1-, 8- and 12-byte buckets). One thread per
 // (request, byte).
@@ -348,35 +284,13 @@ cudaError_t run_peak_kernels(int num_sms, double* lop3_per_s, double* smem_bps, 
 // ---------------------------------------------------------------------------
 // host-side launchers
 // ---------------------------------------------------------------------------
-cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
-                               uint32_t* nsplit_out) {
-    constexpr int RPT = 8;
-    const uint32_t ncol = a.S / 16;
-    const uint32_t gx = (ncol + 127) / 128;
-    const uint32_t gz = (a.B + RPT - 1) / RPT;
-    // enough CTAs for ~8 per SM, split sizes a multiple of 32 buckets
-    uint64_t want = uint64_t(num_sms) * 8;
-    uint64_t per = uint64_t(gx) * gz;
-    uint32_t nsplit = uint32_t((want + per - 1) / per);
-    const uint32_t max_split = (a.nb + 31) / 32;
-    if (nsplit > max_split) nsplit = max_split;
-    if (nsplit < 1) nsplit = 1;
-    const uint64_t out_bytes = uint64_t(a.B) * a.S;
-    while (nsplit > 1 && uint64_t(nsplit) * out_bytes > part_bytes) nsplit = (nsplit + 1) / 2;
-    uint32_t bps = (a.nb + nsplit - 1) / nsplit;
-    bps = (bps + 31) & ~31u;
-    nsplit = (a.nb + bps - 1) / bps;
-    if (nsplit < 1) nsplit = 1;
-    k_scan_direct<RPT><<<dim3(gx, nsplit, gz), 128, 0, a.stream>>>(a.db, a.nb, a.S, a.q, a.q_stride,
-                                                                    a.B, part, bps);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+cudaError_t launch_reduce_parts(const uint8_t* part, uint32_t nsplit, uint64_t out_bytes, uint8_t* out,
+                                int num_sms, cudaStream_t s) {
     const uint64_t n16 = out_bytes / 16;
     uint32_t rg = uint32_t((n16 + 255) / 256);
     if (rg > uint32_t(num_sms) * 16) rg = uint32_t(num_sms) * 16;
     if (rg < 1) rg = 1;
-    k_reduce_parts<<<rg, 256, 0, a.stream>>>(part, nsplit, out_bytes, a.out);
-    *nsplit_out = nsplit;
+    k_reduce_parts<<<rg, 256, 0, s>>>(part, nsplit, out_bytes, out);
     return cudaGetLastError();
 }
 
