@@ -445,17 +445,13 @@ static int run_rows(xpir_store* st, int kernel, const uint8_t* qwin, uint64_t st
         g_last_kernel = 3;
         return XPIR_OK;
     }
-    // direct: partial buffer sized for up to 64 splits, capped at 256 MiB
-    const uint64_t out_bytes = uint64_t(B) * st->S;
-    uint64_t part_bytes = std::min<uint64_t>(out_bytes * 64, uint64_t(256) << 20);
-    part_bytes = std::max(part_bytes, out_bytes);
-    XCK(st->part.ensure(part_bytes));
+    // direct: CTAs XOR their partials straight into `out` (no partial buffer)
     uint32_t nsplit = 0;
     cudaEvent_t ev;
     timing_begin(s, &ev);
-    XCK(launch_scan_direct(a, st->part.as<uint8_t>(), st->part.cap, num_sms(st->device), &nsplit));
+    XCK(launch_scan_direct(a, nullptr, 0, num_sms(st->device), &nsplit));
     timing_end(s, ev);
-    count_launches(2);
+    count_launches(1);
     g_last_kernel = 1;
     return XPIR_OK;
 }

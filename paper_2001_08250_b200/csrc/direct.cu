@@ -9,8 +9,8 @@
 // thread has a long, independent, unrolled stream of 16-byte loads in flight.
 // Selection bits come from 32-bucket query words, bit-reversed so each bucket's
 // all-ones/zero mask is one arithmetic shift. Phases are XOR-reduced in shared
-// memory and each CTA writes its partial answers to part[split] (plain stores;
-// k_reduce_parts XORs the splits into `out` — deterministic, no atomics).
+// memory and each CTA XORs its partial answers into `out` with 64-bit atomicXor
+// (XOR is associative and commutative, so the result is order-independent).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -24,7 +24,7 @@ constexpr int DIRECT_NT = 256;
 template <int RPT>
 __global__ void __launch_bounds__(DIRECT_NT)
 k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ q,
-              uint64_t q_stride, uint32_t B, uint8_t* __restrict__ part, uint32_t bpc, uint32_t cw) {
+              uint64_t q_stride, uint32_t B, uint8_t* __restrict__ out, uint32_t bpc, uint32_t cw) {
     constexpr int RB = RPT < 8 ? RPT : 8;  // requests reduced per shared-memory round
     __shared__ uint4 red[DIRECT_NT * RB];
     const uint32_t ncol = S / 16;
@@ -114,7 +114,12 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
     if (p == 0 && active) {
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
-            if (r0 + i < B) reinterpret_cast<uint4*>(part + (uint64_t(split) * B + r0 + i) * S)[c] = acc[i];
+            if (r0 + i < B) {
+                unsigned long long* o =
+                    reinterpret_cast<unsigned long long*>(out + uint64_t(r0 + i) * S + uint64_t(c) * 16);
+                atomicXor(o, (unsigned long long)acc[i].y << 32 | acc[i].x);
+                atomicXor(o + 1, (unsigned long long)acc[i].w << 32 | acc[i].z);
+            }
     }
 }
 
@@ -133,18 +138,18 @@ static cudaError_t launch_direct_t(const ScanArgs& a, uint8_t* part, uint64_t pa
     const uint64_t unit = 32ull * phases;
     const uint64_t max_split = (a.nb + unit - 1) / unit;
     if (nsplit > max_split) nsplit = max_split;
-    while (nsplit > 1 && nsplit * out_bytes > part_bytes) nsplit = (nsplit + 1) / 2;
     if (nsplit < 1) nsplit = 1;
     uint64_t bpc = (a.nb + nsplit - 1) / nsplit;
     bpc = (bpc + unit - 1) / unit * unit;
     nsplit = (a.nb + bpc - 1) / bpc;
     if (nsplit < 1) nsplit = 1;
     k_scan_direct<RPT><<<dim3(gz, gx, uint32_t(nsplit)), DIRECT_NT, 0, a.stream>>>(
-        a.db, a.nb, a.S, a.q, a.q_stride, a.B, part, uint32_t(bpc), cw);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+        a.db, a.nb, a.S, a.q, a.q_stride, a.B, a.out, uint32_t(bpc), cw);
     *nsplit_out = uint32_t(nsplit);
-    return launch_reduce_parts(part, uint32_t(nsplit), out_bytes, a.out, num_sms, a.stream);
+    (void)part;
+    (void)part_bytes;
+    (void)out_bytes;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
