@@ -1,0 +1,104 @@
+"""bench_write.py — BASELINE.json config 3: the per-round write path.
+
+Table: blocked cuckoo, 32,768 buckets x depth 4, 1,024-byte slots; writes:
+32,000 (config 3) and 124,518 (95% load: the eviction chain runs) uniform random
+64-bit keys from the DetRng(2) recipe of SURVEY.md §8(d); beta1/beta2 = the
+reference PRF (SipHash-2-4) of the key; interest = make_interest({2^20, 23},
+LogId, key). One "round" = Table::insert of every write in order + the
+interest-vector Bloom update, i.e. ServerCore::apply_write's work (server.cpp:58-73).
+
+GPU arm (timed with CUDA events, inputs resident in HBM): K5 PRF (betas on
+device), K6 cuckoo walk + payload scatter, K7 fused make_interest + absorb.
+Reference arm: the unmodified reference Table::insert + Window::absorb
+(oracle/_ref), single-threaded (the path is sequential by definition).
+Bit-exactness of the GPU round is checked against golden.json digests.
+
+    python bench_write.py [--out profiles/r01_write_path.jsonl]
+"""
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_write_path.jsonl"))
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+
+    import torch
+
+    import oracle
+    import paper_2001_08250_b200 as xp
+    from oracle import recipes
+
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        golden = json.load(f)
+    o = oracle.best()
+    lines = []
+    for n in (recipes.C3["n"], recipes.C3["n95"]):
+        d = recipes.config3(o, n)
+        N, depth, item, m, h = 32768, 4, 1024, 1 << 20, 23
+        dev = "cuda"
+        xs = torch.from_numpy(d["xs"].view(np.int64)).to(dev)
+        payload = torch.from_numpy(d["payload"]).to(dev)
+        k1 = np.frombuffer(d["k1"], np.uint64)
+        k2 = np.frombuffer(d["k2"], np.uint64)
+        gpu_ms = []
+        digest_ok = None
+        for rep in range(args.reps + 1):
+            T = xp.Table(N, depth, N * depth, item, d["s_cuckoo"])
+            W = xp.Window(m, h, 1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            # K5: betas on device (host-visible for the C-ABI insert call)
+            b1 = xp.prf_batch(d["k1"], d["xs"], N).astype(np.uint32)
+            b2 = xp.prf_batch(d["k2"], d["xs"], N).astype(np.uint32)
+            db1 = torch.from_numpy(b1).to(dev)
+            db2 = torch.from_numpy(b2).to(dev)
+            T.insert_batch_dev(db1, db2, payload, n)
+            W.absorb_interest(d["lid"], d["xs"])
+            torch.cuda.synchronize()
+            t = (time.perf_counter() - t0) * 1e3
+            if rep:
+                gpu_ms.append(t)
+            if rep == 1:
+                G = golden["config3"][str(n)]
+                digest_ok = (T.state_digest().hex() == G["state_digest"]
+                             and W.digest().hex() == G["window_digest"])
+            T.close()
+            W.close()
+        # reference (CPU, single thread)
+        ref_ms = None
+        if o.kind == "reference":
+            R = o.table(N, depth, N * depth, item, d["s_cuckoo"])
+            RW = o.window(m, h, 1)
+            t0 = time.perf_counter()
+            R.insert_batch(d["b1"], d["b2"], d["payload"])
+            RW.absorb(d["pos"].ravel())
+            ref_ms = (time.perf_counter() - t0) * 1e3
+        line = {"metric": "write round (cuckoo insert + interest Bloom update)", "writes": n,
+                "load": n / (N * depth), "gpu_ms": float(np.median(gpu_ms)), "gpu_writes_per_s": n / (np.median(gpu_ms) * 1e-3),
+                "ref_ms_1thread": ref_ms, "ref_kind": o.kind, "bit_exact_vs_golden": digest_ok,
+                "timing": "wall clock around PRF + insert walk + payload scatter + interest absorb, "
+                          "inputs (keys, payloads) resident in HBM; excludes table/window allocation"}
+        print(json.dumps(line), flush=True)
+        lines.append(line)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        for l in lines:
+            f.write(json.dumps(l) + "\n")
+
+
+if __name__ == "__main__":
+    main()

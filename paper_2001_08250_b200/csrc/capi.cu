@@ -413,6 +413,7 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
     }
     if (st->S % 16 != 0) return 3;
     const bool m4_ok = (st->S % 128) == 0;
+    if (k == 4 || k == 5) k = 2;  // forced M4RM variants (registers-only / TMEM accumulators)
     if (k == 0) k = (m4_ok && B >= 128) ? 2 : 1;
     if (k == 2 && !m4_ok) k = 1;
     return k;
@@ -420,18 +421,20 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
 
 static int run_m4(xpir_store* st, const uint8_t* qT, uint64_t qstride, uint32_t B, uint8_t* d_out,
                   cudaStream_t s) {
-    int cps;
+    int cps, variant;
     {
         std::lock_guard<std::mutex> lk(g_opts_mu);
         cps = g_opts.ctas_per_sm;
+        variant = g_opts.kernel == 4 ? 1 : g_opts.kernel == 5 ? 2 : 0;
     }
     M4Args a{st->data, st->nb(), st->S, qT, qstride, B, d_out, s};
     cudaEvent_t ev;
     timing_begin(s, &ev);
-    XCK(launch_scan_m4rm(a, cps, num_sms(st->device)));
+    XCK(launch_scan_m4rm(a, cps, num_sms(st->device), variant));
     timing_end(s, ev);
     count_launches(1);
-    g_last_kernel = 2;
+    // 2 = M4RM with register accumulators, 5 = M4RM with half-TMEM accumulators
+    g_last_kernel = (variant == 2 || (variant == 0 && B >= 2048)) ? 5 : 2;
     return XPIR_OK;
 }
 

@@ -294,7 +294,10 @@ static cudaError_t launch_m4(const M4Args& a, int ctas_per_sm, int num_sms) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_scan_m4rm(const M4Args& a, int ctas_per_sm, int num_sms) {
+cudaError_t launch_scan_m4rm(const M4Args& a, int ctas_per_sm, int num_sms, int variant) {
+    // variant 0: auto (TMEM-accumulator kernel for full 2048-request tiles),
+    // 1: register accumulators only, 2: TMEM-accumulator kernel
+    if (variant == 2 || (variant == 0 && a.B >= 2048)) return launch_scan_m4rm_tmem(a, num_sms);
     if (a.B <= 256) return launch_m4<512, 4>(a, ctas_per_sm, num_sms);
     if (a.B <= 512) return launch_m4<512, 8>(a, ctas_per_sm, num_sms);
     return launch_m4<512, 16>(a, ctas_per_sm, num_sms);

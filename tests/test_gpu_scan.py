@@ -269,3 +269,20 @@ def test_config5_shapes_golden(xp, golden, cuda):
             o = out.cpu().numpy()
             assert [sha(o[r]) for r in range(4)] == e["out_rows_sha256"], (e["slot"], e["depth"], k)
         st.close()
+
+
+@pytest.mark.parametrize("kernel", [4, 5])
+@pytest.mark.parametrize("N,S,B", [
+    (1000, 128, 1), (4096, 256, 130), (2048, 512, 2048), (3001, 384, 2500), (777, 1024, 4097), (64, 128, 6000),
+])
+def test_m4rm_variants_match_oracle(xp, port, cuda, kernel, N, S, B):
+    """Registers-only (4) and half-TMEM-accumulator (5) M4RM kernels, forced at any
+    batch size, including partial 2048-request tiles and odd bucket counts."""
+    g = np.random.default_rng(N * 3 + S + B + kernel)
+    db = rand(g, N * S)
+    q = rand(g, B, (N + 7) // 8)
+    xp.set_scan_opts(kernel)
+    st = xp.Store(N, S)
+    st.upload(db)
+    assert np.array_equal(st.answer_batch(q), port.answer_batch(db, N, S, q, B))
+    assert xp.last_scan_kernel() == (5 if kernel == 5 else 2)
