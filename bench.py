@@ -337,7 +337,8 @@ def main():
     lookups = B * (nb // 8) * (BUCKET_BYTES // 4)  # M4RM: one 4-byte table word per (request, group, word)
     roof = {
         "bound": "alu",
-        "kernel": {1: "k_scan_direct", 2: "k_scan_m4rm", 5: "k_scan_m4rm_tmem"}.get(xp.last_scan_kernel(), "?"),
+        "kernel": {1: "k_scan_direct", 2: "k_scan_m4rm", 5: "k_scan_m4rm_tmem",
+                   6: "k_scan_nib"}.get(xp.last_scan_kernel(), "?"),
         "unit": "Tops/s (32-bit masked-XOR lane ops)",
         "achieved": achieved / 1e12,
         "peak": peaks["lop3_per_s"] / 1e12,

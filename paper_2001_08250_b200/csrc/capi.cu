@@ -405,6 +405,11 @@ uint64_t xpir_query_window_bytes(const xpir_store* st) {
 // queries), 1 = direct select-XOR (S % 16 == 0; row-major query window),
 // 3 = byte-granular (any S).
 // ---------------------------------------------------------------------------
+// Batch-size crossovers (config-5 sweep): direct below
+// g_nib_min_batch, nibble tables below g_m4_min_batch, byte tables above.
+static uint32_t g_nib_min_batch = 8;
+static uint32_t g_m4_min_batch = 160;
+
 static int choose_kernel(const xpir_store* st, uint32_t B) {
     int k;
     {
@@ -414,8 +419,8 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
     if (st->S % 16 != 0) return 3;
     const bool m4_ok = (st->S % 128) == 0;
     if (k == 4 || k == 5) k = 2;  // forced M4RM variants (registers-only / TMEM accumulators)
-    if (k == 0) k = (m4_ok && B >= 128) ? 2 : 1;
-    if (k == 2 && !m4_ok) k = 1;
+    if (k == 0) k = !m4_ok ? 1 : B >= g_m4_min_batch ? 2 : B >= g_nib_min_batch ? 6 : 1;
+    if ((k == 2 || k == 6) && !m4_ok) k = 1;
     return k;
 }
 
@@ -446,6 +451,15 @@ static int run_rows(xpir_store* st, int kernel, const uint8_t* qwin, uint64_t st
         XCK(launch_scan_bytes(a));
         count_launches(1);
         g_last_kernel = 3;
+        return XPIR_OK;
+    }
+    if (kernel == 6) {
+        cudaEvent_t ev;
+        timing_begin(s, &ev);
+        XCK(launch_scan_nib(a, num_sms(st->device)));
+        timing_end(s, ev);
+        count_launches(1);
+        g_last_kernel = 6;
         return XPIR_OK;
     }
     // direct: CTAs XOR their partials straight into `out` (no partial buffer)

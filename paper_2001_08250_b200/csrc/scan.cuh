@@ -43,6 +43,7 @@ cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byt
 cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
                                uint32_t* nsplit_out);
 cudaError_t launch_scan_bytes(const ScanArgs& a);
+cudaError_t launch_scan_nib(const ScanArgs& a, int num_sms);  // nib.cu, S % 128 == 0
 cudaError_t launch_reduce_parts(const uint8_t* part, uint32_t nsplit, uint64_t out_bytes, uint8_t* out,
                                 int num_sms, cudaStream_t s);
 cudaError_t launch_init_out(uint8_t* out, uint32_t B, uint32_t S, const uint8_t* mask_seeds,

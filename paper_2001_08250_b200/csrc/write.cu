@@ -137,19 +137,35 @@ __global__ void k_absorb(const uint32_t* __restrict__ pos, uint64_t n,
 //   origin == -1  : cleared (zero)
 //   origin <= -2  : the pre-batch content of flat slot (-origin - 2)
 // ---------------------------------------------------------------------------
-constexpr uint32_t WALK_SMEM_MAX_SLOTS = 96 * 1024 * 8;  // bit-packed: 96 KiB each map
+constexpr uint32_t WALK_SMEM_MAX_SLOTS = 64 * 1024 * 8;  // bit-packed: 64 KiB each map
 constexpr uint32_t WALK_MIN_DRAWS = 640;  // >= 1 + 500 draws of one insert, with slack
+constexpr uint32_t WALK_DRAWS_SMEM = 4096;  // draws staged in shared memory per launch
+constexpr uint32_t WALK_CHUNK = 2048;       // inserts whose buckets are staged per round
 
+// Shared memory: [used bits][touched bits] (when use_smem) | draws[4096] u64 |
+// beta1[2048] | beta2[2048] | flag. All threads stage; thread 0 walks. Every
+// load on thread 0's critical path is a shared-memory load except the victim
+// metadata of an eviction hop (one dependent L2 access per hop).
 __global__ void __launch_bounds__(256)
 k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __restrict__ beta1,
               const uint32_t* __restrict__ beta2, uint64_t i0, uint64_t n,
               uint32_t* __restrict__ reports, int use_smem) {
-    extern __shared__ uint32_t sm[];
+    extern __shared__ __align__(16) uint32_t sm[];
     const uint64_t slots = uint64_t(d.buckets) * d.depth;
-    const uint32_t words = uint32_t((slots + 31) / 32);
+    const uint32_t words = use_smem ? uint32_t((slots + 31) / 32) : 0;
     uint32_t* used_bits = sm;
     uint32_t* touch_bits = sm + words;
-    CuckooState s = *gst;
+    uint64_t* dr = reinterpret_cast<uint64_t*>(sm + ((2 * words + 3) & ~3u));
+    uint32_t* sb1 = reinterpret_cast<uint32_t*>(dr + WALK_DRAWS_SMEM);
+    uint32_t* sb2 = sb1 + WALK_CHUNK;
+    uint32_t* stop = sb2 + WALK_CHUNK;
+    __shared__ CuckooState sh_state;
+    if (threadIdx.x == 0) {
+        sh_state = *gst;
+        *stop = 0;
+    }
+    __syncthreads();
+    CuckooState s = sh_state;  // thread 0 mutates its register copy; the others only read it
     if (use_smem) {
         for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
             uint32_t v = 0;
@@ -165,9 +181,13 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
             const uint32_t f = d.touched[k];
             atomicOr(&touch_bits[f >> 5], 1u << (f & 31));
         }
-        __syncthreads();
     }
-    if (threadIdx.x != 0) return;
+    // the next WALK_DRAWS_SMEM draws (nonces rng_block ..) from the global window
+    const uint64_t dr_base = s.rng_block;
+    const uint64_t avail = (s.draw_base + s.draw_count > s.rng_block) ? s.draw_base + s.draw_count - s.rng_block : 0;
+    const uint32_t dr_count = uint32_t(avail < WALK_DRAWS_SMEM ? avail : WALK_DRAWS_SMEM);
+    for (uint32_t k = threadIdx.x; k < dr_count; k += blockDim.x) dr[k] = d.draws[dr_base - s.draw_base + k];
+    __syncthreads();
 
     const uint64_t fmask = d.fifo_cap - 1;
     auto is_used = [&](uint32_t f) -> bool {
@@ -215,89 +235,97 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
     auto uniform = [&](uint64_t bound) -> uint64_t {  // rng.cpp:9-16 over DetRng::fill draws
         const uint64_t tail = (~uint64_t(0) % bound + 1) % bound;
         for (;;) {
-            const uint64_t v = d.draws[s.rng_block - s.draw_base];
+            const uint64_t v = dr[s.rng_block - dr_base];
             s.rng_block++;
             if (tail == 0 || v <= ~uint64_t(0) - tail) return v % bound;
         }
     };
 
-    s.status = 0;
+    if (threadIdx.x == 0) s.status = 0;
     uint64_t i = i0;
-    uint32_t nb1 = i < n ? beta1[i] : 0, nb2 = i < n ? beta2[i] : 0;
-    for (; i < n; ++i) {
-        const uint32_t b1 = nb1, b2 = nb2;
-        if (i + 1 < n) {  // prefetch the next item's buckets
-            nb1 = beta1[i + 1];
-            nb2 = beta2[i + 1];
+    for (uint64_t c0 = i0; c0 < n; c0 += WALK_CHUNK) {
+        const uint32_t cn = uint32_t((n - c0) < WALK_CHUNK ? (n - c0) : WALK_CHUNK);
+        for (uint32_t k = threadIdx.x; k < cn; k += blockDim.x) {
+            sb1[k] = beta1[c0 + k];
+            sb2[k] = beta2[c0 + k];
         }
-        if (s.rng_block + WALK_MIN_DRAWS > s.draw_base + s.draw_count) {
-            s.status = 1;  // host refills draws from nonce s.rng_block and resumes at i
-            break;
-        }
-        uint32_t stored = 0, dropped = 0, gc = 0, disp = 0;
-        s.writes++;                                 // :62
-        if (s.live == d.capacity) {                 // :64-69 FIFO GC of the oldest entry
-            while (d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
-            clear(uint32_t(d.fifo[s.fifo_head & fmask]));
-            gc = 1;
-        }
-        const uint64_t stamp = s.next_stamp++;     // :71
-        if (stamp - s.fifo_head >= d.fifo_cap) {
-            s.status = 2;
-            break;
-        }
-        int fs = free_slot(b1);                     // :73-84
-        if (fs >= 0) {
-            place(b1 * d.depth + fs, b1, b2, stamp, int64_t(i));
-            stored = 1;
-        } else if ((fs = free_slot(b2)) >= 0) {
-            place(b2 * d.depth + fs, b1, b2, stamp, int64_t(i));
-            stored = 1;
-        } else {                                    // :86-125 random-walk eviction
-            uint32_t be = uniform(2) == 0 ? b1 : b2;
-            uint32_t c1 = b1, c2 = b2;
-            uint64_t cst = stamp;
-            int64_t corg = int64_t(i);
-            bool carry_incoming = true, incoming_stored = false, done = false;
-            for (uint32_t hops = 0;; ++hops) {
-                const int f2 = free_slot(be);
-                if (f2 >= 0) {
-                    place(be * d.depth + f2, c1, c2, cst, corg);
-                    if (carry_incoming) incoming_stored = true;
-                    stored = incoming_stored;
-                    disp = hops;
-                    done = true;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (uint32_t k = 0; k < cn; ++k, ++i) {
+                const uint32_t b1 = sb1[k], b2 = sb2[k];
+                if (s.rng_block + WALK_MIN_DRAWS > dr_base + dr_count) {
+                    s.status = 1;  // host refills / re-stages draws from nonce s.rng_block and resumes at i
+                    *stop = 1;
                     break;
                 }
-                if (hops == XPIR_MAX_DISPLACEMENTS_DEV) break;
-                const uint32_t vs = uint32_t(uniform(d.depth));
-                const uint32_t vf = be * d.depth + vs;
-                const uint32_t v1 = d.beta1[vf], v2 = d.beta2[vf];
-                const uint64_t vst = d.stamp[vf];
-                const int64_t vorg = origin_of(vf);
-                clear(vf);
-                place(vf, c1, c2, cst, corg);
-                if (carry_incoming) incoming_stored = true;
-                c1 = v1;
-                c2 = v2;
-                cst = vst;
-                corg = vorg;
-                carry_incoming = false;
-                be = v1 == be ? v2 : v1;            // :118
-            }
-            if (!done) {                            // :122-125
-                disp = XPIR_MAX_DISPLACEMENTS_DEV;
-                dropped = 1;
-                stored = incoming_stored;
+                uint32_t stored = 0, dropped = 0, gc = 0, disp = 0;
+                s.writes++;                                 // :62
+                if (s.live == d.capacity) {                 // :64-69 FIFO GC of the oldest entry
+                    while (d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
+                    clear(uint32_t(d.fifo[s.fifo_head & fmask]));
+                    gc = 1;
+                }
+                const uint64_t stamp = s.next_stamp++;     // :71
+                if (stamp - s.fifo_head >= d.fifo_cap) {
+                    s.status = 2;
+                    *stop = 1;
+                    break;
+                }
+                int fs = free_slot(b1);                     // :73-84
+                if (fs >= 0) {
+                    place(b1 * d.depth + fs, b1, b2, stamp, int64_t(i));
+                    stored = 1;
+                } else if ((fs = free_slot(b2)) >= 0) {
+                    place(b2 * d.depth + fs, b1, b2, stamp, int64_t(i));
+                    stored = 1;
+                } else {                                    // :86-125 random-walk eviction
+                    uint32_t be = uniform(2) == 0 ? b1 : b2;
+                    uint32_t c1 = b1, c2 = b2;
+                    uint64_t cst = stamp;
+                    int64_t corg = int64_t(i);
+                    bool carry_incoming = true, incoming_stored = false, done = false;
+                    for (uint32_t hops = 0;; ++hops) {
+                        const int f2 = free_slot(be);
+                        if (f2 >= 0) {
+                            place(be * d.depth + f2, c1, c2, cst, corg);
+                            if (carry_incoming) incoming_stored = true;
+                            stored = incoming_stored;
+                            disp = hops;
+                            done = true;
+                            break;
+                        }
+                        if (hops == XPIR_MAX_DISPLACEMENTS_DEV) break;
+                        const uint32_t vs = uint32_t(uniform(d.depth));
+                        const uint32_t vf = be * d.depth + vs;
+                        const uint32_t v1 = d.beta1[vf], v2 = d.beta2[vf];
+                        const uint64_t vst = d.stamp[vf];
+                        const int64_t vorg = origin_of(vf);
+                        clear(vf);
+                        place(vf, c1, c2, cst, corg);
+                        if (carry_incoming) incoming_stored = true;
+                        c1 = v1;
+                        c2 = v2;
+                        cst = vst;
+                        corg = vorg;
+                        carry_incoming = false;
+                        be = v1 == be ? v2 : v1;            // :118
+                    }
+                    if (!done) {                            // :122-125
+                        disp = XPIR_MAX_DISPLACEMENTS_DEV;
+                        dropped = 1;
+                        stored = incoming_stored;
+                    }
+                }
+                if (reports) reinterpret_cast<uint4*>(reports)[i] = make_uint4(stored, dropped, gc, disp);
             }
         }
-        if (reports) {
-            uint4 r = make_uint4(stored, dropped, gc, disp);
-            reinterpret_cast<uint4*>(reports)[i] = r;
-        }
+        __syncthreads();
+        if (*stop) break;
     }
-    s.resume_at = i;
-    *gst = s;
+    if (threadIdx.x == 0) {
+        s.resume_at = i;
+        *gst = s;
+    }
 }
 
 // phase 1: stage pre-existing payloads that moved (origin <= -2) into d.gather[k]
@@ -411,12 +439,10 @@ cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32
                                cudaStream_t s) {
     const uint64_t slots = uint64_t(d.buckets) * d.depth;
     const bool use_smem = slots <= WALK_SMEM_MAX_SLOTS;
-    const size_t smem = use_smem ? 2 * ((slots + 31) / 32) * 4 : 0;
-    if (use_smem && smem > 48 * 1024) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k_cuckoo_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        if (e != cudaSuccess) return e;
-    }
+    const size_t words = use_smem ? (slots + 31) / 32 : 0;
+    const size_t smem = ((2 * words + 3) & ~size_t(3)) * 4 + WALK_DRAWS_SMEM * 8 + 2 * WALK_CHUNK * 4 + 16;
+    cudaError_t e = cudaFuncSetAttribute(k_cuckoo_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
     k_cuckoo_walk<<<1, 256, smem, s>>>(d, st, beta1, beta2, i0, n, reports, use_smem ? 1 : 0);
     return cudaGetLastError();
 }
