@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -405,10 +406,12 @@ uint64_t xpir_query_window_bytes(const xpir_store* st) {
 // queries), 1 = direct select-XOR (S % 16 == 0; row-major query window),
 // 3 = byte-granular (any S).
 // ---------------------------------------------------------------------------
-// Batch-size crossovers (config-5 sweep): direct below
-// g_nib_min_batch, nibble tables below g_m4_min_batch, byte tables above.
-static uint32_t g_nib_min_batch = 8;
-static uint32_t g_m4_min_batch = 160;
+// Batch-size crossovers from the config-5 sweep: the byte-table
+// M4RM kernels from 128 requests; below, the direct kernel. The warp-private
+// nibble-table kernel (6) measured slower than direct at every B in [8, 128)
+// (latency-bound), so it is selectable but not chosen automatically.
+static uint32_t g_nib_min_batch = 0xffffffffu;
+static uint32_t g_m4_min_batch = 128;
 
 static int choose_kernel(const xpir_store* st, uint32_t B) {
     int k;
@@ -755,6 +758,8 @@ struct xpir_table {
     uint8_t* data = nullptr;
     cudaStream_t stream = nullptr;
     DevBuf in_b1, in_b2, in_payload, in_reports, gather;
+    CuckooParScratch par;
+    bool parallel_prefix = true;  // XPIR_CUCKOO_SEQUENTIAL=1 disables (A/B checks)
     std::mutex mu;
     uint64_t slots() const { return uint64_t(d.buckets) * d.depth; }
 };
@@ -778,6 +783,7 @@ static void table_free_all(xpir_table* t) {
     t->in_payload.release();
     t->in_reports.release();
     t->gather.release();
+    t->par.release();
     if (t->stream) cudaStreamDestroy(t->stream);
 }
 
@@ -833,6 +839,7 @@ int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t cap
                     std::string("table_create: ") + cudaGetErrorString(e));
     }
     t->h = CuckooState{};
+    if (const char* ev = std::getenv("XPIR_CUCKOO_SEQUENTIAL")) t->parallel_prefix = ev[0] != '1';
     *out = t;
     return XPIR_OK;
 }
@@ -857,6 +864,15 @@ int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint3
     t->h.batch_id += 1;
     t->h.n_touched = 0;
     uint64_t i = 0;
+    // K6a: the eviction-free, GC-free prefix of the round is placed in parallel
+    // (exactly what the sequential walk would do); the walk continues from the
+    // first insert that needs an eviction or a FIFO GC.
+    if (t->parallel_prefix && n >= 64 && t->h.live < t->d.capacity) {
+        const uint64_t room = t->d.capacity - t->h.live;
+        uint64_t applied = 0;
+        XCK(cuckoo_parallel_prefix(t->d, t->h, d_b1, d_b2, n < room ? n : room, d_reports, t->par, &applied, s));
+        i = applied;
+    }
     for (int guard = 0; i < n; ++guard) {
         if (t->h.rng_block + 1024 > t->h.draw_base + t->h.draw_count || guard == 0) {
             // (re)fill the draw window starting at the next unconsumed nonce

@@ -112,4 +112,20 @@ cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32
 cudaError_t launch_cuckoo_apply(const CuckooDev& d, const CuckooState* st_host_copy,
                                 uint8_t* table, const uint8_t* payload, cudaStream_t s);
 
+// Grow-only scratch of the parallel eviction-free prefix (cuckoo_par.cu).
+struct CuckooParScratch {
+    void *keys_a = nullptr, *keys_b = nullptr, *outcome = nullptr, *succ = nullptr;
+    void *slot_of = nullptr, *flags = nullptr, *cub_tmp = nullptr;
+    size_t keys_a_cap = 0, keys_b_cap = 0, outcome_cap = 0, succ_cap = 0, slot_cap = 0, flags_cap = 0,
+           cub_cap = 0;
+    void release() {
+        for (void* p : {keys_a, keys_b, outcome, succ, slot_of, flags, cub_tmp})
+            if (p) cudaFree(p);
+        *this = CuckooParScratch{};
+    }
+};
+cudaError_t cuckoo_parallel_prefix(const CuckooDev& d, CuckooState& h, const uint32_t* b1, const uint32_t* b2,
+                                   uint64_t n, uint32_t* reports, CuckooParScratch& sc, uint64_t* applied,
+                                   cudaStream_t s);
+
 }  // namespace xpir

@@ -156,3 +156,28 @@ def test_seal_into_store_and_read(xp, port, cuda):
     got = st.answer_batch(q)
     for r, b in enumerate(d["b1"][:3]):
         assert np.array_equal(got[r], snap[b])
+
+
+@pytest.mark.parametrize("nb,depth,cap,n,same_frac", [
+    (64, 4, 256, 200, 0.0), (1000, 2, 2000, 1500, 0.1), (37, 3, 111, 90, 0.3), (4096, 4, 16384, 15000, 0.05),
+    (512, 8, 4096, 3000, 0.5), (100, 1, 100, 95, 0.0),
+])
+def test_parallel_prefix_matches_sequential(xp, port, cuda, nb, depth, cap, n, same_frac):
+    """One large batch: the parallel eviction-free prefix (Jacobi-solved claims)
+    followed by the sequential walk must equal the reference order exactly,
+    including beta1 == beta2 items, near-full tables and depth 1."""
+    g = np.random.default_rng(nb * 7 + n)
+    seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+    b1 = g.integers(0, nb, n).astype(np.uint32)
+    b2 = g.integers(0, nb, n).astype(np.uint32)
+    same = g.random(n) < same_frac
+    b2[same] = b1[same]
+    pl = g.integers(0, 256, (n, 16), dtype=np.uint8)
+    T, P = xp.Table(nb, depth, cap, 16, seed), port.table(nb, depth, cap, 16, seed)
+    assert np.array_equal(T.insert_batch(b1, b2, pl), P.insert_batch(b1, b2, pl))
+    _compare_tables(T, P)
+    # a second round on the now-occupied table
+    b1 = g.integers(0, nb, n).astype(np.uint32)
+    b2 = g.integers(0, nb, n).astype(np.uint32)
+    assert np.array_equal(T.insert_batch(b1, b2, pl), P.insert_batch(b1, b2, pl))
+    _compare_tables(T, P)
