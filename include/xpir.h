@@ -162,6 +162,9 @@ int xpir_keystream_rows_dev(int device, const uint8_t key[32], uint64_t nonce0, 
 /* crypto::prf (crypto.cpp:17-33) for n inputs. */
 int xpir_prf_batch(const uint8_t key[16], const uint64_t* inputs, uint64_t n, uint64_t modulus,
                    uint64_t* out);
+/* Same on device buffers; d_out32 (optional) receives the values as uint32 (bucket indices). */
+int xpir_prf_batch_dev(int device, const uint8_t key[16], const uint64_t* d_inputs, uint64_t n,
+                       uint64_t modulus, uint64_t* d_out, uint32_t* d_out32, void* stream);
 /* notify::make_interest (notify.cpp:30-35): out[i*h + k] */
 int xpir_make_interest_batch(uint32_t m_bits, uint32_t h, const uint8_t id[16],
                              const uint64_t* seqs, uint64_t n, uint32_t* out);
@@ -186,6 +189,9 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* beta1, const uint32_t
 int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_beta1, const uint32_t* d_beta2,
                                 const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
                                 void* stream);
+/* Pre-size the per-round scratch (claim sort buffers, payload staging) for
+ * batches of up to max_batch writes, so no allocation happens inside a round. */
+int xpir_table_reserve(xpir_table* t, uint64_t max_batch);
 /* Table::snapshot bytes (cuckoo.cpp:128-135). */
 int xpir_table_snapshot(const xpir_table* t, uint8_t* host_out);
 /* Seal into a store covering the whole table or a bucket range of it (device copy). */
@@ -214,6 +220,8 @@ int xpir_window_absorb_dev(xpir_window* win, const uint32_t* d_positions, uint64
 /* Fused make_interest(bp, id, seq_i) + absorb for n writes (BLAKE2b on device). */
 int xpir_window_absorb_interest(xpir_window* win, const uint8_t id[16], const uint64_t* seqs,
                                 uint64_t n);
+int xpir_window_absorb_interest_dev(xpir_window* win, const uint8_t id[16], const uint64_t* d_seqs,
+                                    uint64_t n, void* stream);
 int xpir_window_rotate(xpir_window* win);
 int xpir_window_info(const xpir_window* win, uint64_t* size, uint64_t* base);
 int xpir_window_delta(const xpir_window* win, uint64_t i, uint64_t* out_words);

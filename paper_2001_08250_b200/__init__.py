@@ -102,6 +102,9 @@ _SIGS = {
     "xpir_keystream_dev": ([C.c_int, _u8p, C.c_uint64, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
     "xpir_keystream_rows_dev": ([C.c_int, _u8p, C.c_uint64, C.c_uint32, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
     "xpir_prf_batch": ([_u8p, _u64p, C.c_uint64, C.c_uint64, _u64p], C.c_int),
+    "xpir_prf_batch_dev": ([C.c_int, _u8p, _vp, C.c_uint64, C.c_uint64, _vp, _vp, _vp], C.c_int),
+    "xpir_table_reserve": ([_vp, C.c_uint64], C.c_int),
+    "xpir_window_absorb_interest_dev": ([_vp, _u8p, _vp, C.c_uint64, _vp], C.c_int),
     "xpir_make_interest_batch": ([C.c_uint32, C.c_uint32, _u8p, _u64p, C.c_uint64, _u32p], C.c_int),
     "xpir_bloom_positions": ([_u8p, C.c_uint64, C.c_uint32, C.c_uint32, _u32p], C.c_int),
     "xpir_blake2b": ([_u8p, C.c_uint64, C.c_uint32, _u8p], C.c_int),
@@ -407,6 +410,12 @@ def prf_batch(key16: bytes, inputs, modulus: int) -> np.ndarray:
     return out[: len(x)]
 
 
+def prf_batch_dev(key16: bytes, d_inputs, n: int, modulus: int, d_out=None, d_out32=None, device: int = 0,
+                  stream=None) -> None:
+    _check(lib().xpir_prf_batch_dev(device, _p(_u8(key16)), _ptr(d_inputs), n, modulus, _ptr(d_out),
+                                    _ptr(d_out32), _stream(stream)))
+
+
 def make_interest_batch(m_bits: int, h: int, id16: bytes, seqs) -> np.ndarray:
     s = np.ascontiguousarray(seqs, np.uint64)
     out = np.empty((max(len(s), 1), max(h, 1)), np.uint32)
@@ -467,6 +476,9 @@ class Table:
     def insert_batch_dev(self, d_b1, d_b2, d_payload, n: int, d_reports=None, stream=None) -> None:
         _check(lib().xpir_table_insert_batch_dev(self.h, _ptr(d_b1), _ptr(d_b2), _ptr(d_payload), n,
                                                  _ptr(d_reports), _stream(stream)))
+
+    def reserve(self, max_batch: int) -> None:
+        _check(lib().xpir_table_reserve(self.h, max_batch))
 
     def snapshot(self) -> np.ndarray:
         out = np.empty(self.buckets * self.depth * self.item, np.uint8)
@@ -534,6 +546,9 @@ class Window:
     def absorb_interest(self, id16: bytes, seqs) -> None:
         s = np.ascontiguousarray(seqs, np.uint64)
         _check(lib().xpir_window_absorb_interest(self.h, _p(_u8(id16)), _p(s, _u64p), len(s)))
+
+    def absorb_interest_dev(self, id16: bytes, d_seqs, n: int, stream=None) -> None:
+        _check(lib().xpir_window_absorb_interest_dev(self.h, _p(_u8(id16)), _ptr(d_seqs), n, _stream(stream)))
 
     def rotate(self) -> None:
         _check(lib().xpir_window_rotate(self.h))

@@ -690,11 +690,22 @@ int xpir_prf_batch(const uint8_t key[16], const uint64_t* inputs, uint64_t n, ui
     uint64_t* d = nullptr;
     XCK(cudaMalloc(&d, 16 * n));
     cudaError_t e = cudaMemcpy(d, inputs, 8 * n, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = launch_prf(ld64le(key), ld64le(key + 8), d, n, modulus, d + n, nullptr);
+    if (e == cudaSuccess) e = launch_prf(ld64le(key), ld64le(key + 8), d, n, modulus, d + n, nullptr, nullptr);
     count_launches(1);
     if (e == cudaSuccess) e = cudaMemcpy(out, d + n, 8 * n, cudaMemcpyDeviceToHost);
     cudaFree(d);
     XCK(e);
+    return XPIR_OK;
+}
+
+int xpir_prf_batch_dev(int device, const uint8_t key[16], const uint64_t* d_in, uint64_t n, uint64_t modulus,
+                       uint64_t* d_out, uint32_t* d_out32, void* stream) {
+    if (modulus == 0) return fail(XPIR_EINVAL, "prf: modulus must be positive");
+    if (!key || (n && !d_in)) return fail(XPIR_EINVAL, "prf: null buffer");
+    DeviceGuard g(device);
+    XCK(launch_prf(ld64le(key), ld64le(key + 8), d_in, n, modulus, d_out, d_out32,
+                   static_cast<cudaStream_t>(stream)));
+    count_launches(1);
     return XPIR_OK;
 }
 
@@ -936,6 +947,20 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b
     return XPIR_OK;
 }
 
+int xpir_table_reserve(xpir_table* t, uint64_t max_batch) {
+    if (!t) return fail(XPIR_EINVAL, "table_reserve: null table");
+    std::lock_guard<std::mutex> lk(t->mu);
+    DeviceGuard g(t->device);
+    const uint64_t n = std::min<uint64_t>(max_batch, t->slots());
+    XCK(t->gather.ensure(n * t->d.item));
+    XCK(t->in_b1.ensure(4 * max_batch));
+    XCK(t->in_b2.ensure(4 * max_batch));
+    XCK(t->in_reports.ensure(16 * max_batch));
+    XCK(cuckoo_reserve(t->par, max_batch, t->d.buckets, t->stream));  // claim-sort scratch
+    XCK(cudaStreamSynchronize(t->stream));
+    return XPIR_OK;
+}
+
 int xpir_table_snapshot(const xpir_table* t, uint8_t* host_out) {
     if (!t || !host_out) return fail(XPIR_EINVAL, "table_snapshot: null argument");
     DeviceGuard g(t->device);
@@ -1114,6 +1139,18 @@ int xpir_window_absorb_interest(xpir_window* win, const uint8_t id[16], const ui
                         win->stream));
     count_launches(1);
     XCK(cudaStreamSynchronize(win->stream));
+    return XPIR_OK;
+}
+
+int xpir_window_absorb_interest_dev(xpir_window* win, const uint8_t id[16], const uint64_t* d_seqs, uint64_t n,
+                                    void* stream) {
+    if (!win || !id) return fail(XPIR_EINVAL, "window_absorb_interest: null argument");
+    if (!n) return XPIR_OK;
+    if (!d_seqs) return fail(XPIR_EINVAL, "window_absorb_interest: null buffer");
+    DeviceGuard g(win->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : win->stream;
+    XCK(launch_interest(id, d_seqs, n, win->h, win->m, nullptr, win->deltas.back(), s));
+    count_launches(1);
     return XPIR_OK;
 }
 

@@ -124,10 +124,13 @@ __global__ void k_par_write(CuckooDev d, uint64_t limit, const uint32_t* __restr
 // Runs on the first `n` inserts of a batch whose walk state is `h` (host copy,
 // batch_id set, n_touched == 0, no GC possible within n). Returns the length k
 // of the eviction-free prefix it applied (0 if it declined) and advances h.
-cudaError_t cuckoo_parallel_prefix(const CuckooDev& d, CuckooState& h, const uint32_t* b1, const uint32_t* b2,
-                                   uint64_t n, uint32_t* reports, CuckooParScratch& sc, uint64_t* applied,
-                                   cudaStream_t s) {
-    *applied = 0;
+static int sort_end_bit(uint32_t buckets) {
+    int end_bit = 32;
+    while (end_bit < 64 && (uint64_t(1) << (end_bit - 32)) <= buckets) ++end_bit;
+    return end_bit;
+}
+
+cudaError_t cuckoo_reserve(CuckooParScratch& sc, uint64_t n, uint32_t buckets, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     const uint64_t m = 2 * n;
     cudaError_t e = cudaSuccess;
@@ -146,14 +149,24 @@ cudaError_t cuckoo_parallel_prefix(const CuckooDev& d, CuckooState& h, const uin
     grow(&sc.slot_of, n * 4, sc.slot_cap);
     grow(&sc.flags, 16, sc.flags_cap);
     if (e != cudaSuccess) return e;
-    int end_bit = 32;
-    while (end_bit < 64 && (uint64_t(1) << (end_bit - 32)) <= d.buckets) ++end_bit;
     size_t tmp = 0;
     e = cub::DeviceRadixSort::SortKeys(nullptr, tmp, static_cast<unsigned long long*>(sc.keys_a),
-                                       static_cast<unsigned long long*>(sc.keys_b), int(m), 0, 64, s);
+                                       static_cast<unsigned long long*>(sc.keys_b), int(m), 0,
+                                       sort_end_bit(buckets), s);
     if (e != cudaSuccess) return e;
     grow(&sc.cub_tmp, tmp, sc.cub_cap);
+    return e;
+}
+
+cudaError_t cuckoo_parallel_prefix(const CuckooDev& d, CuckooState& h, const uint32_t* b1, const uint32_t* b2,
+                                   uint64_t n, uint32_t* reports, CuckooParScratch& sc, uint64_t* applied,
+                                   cudaStream_t s) {
+    *applied = 0;
+    if (n == 0) return cudaSuccess;
+    const uint64_t m = 2 * n;
+    cudaError_t e = cuckoo_reserve(sc, n, d.buckets, s);
     if (e != cudaSuccess) return e;
+    const int end_bit = sort_end_bit(d.buckets);
     auto* keys_in = static_cast<unsigned long long*>(sc.keys_a);
     auto* keys = static_cast<unsigned long long*>(sc.keys_b);
     auto* outcome = static_cast<uint8_t*>(sc.outcome);

@@ -63,7 +63,7 @@ cudaError_t launch_keystream(const uint8_t* key_host32, uint64_t nonce, uint64_t
 cudaError_t launch_keystream_rows(const uint8_t* key_host32, uint64_t nonce0, uint32_t rows,
                                   uint64_t len, uint8_t* out, uint64_t row_stride, cudaStream_t s);
 cudaError_t launch_prf(uint64_t k0, uint64_t k1, const uint64_t* in, uint64_t n, uint64_t modulus,
-                       uint64_t* out, cudaStream_t s);
+                       uint64_t* out, uint32_t* out32, cudaStream_t s);
 cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint64_t n, uint32_t h,
                             uint32_t m_bits, uint32_t* pos_out, unsigned long long* words,
                             cudaStream_t s);
@@ -124,6 +124,7 @@ struct CuckooParScratch {
         *this = CuckooParScratch{};
     }
 };
+cudaError_t cuckoo_reserve(CuckooParScratch& sc, uint64_t n, uint32_t buckets, cudaStream_t s);
 cudaError_t cuckoo_parallel_prefix(const CuckooDev& d, CuckooState& h, const uint32_t* b1, const uint32_t* b2,
                                    uint64_t n, uint32_t* reports, CuckooParScratch& sc, uint64_t* applied,
                                    cudaStream_t s);

@@ -80,9 +80,12 @@ __global__ void k_draws(ChaChaKey key, uint64_t nonce0, uint32_t count, uint64_t
 // K5 PRF, K7 interest / absorb
 // ---------------------------------------------------------------------------
 __global__ void k_prf(uint64_t k0, uint64_t k1, const uint64_t* __restrict__ in, uint64_t n,
-                      uint64_t modulus, uint64_t* __restrict__ out) {
+                      uint64_t modulus, uint64_t* __restrict__ out, uint32_t* __restrict__ out32) {
     const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t < n) out[t] = prf(k0, k1, in[t], modulus);
+    if (t >= n) return;
+    const uint64_t v = prf(k0, k1, in[t], modulus);
+    if (out) out[t] = v;
+    if (out32) out32[t] = uint32_t(v);
 }
 
 struct Id16 {
@@ -398,9 +401,9 @@ cudaError_t launch_draws(const uint8_t* key_host32, uint64_t nonce0, uint32_t co
 }
 
 cudaError_t launch_prf(uint64_t k0, uint64_t k1, const uint64_t* in, uint64_t n, uint64_t modulus,
-                       uint64_t* out, cudaStream_t s) {
+                       uint64_t* out, uint32_t* out32, cudaStream_t s) {
     if (!n) return cudaSuccess;
-    k_prf<<<uint32_t((n + 127) / 128), 128, 0, s>>>(k0, k1, in, n, modulus, out);
+    k_prf<<<uint32_t((n + 127) / 128), 128, 0, s>>>(k0, k1, in, n, modulus, out, out32);
     return cudaGetLastError();
 }
 
