@@ -96,7 +96,7 @@ __device__ __forceinline__ void xor2(uint4& a, const uint4& b) {
 __global__ void __launch_bounds__(TM_NT, 1)
 k_scan_m4rm_tmem(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ qT,
                  uint64_t qstride, uint32_t B, uint8_t* __restrict__ out, uint32_t n_ctiles, uint32_t n_groups,
-                 uint64_t total_work) {
+                 uint64_t n_segments) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const int tid = threadIdx.x;
@@ -118,16 +118,21 @@ k_scan_m4rm_tmem(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const 
     const uint32_t tcol = tbase + (uint32_t((warp & 3) * 32) << 16) + uint32_t(warp >> 2) * 128;
 
     const uint32_t hm5 = 0u - ((warp >> 0) & 1u), hm6 = 0u - ((warp >> 1) & 1u), hm7 = 0u - ((warp >> 2) & 1u);
-    const uint64_t w0 = total_work * blockIdx.x / gridDim.x;
-    const uint64_t w1 = total_work * (blockIdx.x + 1) / gridDim.x;
+    // Work units (column tile c fastest, then request tile, then group segment),
+    // dealt round-robin: at any moment the CTAs work on the same few
+    // (request tile, segment) pairs for all column tiles, so each staged query
+    // chunk and bucket chunk is fetched from HBM once and re-read from L2.
+    const uint32_t n_rtiles = (B + TM_RC - 1) / TM_RC;
+    const uint32_t n_seg = uint32_t(n_segments);  // host-chosen segment count
+    const uint64_t units = uint64_t(n_ctiles) * n_rtiles * n_seg;
 
-    for (uint64_t u = w0; u < w1;) {
-        const uint32_t p = uint32_t(u / n_groups);
-        const uint32_t gs = uint32_t(u - uint64_t(p) * n_groups);
-        const uint64_t pend = uint64_t(p + 1) * n_groups;
-        const uint32_t ge = uint32_t((w1 < pend ? w1 : pend) - uint64_t(p) * n_groups);
-        u = uint64_t(p) * n_groups + ge;
-        const uint32_t rt = p / n_ctiles, c = p - rt * n_ctiles;
+    for (uint64_t v = blockIdx.x; v < units; v += gridDim.x) {
+        const uint32_t c = uint32_t(v % n_ctiles);
+        const uint32_t rt = uint32_t((v / n_ctiles) % n_rtiles);
+        const uint32_t sg = uint32_t(v / (uint64_t(n_ctiles) * n_rtiles));
+        const uint32_t gs = uint32_t(uint64_t(n_groups) * sg / n_seg);
+        const uint32_t ge = uint32_t(uint64_t(n_groups) * (sg + 1) / n_seg);
+        if (gs >= ge) continue;
         const uint32_t r_base = rt * TM_RC;
         const uint32_t nvalid = min(uint32_t(TM_RC), B - r_base);
         const bool active = uint32_t(warp * 4 * TM_SLOTS) < nvalid;  // warp-uniform
@@ -297,12 +302,26 @@ cudaError_t launch_scan_m4rm_tmem(const M4Args& a, int num_sms) {
     const uint32_t n_ctiles = a.S / 128;
     const uint32_t n_rtiles = (a.B + TM_RC - 1) / TM_RC;
     const uint32_t n_groups = (a.nb + 7) / 8;
-    const uint64_t total = uint64_t(n_ctiles) * n_rtiles * n_groups;
-    uint64_t grid = uint64_t(num_sms);
-    const uint64_t max_grid = (total + 7) / 8;
-    if (grid > max_grid) grid = max_grid > 0 ? max_grid : 1;
+    // Segments per (request tile, column tile): about 32 units per CTA, and a unit
+    // count that is a multiple of the grid when the shapes allow (config 4: 4 x 32
+    // pairs x 37 segments = 32 x 148), segments of at least 64 groups.
+    const uint64_t pairs = uint64_t(n_ctiles) * n_rtiles;
+    const uint64_t grid = uint64_t(num_sms);
+    uint64_t a_ = pairs, b_ = grid;
+    while (b_) {
+        const uint64_t t = a_ % b_;
+        a_ = b_;
+        b_ = t;
+    }
+    const uint64_t step = grid / a_;
+    const uint64_t target = (32 * grid + pairs - 1) / pairs;
+    uint64_t n_seg = (target + step - 1) / step * step;
+    if (step > 4 * target) n_seg = target;  // no convenient multiple: stay near the target
+    const uint64_t max_seg = n_groups / 64 > 0 ? n_groups / 64 : 1;
+    if (n_seg > max_seg) n_seg = max_seg;
+    if (n_seg < 1) n_seg = 1;
     k_scan_m4rm_tmem<<<dim3(uint32_t(grid)), TM_NT, TM_SMEM, a.stream>>>(a.db, a.nb, a.S, a.qT, a.qstride, a.B,
-                                                                      a.out, n_ctiles, n_groups, total);
+                                                                      a.out, n_ctiles, n_groups, n_seg);
     return cudaGetLastError();
 }
 
