@@ -184,6 +184,18 @@ def run_reference(args):
     return 0
 
 
+def traffic_from_profile(n_buckets, batch, world, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the committed ncu capture of this same workload (profiles/),
+    or None when the capture does not match the configuration being run."""
+    path = os.path.join(ROOT, "profiles", "r01_traffic_m4rm_tmem.json")
+    if kernel != 5 or world != 1 or n_buckets != 1 << 20 or batch != BATCH or not os.path.exists(path):
+        return None
+    with open(path) as f:
+        t = json.load(f)
+    return t["dram_bytes_read"] + t["dram_bytes_write"]
+
+
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
@@ -344,7 +356,7 @@ def main():
         "peak": peaks["lop3_per_s"] / 1e12,
         "frac": achieved / peaks["lop3_per_s"],
         "peak_source": "measured live: k_lop3_peak (acc ^= w & m, 148 SMs)",
-        "traffic": None,
+        "traffic": traffic_from_profile(N_BUCKETS, B, world, xp.last_scan_kernel()),
         "algorithmic_ops_per_launch": work_lop3,
         "launch_ms": per_launch_ms,
         "note": ("W = B*N_g*S/4 dense GF(2) select-XOR ops; the M4RM kernel does B*N_g*S/32 table "
@@ -356,6 +368,8 @@ def main():
         "hbm": {"achieved_GBps": hbm_bytes / (per_launch_ms * 1e-3) / 1e9, "peak_GBps": hbm_peak,
                 "peak_source": peak_src, "frac": hbm_bytes / (per_launch_ms * 1e-3) / 1e9 / hbm_peak,
                 "bytes_per_launch": hbm_bytes},
+        "traffic_source": "profiles/r01_traffic_m4rm_tmem.json (ncu dram__bytes_read+write of this kernel "
+                          "on this workload; algorithmic bytes per launch = hbm.bytes_per_launch)",
         "kernel_share_of_step": (scan_ms / args.steps) / ms_per_step,
     }
 
