@@ -151,7 +151,7 @@ struct xpir_store {
     uint64_t epoch = 0;
     uint8_t* data = nullptr;
     cudaStream_t stream = nullptr;
-    DevBuf q, part, out, seeds, masks, qwin;
+    DevBuf q, out, seeds, masks, qwin;
     std::mutex mu;
     uint32_t nb() const { return hi - lo; }
     uint64_t bytes() const { return uint64_t(nb()) * S; }
@@ -332,7 +332,6 @@ int xpir_store_destroy(xpir_store* st) {
     cudaStreamSynchronize(st->stream);
     cudaFree(st->data);
     st->q.release();
-    st->part.release();
     st->out.release();
     st->seeds.release();
     st->masks.release();
@@ -469,7 +468,7 @@ static int run_rows(xpir_store* st, int kernel, const uint8_t* qwin, uint64_t st
     uint32_t nsplit = 0;
     cudaEvent_t ev;
     timing_begin(s, &ev);
-    XCK(launch_scan_direct(a, nullptr, 0, num_sms(st->device), &nsplit));
+    XCK(launch_scan_direct(a, num_sms(st->device), &nsplit));
     timing_end(s, ev);
     count_launches(1);
     g_last_kernel = 1;

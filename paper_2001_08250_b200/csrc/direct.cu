@@ -124,8 +124,7 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
 }
 
 template <int RPT>
-static cudaError_t launch_direct_t(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
-                                   uint32_t* nsplit_out) {
+static cudaError_t launch_direct_t(const ScanArgs& a, int num_sms, uint32_t* nsplit_out) {
     const uint32_t ncol = a.S / 16;
     const uint32_t cw = ncol >= DIRECT_NT ? DIRECT_NT : ncol;  // columns per CTA
     const uint32_t phases = DIRECT_NT / cw;
@@ -146,19 +145,16 @@ static cudaError_t launch_direct_t(const ScanArgs& a, uint8_t* part, uint64_t pa
     k_scan_direct<RPT><<<dim3(gz, gx, uint32_t(nsplit)), DIRECT_NT, 0, a.stream>>>(
         a.db, a.nb, a.S, a.q, a.q_stride, a.B, a.out, uint32_t(bpc), cw);
     *nsplit_out = uint32_t(nsplit);
-    (void)part;
-    (void)part_bytes;
     (void)out_bytes;
     return cudaGetLastError();
 }
 
-cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
-                               uint32_t* nsplit_out) {
-    if (a.B <= 1) return launch_direct_t<1>(a, part, part_bytes, num_sms, nsplit_out);
-    if (a.B <= 2) return launch_direct_t<2>(a, part, part_bytes, num_sms, nsplit_out);
-    if (a.B <= 4) return launch_direct_t<4>(a, part, part_bytes, num_sms, nsplit_out);
-    if (a.B <= 8) return launch_direct_t<8>(a, part, part_bytes, num_sms, nsplit_out);
-    return launch_direct_t<16>(a, part, part_bytes, num_sms, nsplit_out);
+cudaError_t launch_scan_direct(const ScanArgs& a, int num_sms, uint32_t* nsplit_out) {
+    if (a.B <= 1) return launch_direct_t<1>(a, num_sms, nsplit_out);
+    if (a.B <= 2) return launch_direct_t<2>(a, num_sms, nsplit_out);
+    if (a.B <= 4) return launch_direct_t<4>(a, num_sms, nsplit_out);
+    if (a.B <= 8) return launch_direct_t<8>(a, num_sms, nsplit_out);
+    return launch_direct_t<16>(a, num_sms, nsplit_out);
 }
 
 }  // namespace xpir

@@ -77,21 +77,6 @@ __global__ void k_scan_bytes(const uint8_t* __restrict__ db, uint32_t nb, uint32
     out[t] ^= acc;
 }
 
-// out ^= XOR over splits of part[split]
-__global__ void k_reduce_parts(const uint8_t* __restrict__ part, uint32_t nsplit, uint64_t bytes,
-                               uint8_t* __restrict__ out) {
-    const uint64_t n16 = bytes / 16;
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        uint4 a = reinterpret_cast<uint4*>(out)[i];
-        for (uint32_t s = 0; s < nsplit; ++s) {
-            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(part + uint64_t(s) * bytes) + i);
-            a.x ^= v.x; a.y ^= v.y; a.z ^= v.z; a.w ^= v.w;
-        }
-        reinterpret_cast<uint4*>(out)[i] = a;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // K3: out[r] = mask pad (prng_expand(mask_seed_r, S)) or zero — applied before
 // the scan XOR-accumulates into it, so the mask costs one write pass.
@@ -160,17 +145,6 @@ __global__ void k_expand(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t
                 o[pos - byte_lo] = uint8_t(ks[k >> 2] >> (8 * (k & 3)));
         }
     }
-}
-
-// Copy a window of query bytes into a 16-byte-aligned, padded layout.
-__global__ void k_repack_queries(const uint8_t* __restrict__ q, uint64_t q_stride, uint64_t byte_lo,
-                                 uint64_t nbytes, uint32_t B, uint8_t* __restrict__ dst,
-                                 uint64_t dst_stride) {
-    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= uint64_t(B) * dst_stride) return;
-    const uint32_t r = uint32_t(t / dst_stride);
-    const uint64_t k = t - uint64_t(r) * dst_stride;
-    dst[t] = k < nbytes ? q[uint64_t(r) * q_stride + byte_lo + k] : uint8_t(0);
 }
 
 // ---------------------------------------------------------------------------
@@ -284,16 +258,6 @@ cudaError_t run_peak_kernels(int num_sms, double* lop3_per_s, double* smem_bps, 
 // ---------------------------------------------------------------------------
 // host-side launchers
 // ---------------------------------------------------------------------------
-cudaError_t launch_reduce_parts(const uint8_t* part, uint32_t nsplit, uint64_t out_bytes, uint8_t* out,
-                                int num_sms, cudaStream_t s) {
-    const uint64_t n16 = out_bytes / 16;
-    uint32_t rg = uint32_t((n16 + 255) / 256);
-    if (rg > uint32_t(num_sms) * 16) rg = uint32_t(num_sms) * 16;
-    if (rg < 1) rg = 1;
-    k_reduce_parts<<<rg, 256, 0, s>>>(part, nsplit, out_bytes, out);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_scan_bytes(const ScanArgs& a) {
     const uint64_t n = uint64_t(a.B) * a.S;
     if (n == 0) return cudaSuccess;
@@ -316,15 +280,6 @@ cudaError_t launch_expand(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, ui
     const uint64_t n = uint64_t(B) * nblk;
     if (n == 0) return cudaSuccess;
     k_expand<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qout, stride);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_repack(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
-                          uint32_t B, uint8_t* dst, uint64_t dst_stride, cudaStream_t s) {
-    const uint64_t n = uint64_t(B) * dst_stride;
-    if (n == 0) return cudaSuccess;
-    k_repack_queries<<<uint32_t((n + 255) / 256), 256, 0, s>>>(q, q_stride, byte_lo, nbytes, B, dst,
-                                                                dst_stride);
     return cudaGetLastError();
 }
 

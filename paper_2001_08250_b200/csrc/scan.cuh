@@ -40,18 +40,13 @@ cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, 
                             uint8_t* qT, uint64_t qstride, cudaStream_t s);
 cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
                                uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s);
-cudaError_t launch_scan_direct(const ScanArgs& a, uint8_t* part, uint64_t part_bytes, int num_sms,
-                               uint32_t* nsplit_out);
+cudaError_t launch_scan_direct(const ScanArgs& a, int num_sms, uint32_t* nsplit_out);
 cudaError_t launch_scan_bytes(const ScanArgs& a);
 cudaError_t launch_scan_nib(const ScanArgs& a, int num_sms);  // nib.cu, S % 128 == 0
-cudaError_t launch_reduce_parts(const uint8_t* part, uint32_t nsplit, uint64_t out_bytes, uint8_t* out,
-                                int num_sms, cudaStream_t s);
 cudaError_t launch_init_out(uint8_t* out, uint32_t B, uint32_t S, const uint8_t* mask_seeds,
                             bool xor_into, cudaStream_t s);
 cudaError_t launch_expand(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
                           uint8_t* qout, uint64_t stride, cudaStream_t s);
-cudaError_t launch_repack(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
-                          uint32_t B, uint8_t* dst, uint64_t dst_stride, cudaStream_t s);
 cudaError_t launch_xor_reduce(uint8_t* dst, const uint8_t* const* d_srcs, uint32_t nsrc,
                               uint64_t bytes, int num_sms, cudaStream_t s);
 cudaError_t run_peak_kernels(int num_sms, double* lop3_per_s, double* smem_bps, cudaStream_t s);

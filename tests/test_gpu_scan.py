@@ -286,3 +286,33 @@ def test_m4rm_variants_match_oracle(xp, port, cuda, kernel, N, S, B):
     st.upload(db)
     assert np.array_equal(st.answer_batch(q), port.answer_batch(db, N, S, q, B))
     assert xp.last_scan_kernel() == (5 if kernel == 5 else 2)
+
+
+def test_concurrent_host_calls_on_one_store(xp, port, cuda):
+    """answer/answer_batch are re-entrant over an immutable snapshot:
+    several host threads (ctypes releases the GIL) query one store at once."""
+    import threading
+
+    N, S = 4096, 512
+    g = np.random.default_rng(404)
+    db = rand(g, N * S)
+    st = xp.Store(N, S)
+    st.upload(db)
+    qs = [rand(g, B, N // 8) for B in (3, 64, 200, 700)]
+    want = [port.answer_batch(db, N, S, q, q.shape[0]) for q in qs]
+    errors = []
+
+    def worker(k):
+        try:
+            for _ in range(4):
+                if not np.array_equal(st.answer_batch(qs[k]), want[k]):
+                    errors.append(k)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(len(qs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors
