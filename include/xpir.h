@@ -113,7 +113,7 @@ int xpir_xor_reduce_dev(int device, uint8_t* d_dst, const uint8_t* const* d_srcs
 typedef struct {
     int kernel;        /* 0 = auto, 1 = direct select-XOR, 2 = M4RM byte tables (auto variant),
                           4 = M4RM register accumulators, 5 = M4RM half-TMEM accumulators,
-                          6 = warp-private nibble tables */
+                          6 = warp-private nibble tables, 7 = M4RM nibble tables */
     int ctas_per_sm;   /* 0 = auto */
     int reserved[6];
 } xpir_scan_opts;

@@ -410,7 +410,8 @@ uint64_t xpir_query_window_bytes(const xpir_store* st) {
 // nibble-table kernel (6) measured slower than direct at every B in [8, 128)
 // (latency-bound), so it is selectable but not chosen automatically.
 static uint32_t g_nib_min_batch = 0xffffffffu;
-static uint32_t g_m4_min_batch = 128;
+static uint32_t g_k4_min_batch = 16;   // nibble-table M4RM (kernel 7) from here
+static uint32_t g_m4_min_batch = 257;  // byte-table M4RM (kernels 2/5) from here
 
 static int choose_kernel(const xpir_store* st, uint32_t B) {
     int k;
@@ -421,13 +422,14 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
     if (st->S % 16 != 0) return 3;
     const bool m4_ok = (st->S % 128) == 0;
     if (k == 4 || k == 5) k = 2;  // forced M4RM variants (registers-only / TMEM accumulators)
-    if (k == 0) k = !m4_ok ? 1 : B >= g_m4_min_batch ? 2 : B >= g_nib_min_batch ? 6 : 1;
-    if ((k == 2 || k == 6) && !m4_ok) k = 1;
+    if (k == 0)
+        k = !m4_ok ? 1 : B >= g_m4_min_batch ? 2 : B >= g_k4_min_batch ? 7 : B >= g_nib_min_batch ? 6 : 1;
+    if ((k == 2 || k == 6 || k == 7) && !m4_ok) k = 1;
     return k;
 }
 
 static int run_m4(xpir_store* st, const uint8_t* qT, uint64_t qstride, uint32_t B, uint8_t* d_out,
-                  cudaStream_t s) {
+                  cudaStream_t s, int kernel) {
     int cps, variant;
     {
         std::lock_guard<std::mutex> lk(g_opts_mu);
@@ -436,6 +438,14 @@ static int run_m4(xpir_store* st, const uint8_t* qT, uint64_t qstride, uint32_t 
     }
     M4Args a{st->data, st->nb(), st->S, qT, qstride, B, d_out, s};
     cudaEvent_t ev;
+    if (kernel == 7) {  // nibble tables
+        timing_begin(s, &ev);
+        XCK(launch_scan_m4rm4(a, num_sms(st->device)));
+        timing_end(s, ev);
+        count_launches(1);
+        g_last_kernel = 7;
+        return XPIR_OK;
+    }
     timing_begin(s, &ev);
     XCK(launch_scan_m4rm(a, cps, num_sms(st->device), variant));
     timing_end(s, ev);
@@ -483,12 +493,12 @@ static int scan_rows(xpir_store* st, const uint8_t* rows, uint64_t stride, uint3
     if (B == 0) return XPIR_OK;
     const int k = choose_kernel(st, B);
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
-    if (k != 2) return run_rows(st, k, rows + blo, stride, B, d_out, s);
+    if (k != 2 && k != 7) return run_rows(st, k, rows + blo, stride, B, d_out, s);
     const uint64_t qs = m4rm_qstride(B);
     XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
     XCK(launch_transpose_q(rows, stride, blo, nbw, B, st->qwin.as<uint8_t>(), qs, s));
     count_launches(1);
-    return run_m4(st, st->qwin.as<uint8_t>(), qs, B, d_out, s);
+    return run_m4(st, st->qwin.as<uint8_t>(), qs, B, d_out, s, k);
 }
 
 extern "C" {
@@ -518,12 +528,12 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
     // K2: expand only this shard's window of every request's selection vector,
     // straight into the layout the chosen scan kernel reads.
-    if (k == 2) {
+    if (k == 2 || k == 7) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
         XCK(launch_expand_T(d_seeds, B, blo, nbw, st->qwin.as<uint8_t>(), qs, s));
         count_launches(1);
-        return run_m4(st, st->qwin.as<uint8_t>(), qs, B, d_out, s);
+        return run_m4(st, st->qwin.as<uint8_t>(), qs, B, d_out, s, k);
     }
     const uint64_t ws = xpir_query_window_bytes(st);
     XCK(st->qwin.ensure(ws * B));
@@ -561,12 +571,12 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
     count_launches(1);
     const int k = choose_kernel(st, B);
     int rc;
-    if (k == 2) {
+    if (k == 2 || k == 7) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
         XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s));
         count_launches(1);
-        rc = run_m4(st, st->qwin.as<uint8_t>(), qs, B, dout, s);
+        rc = run_m4(st, st->qwin.as<uint8_t>(), qs, B, dout, s, k);
     } else {
         rc = run_rows(st, k, st->q.as<uint8_t>(), ws, B, dout, s);
     }

@@ -34,6 +34,7 @@ struct M4Args {
 };
 cudaError_t launch_scan_m4rm(const M4Args& a, int ctas_per_sm, int num_sms, int variant);
 cudaError_t launch_scan_m4rm_tmem(const M4Args& a, int num_sms);
+cudaError_t launch_scan_m4rm4(const M4Args& a, int num_sms);  // nibble tables (m4rm4.cu)
 uint64_t m4rm_qstride(uint32_t B);
 uint64_t m4rm_qrows(uint64_t n_groups);  // rows to allocate (staging reads 16-row chunks)
 cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,

@@ -199,25 +199,33 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
     auto is_touched = [&](uint32_t f) -> bool {
         return use_smem ? ((touch_bits[f >> 5] >> (f & 31)) & 1u) : d.touched_mark[f] == s.batch_id;
     };
+    // In shared-memory mode the occupancy and touched maps live in shared memory
+    // (global `used` is written back once at the end, `touched_mark` is only the
+    // fallback map), so a placement costs no global loads and few stores.
     auto touch = [&](uint32_t f, int64_t org) {
         if (!is_touched(f)) {
             if (use_smem) touch_bits[f >> 5] |= 1u << (f & 31);
-            d.touched_mark[f] = s.batch_id;
+            else d.touched_mark[f] = s.batch_id;
             d.touched[s.n_touched++] = f;
         }
         d.origin[f] = org;
     };
-    auto origin_of = [&](uint32_t f) -> int64_t {
-        return is_touched(f) ? d.origin[f] : -int64_t(f) - 2;
-    };
-    auto free_slot = [&](uint32_t b) -> int {  // cuckoo.cpp:31-35
+    auto free_slot = [&](uint32_t b) -> int {  // cuckoo.cpp:31-35: lowest free slot of bucket b
+        if (use_smem && d.depth <= 32) {
+            const uint32_t f0 = b * d.depth, w0 = f0 >> 5, sh = f0 & 31;
+            uint64_t bits = used_bits[w0];
+            if (sh + d.depth > 32) bits |= uint64_t(used_bits[w0 + 1]) << 32;
+            const uint64_t mask = d.depth == 32 ? 0xffffffffull : ((1ull << d.depth) - 1);
+            const uint64_t freeb = ~(bits >> sh) & mask;
+            return freeb ? __ffsll(static_cast<long long>(freeb)) - 1 : -1;
+        }
         for (uint32_t sl = 0; sl < d.depth; ++sl)
             if (!is_used(b * d.depth + sl)) return int(sl);
         return -1;
     };
     auto place = [&](uint32_t f, uint32_t b1, uint32_t b2, uint64_t stamp, int64_t org) {  // :37-46
         if (use_smem) used_bits[f >> 5] |= 1u << (f & 31);
-        d.used[f] = 1;
+        else d.used[f] = 1;
         d.beta1[f] = b1;
         d.beta2[f] = b2;
         d.stamp[f] = stamp;
@@ -227,8 +235,8 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
     };
     auto clear = [&](uint32_t f) {  // :48-54
         if (use_smem) used_bits[f >> 5] &= ~(1u << (f & 31));
+        else d.used[f] = 0;
         d.fifo[d.stamp[f] & fmask] = -1;
-        d.used[f] = 0;
         d.beta1[f] = 0;
         d.beta2[f] = 0;
         d.stamp[f] = 0;
@@ -302,9 +310,16 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
                         const uint32_t vf = be * d.depth + vs;
                         const uint32_t v1 = d.beta1[vf], v2 = d.beta2[vf];
                         const uint64_t vst = d.stamp[vf];
-                        const int64_t vorg = origin_of(vf);
-                        clear(vf);
-                        place(vf, c1, c2, cst, corg);
+                        const int64_t vo = d.origin[vf];  // loaded beside the metadata (speculative)
+                        const int64_t vorg = is_touched(vf) ? vo : -int64_t(vf) - 2;
+                        // clear(vf) then place(vf, carry) (:110-113): the slot stays occupied and
+                        // live is unchanged, so only the FIFO, metadata and origin change.
+                        d.fifo[vst & fmask] = -1;
+                        d.beta1[vf] = c1;
+                        d.beta2[vf] = c2;
+                        d.stamp[vf] = cst;
+                        d.fifo[cst & fmask] = int64_t(vf);
+                        touch(vf, corg);
                         if (carry_incoming) incoming_stored = true;
                         c1 = v1;
                         c2 = v2;
@@ -324,6 +339,24 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
         }
         __syncthreads();
         if (*stop) break;
+    }
+    if (use_smem) {  // occupancy map back to the global byte array
+        __syncthreads();
+        for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
+            const uint32_t v = used_bits[w];
+            const uint64_t f0 = uint64_t(w) * 32;
+            if (f0 + 32 <= slots && (reinterpret_cast<uintptr_t>(d.used + f0) & 15) == 0) {
+                uint32_t b[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    b[k] = ((v >> (4 * k)) & 1u) | ((v >> (4 * k + 1)) & 1u) << 8 | ((v >> (4 * k + 2)) & 1u) << 16 |
+                           ((v >> (4 * k + 3)) & 1u) << 24;
+                reinterpret_cast<uint4*>(d.used + f0)[0] = make_uint4(b[0], b[1], b[2], b[3]);
+                reinterpret_cast<uint4*>(d.used + f0)[1] = make_uint4(b[4], b[5], b[6], b[7]);
+            } else {
+                for (uint32_t k = 0; k < 32 && f0 + k < slots; ++k) d.used[f0 + k] = (v >> k) & 1u;
+            }
+        }
     }
     if (threadIdx.x == 0) {
         s.resume_at = i;

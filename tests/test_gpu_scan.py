@@ -50,7 +50,7 @@ def test_full_retrieval_every_target(xp, port, cuda):
             assert np.array_equal(np.bitwise_xor.reduce(ans, axis=0), db.reshape(N, S)[beta])
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
 @pytest.mark.parametrize("N,S,B", [
     (8, 128, 1), (9, 128, 3), (1000, 256, 97), (1024, 4096, 64), (777, 512, 130),
     (4096, 128, 1), (2048, 1024, 513), (4000, 2048, 1025), (256, 32768, 40), (12345, 128, 300),
@@ -78,7 +78,7 @@ def test_dirty_trailing_bits_are_ignored(xp, port, cuda):
     q[:, -1] |= 0xFE
     st = xp.Store(N, S)
     st.upload(db)
-    for k in (1, 2, 6):
+    for k in (1, 2, 6, 7):
         xp.set_scan_opts(k)
         assert np.array_equal(st.answer_batch(q), port.answer_batch(db, N, S, q, B))
 
@@ -155,7 +155,7 @@ def test_config1_golden(xp, port, golden, cuda):
     db, q = recipes.config1(port)
     st = xp.Store(1024, 4096)
     st.upload(db)
-    for k in (0, 1, 2):
+    for k in (0, 1, 2, 7):
         xp.set_scan_opts(k)
         out = st.answer_batch(q)
         assert out[0, :8].tobytes().hex() == "877147f881293508"
