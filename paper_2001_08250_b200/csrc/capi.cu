@@ -410,7 +410,7 @@ uint64_t xpir_query_window_bytes(const xpir_store* st) {
 // nibble-table kernel (6) measured slower than direct at every B in [8, 128)
 // (latency-bound), so it is selectable but not chosen automatically.
 static uint32_t g_nib_min_batch = 0xffffffffu;
-static uint32_t g_k4_min_batch = 16;   // nibble-table M4RM (kernel 7) from here
+static uint32_t g_k4_min_batch = 24;   // nibble-table M4RM (kernel 7) from here
 static uint32_t g_m4_min_batch = 257;  // byte-table M4RM (kernels 2/5) from here
 
 static int choose_kernel(const xpir_store* st, uint32_t B) {
