@@ -34,6 +34,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_write_path.jsonl"))
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--only", choices=["24", "95"], default=None, help="run one load level (profiling)")
     args = ap.parse_args()
 
     import torch
@@ -46,7 +47,8 @@ def main():
         golden = json.load(f)
     o = oracle.best()
     lines = []
-    for n in (recipes.C3["n"], recipes.C3["n95"]):
+    sizes = {"24": [recipes.C3["n"]], "95": [recipes.C3["n95"]]}.get(args.only, [recipes.C3["n"], recipes.C3["n95"]])
+    for n in sizes:
         d = recipes.config3(o, n)
         N, depth, item, m, h = 32768, 4, 1024, 1 << 20, 23
         dev = "cuda"
