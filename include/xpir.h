@@ -13,8 +13,13 @@
  *     XPIR_ESTATE (-4)       internal invariant (e.g. FIFO ring overflow)
  *
  * and xpir_last_error() returns a thread-local message for the last failure.
- * Functions taking host buffers are synchronous; *_dev functions take device
- * pointers, enqueue on `stream` and return without synchronising.
+ * Functions taking host buffers are synchronous and thread-safe (one mutex per
+ * handle). *_dev functions take device pointers and enqueue on `stream`; the
+ * scan/expand/mask/reduce ones return without synchronising, while
+ * xpir_table_insert_batch_dev and xpir_window_absorb_dev synchronise once (the
+ * cuckoo walk's resume state and the absorb range check come back to the host).
+ * A store's query scratch is per handle: concurrent *_dev scans on ONE store
+ * from different streams must be ordered by the caller.
  *
  * Bit and byte layouts are the reference's:
  *   query vector   bit j = q[j/8] >> (j%8) & 1, ceil(N/8) bytes     (pir.hpp:14-28)
