@@ -233,6 +233,33 @@ int xpir_window_delta(const xpir_window* win, uint64_t i, uint64_t* out_words);
 /* Window::digest (notify.cpp:87-107). */
 int xpir_window_digest(const xpir_window* win, uint8_t out[32]);
 
+/* ------------------------------------------------------------------------ */
+/* Replica state machine — server::ServerCore (server.hpp:57-98,             */
+/* server.cpp:28-91) on device: cuckoo table + interest window + a ring of     */
+/* at most epoch_ring sealed stores. Creation rotates the window once and     */
+/* seals epoch 1 (server.cpp:40-42). A sealed store is re-sealed incrementally */
+/* when it falls off the ring: only slots rewritten since it was last synced  */
+/* are copied (the reference copies the whole table per seal).               */
+/* ------------------------------------------------------------------------ */
+typedef struct xpir_server xpir_server;
+
+int xpir_server_create(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
+                       const uint8_t seed[32], uint32_t m_bits, uint32_t h, uint32_t window_deltas,
+                       uint32_t rotate_writes, uint32_t epoch_ring, xpir_server** out);
+int xpir_server_destroy(xpir_server* sv);
+/* n calls of ServerCore::apply_write (server.cpp:58-73) in order — insert,
+ * absorb the write's h_per_write interest positions, rotate every rotate_writes
+ * writes — then seal once if seal_after (the last write's seal_after). */
+int xpir_server_apply_round(xpir_server* sv, const uint32_t* beta1, const uint32_t* beta2, const uint8_t* payload,
+                            const uint32_t* interest, uint32_t h_per_write, uint64_t n, int seal_after,
+                            uint32_t* reports, uint64_t* sealed_epoch);
+int xpir_server_seal(xpir_server* sv, uint64_t* epoch);            /* seal_epoch, server.cpp:75-81 */
+/* snapshot_at (server.cpp:83-87); epoch 0 = latest. The store stays owned by the
+ * server and valid until its epoch leaves the ring. */
+int xpir_server_snapshot(xpir_server* sv, uint64_t epoch, xpir_store** st);
+int xpir_server_info(xpir_server* sv, uint64_t* writes, uint64_t* latest_epoch, uint64_t* oldest_epoch,
+                     xpir_table** table, xpir_window** window);
+
 #ifdef __cplusplus
 }
 #endif

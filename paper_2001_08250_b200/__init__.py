@@ -128,6 +128,14 @@ _SIGS = {
     "xpir_window_info": ([_vp, _u64p, _u64p], C.c_int),
     "xpir_window_delta": ([_vp, C.c_uint64, _u64p], C.c_int),
     "xpir_window_digest": ([_vp, _u8p], C.c_int),
+    "xpir_server_create": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _u8p, C.c_uint32, C.c_uint32,
+                            C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "xpir_server_destroy": ([_vp], C.c_int),
+    "xpir_server_apply_round": ([_vp, _u32p, _u32p, _u8p, _u32p, C.c_uint32, C.c_uint64, C.c_int, _u32p, _u64p],
+                                C.c_int),
+    "xpir_server_seal": ([_vp, _u64p], C.c_int),
+    "xpir_server_snapshot": ([_vp, C.c_uint64, C.POINTER(_vp)], C.c_int),
+    "xpir_server_info": ([_vp, _u64p, _u64p, _u64p, C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
@@ -572,4 +580,81 @@ class Window:
     def digest(self) -> bytes:
         out = np.empty(32, np.uint8)
         _check(lib().xpir_window_digest(self.h, _p(out)))
+        return out.tobytes()
+
+
+# ---------------------------------------------------------------------------
+# server::ServerCore
+# ---------------------------------------------------------------------------
+class _BorrowedStore(Store):
+    """A sealed store owned by a Server (valid while its epoch is in the ring)."""
+
+    def __init__(self, handle, N: int, S: int, device: int):  # noqa: D401 - no super().__init__
+        self.h, self.N, self.S, self.lo, self.hi, self.device = handle, N, S, 0, N, device
+
+    def close(self):
+        self.h = None
+
+    __del__ = close
+
+
+class Server:
+    """Device ServerCore: Table + Window + ring of sealed stores (server.cpp:28-91)."""
+
+    def __init__(self, buckets: int, depth: int, capacity: int, item_size: int, seed32: bytes, m_bits: int, h: int,
+                 window_deltas: int, rotate_writes: int, epoch_ring: int, device: int = 0):
+        hd = _vp()
+        _check(lib().xpir_server_create(device, buckets, depth, capacity, item_size, _p(_u8(seed32)), m_bits, h,
+                                        window_deltas, rotate_writes, epoch_ring, C.byref(hd)))
+        self.h, self.buckets, self.depth, self.item, self.device = hd, buckets, depth, item_size, device
+        self.nh = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xpir_server_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def apply_round(self, beta1, beta2, payload, interest, seal_after: bool = False):
+        b1 = np.ascontiguousarray(beta1, np.uint32)
+        b2 = np.ascontiguousarray(beta2, np.uint32)
+        n = len(b1)
+        pl = _u8(payload).reshape(-1)
+        pos = np.ascontiguousarray(interest, np.uint32).reshape(n, -1) if n else np.zeros((0, self.nh), np.uint32)
+        rep = np.zeros((max(n, 1), 4), np.uint32)
+        ep = C.c_uint64()
+        _check(lib().xpir_server_apply_round(self.h, _p(b1, _u32p), _p(b2, _u32p), _p(pl),
+                                             _p(pos, _u32p) if pos.size else None, pos.shape[1] if n else 0, n,
+                                             1 if seal_after else 0, _p(rep, _u32p), C.byref(ep)))
+        return rep[:n], ep.value
+
+    def seal(self) -> int:
+        ep = C.c_uint64()
+        _check(lib().xpir_server_seal(self.h, C.byref(ep)))
+        return ep.value
+
+    def snapshot(self, epoch: int = 0) -> Store:
+        st = _vp()
+        _check(lib().xpir_server_snapshot(self.h, epoch, C.byref(st)))
+        return _BorrowedStore(st, self.buckets, self.depth * self.item, self.device)
+
+    def info(self):
+        w, l, o = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().xpir_server_info(self.h, C.byref(w), C.byref(l), C.byref(o), None, None))
+        return {"writes": w.value, "latest_epoch": l.value, "oldest_epoch": o.value}
+
+    def _handles(self):
+        t, w = _vp(), _vp()
+        _check(lib().xpir_server_info(self.h, None, None, None, C.byref(t), C.byref(w)))
+        return t, w
+
+    def window_digest(self) -> bytes:
+        out = np.empty(32, np.uint8)
+        _check(lib().xpir_window_digest(self._handles()[1], _p(out)))
+        return out.tobytes()
+
+    def table_digest(self) -> bytes:
+        out = np.empty(32, np.uint8)
+        _check(lib().xpir_table_state_digest(self._handles()[0], _p(out)))
         return out.tobytes()

@@ -794,6 +794,7 @@ static void table_free_all(xpir_table* t) {
     cudaFree(t->d.origin);
     cudaFree(t->d.touched_mark);
     cudaFree(t->d.touched);
+    cudaFree(t->d.mod_batch);
     cudaFree(t->d.fifo);
     cudaFree(t->d.draws);
     cudaFree(t->dstate);
@@ -846,6 +847,7 @@ int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t cap
     M(reinterpret_cast<void**>(&t->d.origin), 8 * slots);
     M(reinterpret_cast<void**>(&t->d.touched_mark), 4 * slots);
     M(reinterpret_cast<void**>(&t->d.touched), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.mod_batch), 4 * slots);
     M(reinterpret_cast<void**>(&t->d.fifo), 8 * fc);
     M(reinterpret_cast<void**>(&t->d.draws), 8 * uint64_t(DRAW_CAP));
     M(reinterpret_cast<void**>(&t->dstate), sizeof(CuckooState));
@@ -1213,6 +1215,155 @@ int xpir_window_digest(const xpir_window* win, uint8_t out[32]) {  // notify.cpp
         h.update(reinterpret_cast<const uint8_t*>(words.data()), 8 * words.size());  // LE words
     }
     h.final(out);
+    return XPIR_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// replica state machine — server::ServerCore (server.hpp:57-98, server.cpp:28-91)
+// on device: cuckoo table + interest window + a ring of sealed stores.
+// ===========================================================================
+struct xpir_server {
+    int device;
+    xpir_table* table = nullptr;
+    xpir_window* window = nullptr;
+    uint32_t rotate_writes, epoch_ring;
+    uint64_t writes = 0, latest_epoch = 0;
+    struct Sealed {
+        uint64_t epoch;
+        uint32_t since_batch;  // table batch id the image is synchronised with
+        xpir_store* st;
+    };
+    std::deque<Sealed> ring;  // oldest first
+    std::mutex mu;
+};
+
+static int server_seal(xpir_server* sv, uint64_t* epoch_out) {  // server.cpp:75-81
+    xpir_table* t = sv->table;
+    DeviceGuard g(sv->device);
+    xpir_server::Sealed e{};
+    if (sv->ring.size() >= sv->epoch_ring) {
+        // reuse the oldest image: only slots rewritten since it was sealed are copied
+        e = sv->ring.front();
+        sv->ring.pop_front();
+        XCK(launch_seal_incremental(t->d, e.since_batch, t->data, e.st->data, num_sms(sv->device), t->stream));
+        count_launches(1);
+    } else {
+        int rc = xpir_store_create(sv->device, t->d.buckets, uint32_t(t->d.depth * t->d.item), 0, t->d.buckets,
+                                   &e.st);
+        if (rc) return rc;
+        XCK(cudaMemcpyAsync(e.st->data, t->data, e.st->bytes(), cudaMemcpyDeviceToDevice, t->stream));
+    }
+    XCK(cudaStreamSynchronize(t->stream));
+    e.since_batch = t->h.batch_id;
+    e.epoch = ++sv->latest_epoch;
+    e.st->epoch = e.epoch;
+    sv->ring.push_back(e);
+    if (epoch_out) *epoch_out = e.epoch;
+    return XPIR_OK;
+}
+
+extern "C" {
+
+int xpir_server_create(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
+                       const uint8_t seed[32], uint32_t m_bits, uint32_t h, uint32_t window_deltas,
+                       uint32_t rotate_writes, uint32_t epoch_ring, xpir_server** out) {
+    if (!out) return fail(XPIR_EINVAL, "server_create: null out");
+    if (rotate_writes == 0) return fail(XPIR_EINVAL, "server_create: rotate_writes must be positive");
+    if (epoch_ring == 0) return fail(XPIR_EINVAL, "server_create: epoch_ring must be positive");
+    auto* sv = new xpir_server;
+    sv->device = device;
+    sv->rotate_writes = rotate_writes;
+    sv->epoch_ring = epoch_ring;
+    int rc = xpir_table_create(device, buckets, depth, capacity, item_size, seed, &sv->table);
+    if (!rc) rc = xpir_window_create(device, m_bits, h, window_deltas, &sv->window);
+    if (!rc) rc = xpir_window_rotate(sv->window);  // server.cpp:40
+    if (!rc) rc = server_seal(sv, nullptr);          // server.cpp:42, epoch 1 (all zeros)
+    if (rc) {
+        std::string msg = g_err;
+        xpir_server_destroy(sv);
+        return fail(rc, msg);
+    }
+    *out = sv;
+    return XPIR_OK;
+}
+
+int xpir_server_destroy(xpir_server* sv) {
+    if (!sv) return XPIR_OK;
+    for (auto& e : sv->ring) xpir_store_destroy(e.st);
+    xpir_table_destroy(sv->table);
+    xpir_window_destroy(sv->window);
+    delete sv;
+    return XPIR_OK;
+}
+
+int xpir_server_apply_round(xpir_server* sv, const uint32_t* beta1, const uint32_t* beta2, const uint8_t* payload,
+                            const uint32_t* interest, uint32_t h_per_write, uint64_t n, int seal_after,
+                            uint32_t* reports, uint64_t* sealed_epoch) {
+    if (!sv) return fail(XPIR_EINVAL, "server_apply: null server");
+    if (sealed_epoch) *sealed_epoch = 0;
+    if (n && (!beta1 || !beta2 || !payload || (h_per_write && !interest)))
+        return fail(XPIR_EINVAL, "server_apply: null buffer");
+    std::lock_guard<std::mutex> lk(sv->mu);
+    // apply_write (server.cpp:58-73) for writes in order: beta range check
+    // (server.cpp:60-61) happens before any state changes of that write.
+    uint64_t ok = n;
+    for (uint64_t k = 0; k < n; ++k)
+        if (beta1[k] >= sv->table->d.buckets || beta2[k] >= sv->table->d.buckets) {
+            ok = k;
+            break;
+        }
+    if (ok) {
+        int rc = xpir_table_insert_batch(sv->table, beta1, beta2, payload, ok, reports);
+        if (rc) return rc;
+        // interest positions per rotation segment, then rotate (server.cpp:64-70)
+        uint64_t a = 0;
+        while (a < ok) {
+            const uint64_t to_rot = sv->rotate_writes - (sv->writes % sv->rotate_writes);
+            const uint64_t b = std::min(ok, a + to_rot);
+            if (h_per_write) {
+                rc = xpir_window_absorb(sv->window, interest + a * h_per_write, (b - a) * h_per_write);
+                if (rc) return rc;
+            }
+            sv->writes += b - a;
+            if (sv->writes % sv->rotate_writes == 0) {
+                rc = xpir_window_rotate(sv->window);
+                if (rc) return rc;
+            }
+            a = b;
+        }
+    }
+    if (ok < n) return fail(XPIR_EINVAL, "write targets a bucket outside the table");
+    if (seal_after) return server_seal(sv, sealed_epoch);
+    return XPIR_OK;
+}
+
+int xpir_server_seal(xpir_server* sv, uint64_t* epoch) {
+    if (!sv) return fail(XPIR_EINVAL, "server_seal: null server");
+    std::lock_guard<std::mutex> lk(sv->mu);
+    return server_seal(sv, epoch);
+}
+
+int xpir_server_snapshot(xpir_server* sv, uint64_t epoch, xpir_store** st) {  // server.cpp:83-91
+    if (!sv || !st) return fail(XPIR_EINVAL, "server_snapshot: null argument");
+    std::lock_guard<std::mutex> lk(sv->mu);
+    *st = nullptr;
+    if (epoch == 0) epoch = sv->latest_epoch;
+    for (auto& e : sv->ring)
+        if (e.epoch == epoch) *st = e.st;
+    return *st ? XPIR_OK : fail(XPIR_EINVAL, "server_snapshot: epoch not in the ring");
+}
+
+int xpir_server_info(xpir_server* sv, uint64_t* writes, uint64_t* latest_epoch, uint64_t* oldest_epoch,
+                     xpir_table** table, xpir_window** window) {
+    if (!sv) return fail(XPIR_EINVAL, "server_info: null server");
+    std::lock_guard<std::mutex> lk(sv->mu);
+    if (writes) *writes = sv->writes;
+    if (latest_epoch) *latest_epoch = sv->latest_epoch;
+    if (oldest_epoch) *oldest_epoch = sv->ring.empty() ? 0 : sv->ring.front().epoch;
+    if (table) *table = sv->table;
+    if (window) *window = sv->window;
     return XPIR_OK;
 }
 

@@ -88,7 +88,10 @@ struct CuckooDev {
     uint64_t* draws;      // [draw_cap] precomputed DetRng::next_u64 values
     uint32_t draw_cap;
     uint8_t* gather;      // [slots*item] staging for moved pre-existing payloads
+    uint32_t* mod_batch;  // [slots] last round (batch id) that rewrote the slot's payload
 };
+cudaError_t launch_seal_incremental(const CuckooDev& d, uint32_t since, const uint8_t* table, uint8_t* img,
+                                    int num_sms, cudaStream_t s);
 
 // Scalars the walk reads and advances (device memory, one struct).
 struct CuckooState {

@@ -384,11 +384,12 @@ __global__ void k_cuckoo_gather(CuckooDev d, uint32_t n_touched, const uint8_t* 
 
 // phase 2: write each touched slot's final content
 __global__ void k_cuckoo_scatter(CuckooDev d, uint32_t n_touched, uint8_t* __restrict__ table,
-                                 const uint8_t* __restrict__ payload) {
+                                 const uint8_t* __restrict__ payload, uint32_t batch_id) {
     const uint32_t k = blockIdx.x;
     if (k >= n_touched) return;
     const uint32_t f = d.touched[k];
     const int64_t o = d.origin[f];
+    if (threadIdx.x == 0) d.mod_batch[f] = batch_id;  // for incremental seals
     uint8_t* dst = table + uint64_t(f) * d.item;
     const uint8_t* src = o >= 0 ? payload + uint64_t(o) * d.item
                         : o == -1 ? nullptr
@@ -400,6 +401,37 @@ __global__ void k_cuckoo_scatter(CuckooDev d, uint32_t n_touched, uint8_t* __res
     } else {
         for (uint64_t b = threadIdx.x; b < d.item; b += blockDim.x) dst[b] = src ? src[b] : 0;
     }
+}
+
+// Incremental seal (ServerCore::seal_epoch, server.cpp:75-81, without the full
+// copy): bring a sealed image last synchronised at round `since` up to date by
+// copying only the slots a later round modified. One warp per slot range.
+__global__ void k_seal_incremental(const uint32_t* __restrict__ mod_batch, uint64_t slots, uint64_t item,
+                                   uint32_t since, const uint8_t* __restrict__ table, uint8_t* __restrict__ img) {
+    const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t f = warp; f < slots; f += nwarps) {
+        if (mod_batch[f] <= since) continue;
+        const uint8_t* s = table + f * item;
+        uint8_t* dst = img + f * item;
+        if ((item & 15) == 0) {
+            for (uint64_t b = lane * 16; b < item; b += 32 * 16)
+                *reinterpret_cast<uint4*>(dst + b) = *reinterpret_cast<const uint4*>(s + b);
+        } else {
+            for (uint64_t b = lane; b < item; b += 32) dst[b] = s[b];
+        }
+    }
+}
+
+cudaError_t launch_seal_incremental(const CuckooDev& d, uint32_t since, const uint8_t* table, uint8_t* img,
+                                    int num_sms, cudaStream_t s) {
+    const uint64_t slots = uint64_t(d.buckets) * d.depth;
+    if (!slots) return cudaSuccess;
+    uint64_t g = (slots * 32 + 255) / 256;
+    if (g > uint64_t(num_sms) * 16) g = uint64_t(num_sms) * 16;
+    k_seal_incremental<<<uint32_t(g), 256, 0, s>>>(d.mod_batch, slots, d.item, since, table, img);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -488,7 +520,7 @@ cudaError_t launch_cuckoo_apply(const CuckooDev& d, const CuckooState* st, uint8
     if (!st->n_touched) return cudaSuccess;
     const uint32_t thr = d.item >= 1024 ? 64 : 32;
     k_cuckoo_gather<<<st->n_touched, thr, 0, s>>>(d, st->n_touched, table);
-    k_cuckoo_scatter<<<st->n_touched, thr, 0, s>>>(d, st->n_touched, table, payload);
+    k_cuckoo_scatter<<<st->n_touched, thr, 0, s>>>(d, st->n_touched, table, payload, st->batch_id);
     return cudaGetLastError();
 }
 

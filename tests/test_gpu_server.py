@@ -1,0 +1,67 @@
+"""GPU: the device ServerCore (xpir_server_*) against the reference's replica
+state machine semantics (server.cpp:28-91) restated with the oracle: rounds of
+apply_write (insert + absorb + rotate every rotate_writes writes), seals into a
+ring of epoch_ring stores with incremental re-seal, snapshot_at for every
+epoch still in the ring."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("nb,depth,item,ring,R", [(256, 4, 64, 3, 37), (64, 2, 48, 2, 5), (1000, 8, 128, 4, 100)])
+def test_server_rounds_and_epoch_ring(xp, port, cuda, nb, depth, item, ring, R):
+    m, h, W = 4096, 5, 3
+    g = np.random.default_rng(nb + ring)
+    seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+    cap = nb * depth * 3 // 4
+    sv = xp.Server(nb, depth, cap, item, seed, m, h, W, R, ring)
+    T = port.table(nb, depth, cap, item, seed)
+    PW = port.window(m, h, W)
+    PW.rotate()  # server.cpp:40
+    sealed = {1: np.zeros(nb * depth * item, np.uint8)}
+    writes = 0
+    assert sv.info()["latest_epoch"] == 1
+    for rnd in range(9):
+        n = int(g.integers(1, 3 * cap // 4))
+        b1 = g.integers(0, nb, n).astype(np.uint32)
+        b2 = g.integers(0, nb, n).astype(np.uint32)
+        pl = g.integers(0, 256, (n, item), dtype=np.uint8)
+        pos = g.integers(0, m, (n, h)).astype(np.uint32)
+        seal = rnd % 3 != 1
+        rep, ep = sv.apply_round(b1, b2, pl, pos, seal_after=seal)
+        # reference semantics, one write at a time (server.cpp:58-73)
+        prep = T.insert_batch(b1, b2, pl)
+        for i in range(n):
+            PW.absorb(pos[i])
+            writes += 1
+            if writes % R == 0:
+                PW.rotate()
+        assert np.array_equal(rep, prep)
+        assert sv.window_digest() == PW.digest()
+        assert sv.table_digest() == T.state_digest()
+        if seal:
+            assert ep == max(sealed) + 1
+            sealed[ep] = T.data().copy()
+            for old in sorted(sealed)[:-ring]:
+                del sealed[old]
+        else:
+            assert ep == 0
+        info = sv.info()
+        assert info["writes"] == writes and info["latest_epoch"] == max(sealed)
+        assert info["oldest_epoch"] == min(sealed)
+        for e, img in sealed.items():
+            assert np.array_equal(sv.snapshot(e).download(), img), (rnd, e)
+    with pytest.raises(xp.InvalidArgument):
+        sv.snapshot(min(sealed) - 1)  # pruned epoch
+    # a sealed epoch answers PIR reads (answer_share's scan step)
+    st = sv.snapshot(0)
+    q = np.zeros((2, (nb + 7) // 8), np.uint8)
+    q[0, 0] = 1
+    q[1, :] = 0xFF
+    if nb % 8:
+        q[1, -1] &= (1 << (nb % 8)) - 1
+    out = st.answer_batch(q)
+    img = sealed[max(sealed)].reshape(nb, depth * item)
+    assert np.array_equal(out[0], img[0])
+    assert np.array_equal(out[1], np.bitwise_xor.reduce(img, axis=0))
