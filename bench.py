@@ -5,7 +5,8 @@ selection vector expanded on device from a 16-byte seed (zero-extended to the
 reference's 32-byte PRG seed, crypto.hpp:20) with the reference's ChaCha20 PRG,
 answered against a 4 GiB store (1,048,576 buckets x 4 x 1,024-byte slots) of
 DetRng(3) bytes, bucket-range sharded over the N ranks, partial answers
-XOR-reduced over NVLink peer memory. Everything is generated on device from the
+XOR-reduced over NVLink peer memory (fused into the scan epilogue: each rank's
+accumulator flushes are peer atomics into the row owner's buffer). Everything is generated on device from the
 recipe in SURVEY.md §8(d); data = synthetic.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -402,6 +403,8 @@ def main():
                                    "requests, bucket-range sharded",
                        "store_bytes": N_BUCKETS * BUCKET_BYTES, "batch": B, "buckets": N_BUCKETS,
                        "bucket_bytes": BUCKET_BYTES, "parallelism": f"bucket-range shards x{world}",
+                       "reduce": ("none" if sh is None else
+                                  "fused peer-atomic epilogue" if sh.fused else "IPC xor reduce-scatter"),
                        "l2": "inputs larger than L2 (4 GiB store streamed every step)"},
             "effective_scan_GBps": B * N_BUCKETS * BUCKET_BYTES / (ms_per_step * 1e-3) / 1e9,
             "gpu_launches": launches,

@@ -100,6 +100,22 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
                                  const uint8_t* d_mask_seeds, uint8_t* d_out, void* stream);
 uint64_t xpir_query_window_bytes(const xpir_store* st);
 
+/* Sharded scan with the cross-GPU XOR reduction FUSED into the scan kernel's
+ * epilogue: every accumulator flush of this shard's partial answers is XORed
+ * (64-bit atomics over NVLink) straight into the answer buffer of the rank that
+ * owns the row — rank k owns rows [row_bounds[k], row_bounds[k+1]) and its
+ * buffer out_ptrs[k] (a local or CUDA-IPC-mapped peer pointer) holds all B rows
+ * at the same offsets. Each owner must have initialised its rows (zero or mask
+ * pad, xpir_init_rows_dev) before any rank launches; after every rank's scan
+ * completes the owner's rows are final. Needs S % 128 == 0 and B >= 2048
+ * (the half-TMEM M4RM kernel); 1..8 ranks. pir::reconstruct semantics. */
+int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, uint32_t batch,
+                                      uint8_t* const* out_ptrs, const uint32_t* row_bounds, uint32_t n_ranks,
+                                      void* stream);
+/* d_out rows [r0, r1) of S bytes = mask pad prng_expand(mask_seed_r, S) (or zero). */
+int xpir_init_rows_dev(int device, uint8_t* d_out, uint32_t r0, uint32_t r1, uint32_t S,
+                       const uint8_t* d_mask_seeds, void* stream);
+
 /* K2 alone: d_q[r*q_stride + k] = prng_expand(seed_r)[byte_lo + k], k < nbytes. */
 int xpir_expand_queries_dev(int device, const uint8_t* d_seeds, uint32_t batch, uint64_t byte_lo,
                             uint64_t nbytes, uint8_t* d_q, uint64_t q_stride, void* stream);

@@ -94,6 +94,9 @@ _SIGS = {
     "xpir_answer_batch_dev": ([_vp, _vp, C.c_uint64, C.c_uint32, C.c_uint32, _vp, _vp, _vp], C.c_int),
     "xpir_answer_batch_seeded_dev": ([_vp, _vp, C.c_uint32, _vp, _vp, _vp], C.c_int),
     "xpir_query_window_bytes": ([_vp], C.c_uint64),
+    "xpir_answer_batch_seeded_peer_dev": ([_vp, _vp, C.c_uint32, C.POINTER(_vp), _u32p, C.c_uint32, _vp],
+                                          C.c_int),
+    "xpir_init_rows_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp], C.c_int),
     "xpir_expand_queries_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint64, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
     "xpir_mask_answer": ([_u8p, C.c_uint64, _u8p, _u8p], C.c_int),
     "xpir_mask_dev": ([C.c_int, _vp, _vp, C.c_uint32, C.c_uint32, _vp], C.c_int),
@@ -362,6 +365,18 @@ class Store:
     def answer_batch_seeded_dev(self, d_seeds, B: int, d_out, d_mask=None, stream=None) -> None:
         _check(lib().xpir_answer_batch_seeded_dev(self.h, _ptr(d_seeds), B, _ptr(d_mask), _ptr(d_out),
                                                   _stream(stream)))
+
+    def answer_batch_seeded_peer_dev(self, d_seeds, B: int, out_ptrs: list[int], row_bounds: list[int],
+                                     stream=None) -> None:
+        """Shard scan whose epilogue XORs each answer row into its owner rank's buffer."""
+        ptrs = (_vp * len(out_ptrs))(*out_ptrs)
+        bounds = np.ascontiguousarray(row_bounds, np.uint32)
+        _check(lib().xpir_answer_batch_seeded_peer_dev(self.h, _ptr(d_seeds), B, ptrs, _p(bounds, _u32p),
+                                                       len(out_ptrs), _stream(stream)))
+
+
+def init_rows_dev(d_out, r0: int, r1: int, S: int, d_mask=None, device: int = 0, stream=None) -> None:
+    _check(lib().xpir_init_rows_dev(device, _ptr(d_out), r0, r1, S, _ptr(d_mask), _stream(stream)))
 
 
 def expand_queries_dev(d_seeds, B: int, byte_lo: int, nbytes: int, d_q, q_stride: int, device: int = 0,

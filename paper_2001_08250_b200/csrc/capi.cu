@@ -611,6 +611,48 @@ int xpir_answer_batch_seeded(xpir_store* st, const uint8_t* seeds, uint32_t B,
     return XPIR_OK;
 }
 
+int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, uint32_t B,
+                                      uint8_t* const* out_ptrs, const uint32_t* row_bounds, uint32_t n_ranks,
+                                      void* stream) {
+    if (!st) return fail(XPIR_EINVAL, "answer_batch_seeded_peer: null store");
+    if (n_ranks < 1 || n_ranks > 8) return fail(XPIR_EINVAL, "answer_batch_seeded_peer: 1..8 ranks");
+    if (!out_ptrs || !row_bounds || (B && !d_seeds)) return fail(XPIR_EINVAL, "answer_batch_seeded_peer: null");
+    if (row_bounds[0] != 0 || row_bounds[n_ranks] != B)
+        return fail(XPIR_EINVAL, "answer_batch_seeded_peer: row bounds must cover [0, B)");
+    if (st->S % 128 != 0 || B < 2048)
+        return fail(XPIR_EINVAL, "answer_batch_seeded_peer: fused reduce needs S % 128 == 0 and B >= 2048");
+    DeviceGuard g(st->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
+    const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
+    const uint64_t qs = m4rm_qstride(B);
+    XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
+    XCK(launch_expand_T(d_seeds, B, blo, nbw, st->qwin.as<uint8_t>(), qs, s));
+    M4Args a{st->data, st->nb(), st->S, st->qwin.as<uint8_t>(), qs, B, out_ptrs[0], s};
+    a.peers.n = n_ranks;
+    for (uint32_t k = 0; k < n_ranks; ++k) {
+        a.peers.ptr[k] = out_ptrs[k];
+        a.peers.bound[k] = row_bounds[k];
+    }
+    a.peers.bound[n_ranks] = row_bounds[n_ranks];
+    cudaEvent_t ev;
+    timing_begin(s, &ev);
+    XCK(launch_scan_m4rm_tmem(a, num_sms(st->device)));
+    timing_end(s, ev);
+    count_launches(2);
+    g_last_kernel = 5;
+    return XPIR_OK;
+}
+
+int xpir_init_rows_dev(int device, uint8_t* d_out, uint32_t r0, uint32_t r1, uint32_t S,
+                       const uint8_t* d_mask_seeds, void* stream) {
+    if (r1 < r0 || (r1 > r0 && !d_out)) return fail(XPIR_EINVAL, "init_rows: bad range");
+    DeviceGuard g(device);
+    XCK(launch_init_out(d_out + uint64_t(r0) * S, r1 - r0, S, d_mask_seeds ? d_mask_seeds + uint64_t(r0) * 32 : nullptr,
+                        false, static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    return XPIR_OK;
+}
+
 int xpir_expand_queries_dev(int device, const uint8_t* d_seeds, uint32_t B, uint64_t byte_lo,
                             uint64_t nbytes, uint8_t* d_q, uint64_t q_stride, void* stream) {
     if (B && (!d_seeds || !d_q)) return fail(XPIR_EINVAL, "expand_queries: null buffer");

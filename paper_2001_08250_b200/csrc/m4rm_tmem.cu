@@ -96,7 +96,7 @@ __device__ __forceinline__ void xor2(uint4& a, const uint4& b) {
 __global__ void __launch_bounds__(TM_NT, 1)
 k_scan_m4rm_tmem(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ qT,
                  uint64_t qstride, uint32_t B, uint8_t* __restrict__ out, uint32_t n_ctiles, uint32_t n_groups,
-                 uint64_t n_segments) {
+                 uint64_t n_segments, PeerOut peers) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const int tid = threadIdx.x;
@@ -279,7 +279,10 @@ k_scan_m4rm_tmem(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const 
                 for (int k = 0; k < 4; ++k) {
                     const uint32_t rl = slot0 + s + k;
                     if (rl < nvalid) {
-                        uint8_t* o = out + uint64_t(r_base + rl) * S + uint64_t(c) * 128 + l8 * 16;
+                        // fused cross-GPU reduce: with peers, the row is XORed straight into its
+                        // owner rank's answer buffer (NVLink peer atomics); otherwise locally
+                        uint8_t* const base = peers.n ? peers.owner_out(r_base + rl) : out;
+                        uint8_t* o = base + uint64_t(r_base + rl) * S + uint64_t(c) * 128 + l8 * 16;
                         red_xor64(o, uint64_t(v[k].y) << 32 | v[k].x);
                         red_xor64(o + 8, uint64_t(v[k].w) << 32 | v[k].z);
                     }
@@ -321,7 +324,7 @@ cudaError_t launch_scan_m4rm_tmem(const M4Args& a, int num_sms) {
     if (n_seg > max_seg) n_seg = max_seg;
     if (n_seg < 1) n_seg = 1;
     k_scan_m4rm_tmem<<<dim3(uint32_t(grid)), TM_NT, TM_SMEM, a.stream>>>(a.db, a.nb, a.S, a.qT, a.qstride, a.B,
-                                                                      a.out, n_ctiles, n_groups, n_seg);
+                                                                      a.out, n_ctiles, n_groups, n_seg, a.peers);
     return cudaGetLastError();
 }
 

@@ -22,6 +22,22 @@ struct ScanArgs {
     cudaStream_t stream;
 };
 
+// Fused cross-GPU reduction target: answer row r belongs to the rank g with
+// bound[g] <= r < bound[g+1]; every rank's buffer holds all B rows at the same
+// offsets (only the owner's rows are meaningful). n == 0: no peers.
+struct PeerOut {
+    uint8_t* ptr[8];
+    uint32_t bound[9];
+    uint32_t n;
+    __device__ __forceinline__ uint8_t* owner_out(uint32_t r) const {
+        uint32_t g = 0;
+#pragma unroll
+        for (int k = 1; k < 8; ++k)
+            if (k < int(n) && r >= bound[k]) g = k;
+        return ptr[g];
+    }
+};
+
 // M4RM scan (m4rm.cu): queries in the group-major layout qT[g*qstride + r].
 struct M4Args {
     const uint8_t* db;
@@ -31,6 +47,7 @@ struct M4Args {
     uint32_t B;
     uint8_t* out;
     cudaStream_t stream;
+    PeerOut peers{};     // set only by the sharded fused path (TMEM kernel)
 };
 cudaError_t launch_scan_m4rm(const M4Args& a, int ctas_per_sm, int num_sms, int variant);
 cudaError_t launch_scan_m4rm_tmem(const M4Args& a, int num_sms);

@@ -11,6 +11,12 @@ exchange is our own: every rank maps its peers' partial buffers through CUDA IPC
 (reduce-scatter: rank g owns requests [g*B/G, (g+1)*B/G)). The mask pad (K3) is
 applied exactly once, after the reduce, by the owner.
 
+Fused mode (B >= 2048, the half-TMEM M4RM kernel): the reduce disappears into
+the scan. Every owner first initialises its rows (mask pad or zero); then each
+rank's scan kernel XORs every accumulator flush straight into the owner rank's
+buffer over NVLink (64-bit peer atomics), so the partial answers never exist as
+separate buffers and the transfer overlaps the scan tile by tile.
+
 Control plane (handle exchange, barriers) goes through ``torch.distributed``; the
 data plane is peer memory only.
 """
@@ -56,7 +62,7 @@ def xor_reduce_scatter_reference(partials: list[np.ndarray], plan: ShardPlan, ra
 class ShardedScan:
     """Per-rank driver: local shard scan + peer XOR reduce-scatter (+ mask)."""
 
-    def __init__(self, xp, torch, dist, N: int, S: int, B: int, device: int):
+    def __init__(self, xp, torch, dist, N: int, S: int, B: int, device: int, fused: bool | None = None):
         self.xp, self.torch, self.dist = xp, torch, dist
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
         self.plan = ShardPlan(N, self.world)
@@ -69,6 +75,7 @@ class ShardedScan:
         self.r0, self.r1 = self.plan.row_range(self.rank, B)
         self.peers: list[int] = []
         self.src_ptrs = None
+        self.fused = (B >= 2048 and S % 128 == 0) if fused is None else bool(fused)
         self._exchange_handles()
 
     def _exchange_handles(self):
@@ -77,10 +84,14 @@ class ShardedScan:
         handles: list = [None] * self.world
         dist.all_gather_object(handles, h)
         self.peer_base = []
+        self.out_ptrs = []  # every rank's answer buffer, rank order (fused mode)
         for g, hg in enumerate(handles):
             if g == self.rank:
+                self.out_ptrs.append(self.partial.data_ptr())
                 continue
             self.peer_base.append(xp.ipc_open(hg, self.device))
+            self.out_ptrs.append(self.peer_base[-1])
+        self.row_bounds = [self.plan.row_range(g, self.B)[0] for g in range(self.world)] + [self.B]
         row = self.r0 * self.S
         ptrs = [p + row for p in self.peer_base]
         self.src_ptrs = torch.tensor(ptrs if ptrs else [0], dtype=torch.int64, device=f"cuda:{self.device}")
@@ -98,6 +109,8 @@ class ShardedScan:
         """One batch: partial scan of this shard, barrier, reduce own rows from
         peers, barrier. Returns the view of this rank's final rows."""
         xp, torch, dist = self.xp, self.torch, self.dist
+        if self.fused:
+            return self._step_fused(d_seeds, stream, d_mask)
         self.store.answer_batch_seeded_dev(d_seeds, self.B, self.partial, stream=stream)
         own = self.partial[self.r0:self.r1]
         if self.world > 1:
@@ -112,3 +125,20 @@ class ShardedScan:
             torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
             dist.barrier()  # peers finished reading our partial before it is overwritten
         return own
+
+    def _sync_barrier(self, stream):
+        torch = self.torch
+        torch.cuda.current_stream(self.device).synchronize() if stream is None else stream.synchronize()
+        if self.world > 1:
+            self.dist.barrier()
+
+    def _step_fused(self, d_seeds, stream, d_mask):
+        """Owner init -> barrier -> scan whose epilogue XORs into the owners'
+        buffers -> barrier. The second barrier also guarantees no peer still
+        writes our rows when the next step re-initialises them."""
+        xp = self.xp
+        xp.init_rows_dev(self.partial, self.r0, self.r1, self.S, d_mask, device=self.device, stream=stream)
+        self._sync_barrier(stream)
+        self.store.answer_batch_seeded_peer_dev(d_seeds, self.B, self.out_ptrs, self.row_bounds, stream=stream)
+        self._sync_barrier(stream)
+        return self.partial[self.r0:self.r1]

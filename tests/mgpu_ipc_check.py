@@ -1,4 +1,5 @@
-"""Multi-rank check of the sharded scan + CUDA-IPC XOR reduce-scatter, launched by
+"""Multi-rank check of the sharded scan + CUDA-IPC XOR reduce-scatter (or the
+fused variant whose scan epilogue XORs into the owners' buffers, XP_FUSED=1), launched by
 tests/test_gpu_sharded.py under torchrun. With fewer GPUs than ranks every rank
 uses the same device (peer mapping of another process's allocation on the same
 GPU is still CUDA IPC) and the control plane is gloo; the kernels never wait on
@@ -30,7 +31,10 @@ def main():
     key = bytes(range(32))
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    sh = ShardedScan(xp, torch, dist, N, S, B, dev)
+    fused = {"1": True, "0": False}.get(os.environ.get("XP_FUSED", ""), None)
+    sh = ShardedScan(xp, torch, dist, N, S, B, dev, fused=fused)
+    if rank == 0:
+        print(f"mode={'fused' if sh.fused else 'reduce'}", flush=True)
     sh.store.fill_keystream(key, 7)
     seeds = torch.zeros((B, 32), dtype=torch.uint8, device="cuda")
     xp.keystream_rows_dev(key, 100, B, 32, seeds, 32, device=dev)

@@ -1,5 +1,6 @@
 """GPU: the sharded scan's real data path — per-rank shard scans, CUDA-IPC peer
-mapping and the K4 XOR reduce-scatter, mask applied once by the owner — run as a
+mapping and the K4 XOR reduce-scatter (or the fused scan epilogue that XORs into
+the owners' rows over peer memory), mask applied once by the owner — run as a
 2- and 3-rank torchrun job (ranks share the GPU when fewer are present) and
 compared bit-exactly with the unsharded scan."""
 import os
@@ -22,9 +23,13 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("world,N,S,B", [(2, 8192, 512, 300), (3, 4096 + 24, 256, 130), (2, 1024, 4096, 64)])
-def test_sharded_ipc_reduce(cuda, world, N, S, B):
-    env = dict(os.environ, XP_N=str(N), XP_S=str(S), XP_B=str(B))
+@pytest.mark.parametrize("world,N,S,B,fused", [
+    (2, 8192, 512, 300, "0"), (3, 4096 + 24, 256, 130, "0"), (2, 1024, 4096, 64, "0"),
+    # fused epilogue: peer atomics straight into the owner's rows (TMEM kernel, B >= 2048)
+    (2, 8192, 512, 2100, "1"), (3, 16384 + 40, 1024, 4096, "1"), (4, 4096, 256, 2048 + 3, "1"),
+])
+def test_sharded_ipc_reduce(cuda, world, N, S, B, fused):
+    env = dict(os.environ, XP_N=str(N), XP_S=str(S), XP_B=str(B), XP_FUSED=fused)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "mgpu_ipc_check.py")]
