@@ -361,7 +361,7 @@ def main():
     roof = {
         "bound": "alu",
         "kernel": {1: "k_scan_direct", 2: "k_scan_m4rm", 5: "k_scan_m4rm_tmem",
-                   6: "k_scan_nib", 7: "k_scan_m4rm4"}.get(xp.last_scan_kernel(), "?"),
+                   6: "k_scan_nib", 7: "k_scan_m4rm4", 8: "k_scan_m4rm_q"}.get(xp.last_scan_kernel(), "?"),
         "unit": "Tops/s (32-bit masked-XOR lane ops)",
         "achieved": achieved / 1e12,
         "peak": peaks["lop3_per_s"] / 1e12,

@@ -134,12 +134,14 @@ int xpir_xor_reduce_dev(int device, uint8_t* d_dst, const uint8_t* const* d_srcs
 typedef struct {
     int kernel;        /* 0 = auto, 1 = direct select-XOR, 2 = M4RM byte tables (auto variant),
                           4 = M4RM register accumulators, 5 = M4RM half-TMEM accumulators,
-                          6 = warp-private nibble tables, 7 = M4RM nibble tables */
+                          6 = warp-private nibble tables, 7 = M4RM nibble tables,
+                          8 = M4RM quad-interleaved 32-byte-column tables with full-TMEM
+                              accumulators (auto for B >= 2048, S % 32 == 0) */
     int ctas_per_sm;   /* 0 = auto */
     int reserved[6];
 } xpir_scan_opts;
 int xpir_set_scan_opts(const xpir_scan_opts* o);
-/* Which kernel the last scan used (1 direct, 2 M4RM, 3 byte-granular). */
+/* Which kernel the last scan used (the ids above; 3 = byte-granular, 5 = M4RM half-TMEM). */
 int xpir_last_scan_kernel(void);
 /* When enabled, CUDA events bracket every scan-kernel launch on its own stream;
  * collect returns the summed kernel milliseconds and launch count since the last

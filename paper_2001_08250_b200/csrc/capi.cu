@@ -412,6 +412,7 @@ uint64_t xpir_query_window_bytes(const xpir_store* st) {
 static uint32_t g_nib_min_batch = 0xffffffffu;
 static uint32_t g_k4_min_batch = 24;   // nibble-table M4RM (kernel 7) from here
 static uint32_t g_m4_min_batch = 257;  // byte-table M4RM (kernels 2/5) from here
+static uint32_t g_q_min_batch = 2048;  // quad-table full-TMEM M4RM (kernel 8) from here
 
 static int choose_kernel(const xpir_store* st, uint32_t B) {
     int k;
@@ -421,10 +422,14 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
     }
     if (st->S % 16 != 0) return 3;
     const bool m4_ok = (st->S % 128) == 0;
+    const bool q_ok = (st->S % 32) == 0;
     if (k == 4 || k == 5) k = 2;  // forced M4RM variants (registers-only / TMEM accumulators)
-    if (k == 0)
+    if (k == 0) {
+        if (q_ok && B >= g_q_min_batch) return 8;
         k = !m4_ok ? 1 : B >= g_m4_min_batch ? 2 : B >= g_k4_min_batch ? 7 : B >= g_nib_min_batch ? 6 : 1;
+    }
     if ((k == 2 || k == 6 || k == 7) && !m4_ok) k = 1;
+    if (k == 8 && !q_ok) k = 1;
     return k;
 }
 
@@ -438,6 +443,14 @@ static int run_m4(xpir_store* st, const uint8_t* qT, uint64_t qstride, uint32_t 
     }
     M4Args a{st->data, st->nb(), st->S, qT, qstride, B, d_out, s};
     cudaEvent_t ev;
+    if (kernel == 8) {  // quad-interleaved 32-byte-column tables, full-TMEM accumulators
+        timing_begin(s, &ev);
+        XCK(launch_scan_m4rm_q(a, num_sms(st->device)));
+        timing_end(s, ev);
+        count_launches(1);
+        g_last_kernel = 8;
+        return XPIR_OK;
+    }
     if (kernel == 7) {  // nibble tables
         timing_begin(s, &ev);
         XCK(launch_scan_m4rm4(a, num_sms(st->device)));
@@ -493,7 +506,7 @@ static int scan_rows(xpir_store* st, const uint8_t* rows, uint64_t stride, uint3
     if (B == 0) return XPIR_OK;
     const int k = choose_kernel(st, B);
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
-    if (k != 2 && k != 7) return run_rows(st, k, rows + blo, stride, B, d_out, s);
+    if (k != 2 && k != 7 && k != 8) return run_rows(st, k, rows + blo, stride, B, d_out, s);
     const uint64_t qs = m4rm_qstride(B);
     XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
     XCK(launch_transpose_q(rows, stride, blo, nbw, B, st->qwin.as<uint8_t>(), qs, s));
@@ -528,7 +541,7 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
     // K2: expand only this shard's window of every request's selection vector,
     // straight into the layout the chosen scan kernel reads.
-    if (k == 2 || k == 7) {
+    if (k == 2 || k == 7 || k == 8) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
         XCK(launch_expand_T(d_seeds, B, blo, nbw, st->qwin.as<uint8_t>(), qs, s));
@@ -571,7 +584,7 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
     count_launches(1);
     const int k = choose_kernel(st, B);
     int rc;
-    if (k == 2 || k == 7) {
+    if (k == 2 || k == 7 || k == 8) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
         XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s));
@@ -619,8 +632,8 @@ int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, ui
     if (!out_ptrs || !row_bounds || (B && !d_seeds)) return fail(XPIR_EINVAL, "answer_batch_seeded_peer: null");
     if (row_bounds[0] != 0 || row_bounds[n_ranks] != B)
         return fail(XPIR_EINVAL, "answer_batch_seeded_peer: row bounds must cover [0, B)");
-    if (st->S % 128 != 0 || B < 2048)
-        return fail(XPIR_EINVAL, "answer_batch_seeded_peer: fused reduce needs S % 128 == 0 and B >= 2048");
+    if (st->S % 32 != 0 || B < 2048)
+        return fail(XPIR_EINVAL, "answer_batch_seeded_peer: fused reduce needs S % 32 == 0 and B >= 2048");
     DeviceGuard g(st->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
@@ -636,10 +649,10 @@ int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, ui
     a.peers.bound[n_ranks] = row_bounds[n_ranks];
     cudaEvent_t ev;
     timing_begin(s, &ev);
-    XCK(launch_scan_m4rm_tmem(a, num_sms(st->device)));
+    XCK(launch_scan_m4rm_q(a, num_sms(st->device)));
     timing_end(s, ev);
     count_launches(2);
-    g_last_kernel = 5;
+    g_last_kernel = 8;
     return XPIR_OK;
 }
 

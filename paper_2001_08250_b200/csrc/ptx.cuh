@@ -37,8 +37,9 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(addr), "r"(v));
 }
+// 64-bit XOR reduction into global memory (local or NVLink peer address).
 __device__ __forceinline__ void red_xor64(void* p, uint64_t v) {
-    atomicXor(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+    asm volatile("red.relaxed.gpu.global.xor.b64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
 }
 
 }  // namespace ptx

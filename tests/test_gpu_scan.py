@@ -288,6 +288,25 @@ def test_m4rm_variants_match_oracle(xp, port, cuda, kernel, N, S, B):
     assert xp.last_scan_kernel() == (5 if kernel == 5 else 2)
 
 
+@pytest.mark.parametrize("N,S,B", [
+    (1000, 32, 1), (4096, 64, 130), (2048, 96, 2048), (3001, 384, 2500), (777, 1024, 4097),
+    (64, 128, 6000), (5000, 160, 8192), (131, 4096, 9000), (100003, 32, 2049), (40, 32, 16385),
+])
+def test_m4rm_quad_tables_match_oracle(xp, port, cuda, N, S, B):
+    """Quad-interleaved 32-byte-column tables with full-TMEM accumulators (8), forced
+    at any batch size: partial 2048/4096/8192-request tiles, bucket counts that end
+    mid-group and mid-set, bucket sizes that are multiples of 32 but not of 128."""
+    g = np.random.default_rng(N * 5 + S + B)
+    db = rand(g, N * S)
+    q = rand(g, B, (N + 7) // 8)
+    xp.set_scan_opts(8)
+    st = xp.Store(N, S)
+    st.upload(db)
+    got = st.answer_batch(q)
+    assert xp.last_scan_kernel() == 8
+    assert np.array_equal(got, port.answer_batch(db, N, S, q, B))
+
+
 def test_concurrent_host_calls_on_one_store(xp, port, cuda):
     """answer/answer_batch are re-entrant over an immutable snapshot:
     several host threads (ctypes releases the GIL) query one store at once."""
