@@ -189,8 +189,9 @@ def traffic_from_profile(n_buckets, batch, world, kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel from the committed ncu capture of this same workload (profiles/),
     or None when the capture does not match the configuration being run."""
-    path = os.path.join(ROOT, "profiles", "r01_traffic_m4rm_tmem.json")
-    if kernel != 5 or world != 1 or n_buckets != 1 << 20 or batch != BATCH or not os.path.exists(path):
+    name = {5: "m4rm_tmem", 8: "m4rm_q"}.get(kernel)
+    path = os.path.join(ROOT, "profiles", f"r01_traffic_{name}.json")
+    if name is None or world != 1 or n_buckets != 1 << 20 or batch != BATCH or not os.path.exists(path):
         return None
     with open(path) as f:
         t = json.load(f)
@@ -379,7 +380,7 @@ def main():
         "hbm": {"achieved_GBps": hbm_bytes / (per_launch_ms * 1e-3) / 1e9, "peak_GBps": hbm_peak,
                 "peak_source": peak_src, "frac": hbm_bytes / (per_launch_ms * 1e-3) / 1e9 / hbm_peak,
                 "bytes_per_launch": hbm_bytes},
-        "traffic_source": "profiles/r01_traffic_m4rm_tmem.json (ncu dram__bytes_read+write of this kernel "
+        "traffic_source": "profiles/r01_traffic_<kernel>.json (ncu dram__bytes_read+write of this kernel "
                           "on this workload; algorithmic bytes per launch = hbm.bytes_per_launch)",
         "kernel_share_of_step": (scan_ms / args.steps) / ms_per_step,
     }
