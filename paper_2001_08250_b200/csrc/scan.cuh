@@ -128,6 +128,10 @@ struct CuckooState {
 cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32_t* beta1,
                                const uint32_t* beta2, uint64_t i0, uint64_t n, uint32_t* reports,
                                cudaStream_t s);
+// warp-cooperative walk (walk.cu); used by launch_cuckoo_walk when supported
+bool walk_w_supported(const CuckooDev& d);
+cudaError_t launch_cuckoo_walk_w(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
+                                 uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s);
 cudaError_t launch_cuckoo_apply(const CuckooDev& d, const CuckooState* st_host_copy,
                                 uint8_t* table, const uint8_t* payload, cudaStream_t s);
 
