@@ -158,6 +158,27 @@ int xpir_measure_peaks(int device, double* lop3_per_s, double* smem_bytes_per_s,
 int xpir_probe_tmem(int device, int variant, double* bytes_per_clk_sm);
 
 /* ------------------------------------------------------------------------ */
+/* Read batcher ("Read requests are batched and forwarded to   */
+/* the GPU"): concurrent single-request callers — server::answer_share       */
+/* (server.cpp:115-135) from node.cpp's session/link threads — are coalesced  */
+/* into one scan. A batch is sealed when it holds max_batch requests or       */
+/* max_wait_us after its first request; two pinned batches alternate (one     */
+/* forming while the other is scanned). Callers pack their own query and      */
+/* unpack their own answer. Thread-safe; the store must outlive the batcher.  */
+/* ------------------------------------------------------------------------ */
+typedef struct xpir_batcher xpir_batcher;
+
+int xpir_batcher_create(xpir_store* st, uint32_t max_batch, uint32_t max_wait_us, xpir_batcher** out);
+/* Waits for the requests already submitted, then stops the worker. */
+int xpir_batcher_destroy(xpir_batcher* b);
+/* Blocking: out (bucket_size bytes) = pir::answer(snapshot, q) (pir.cpp:29-39), or
+ * pir::mask_answer(pir::answer(snapshot, q), mask_seed) when mask_seed != NULL
+ * (answer_share, server.cpp:122-123). q holds ceil(N/8) bytes; q_bits must be N. */
+int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, const uint8_t* mask_seed,
+                        uint8_t* out);
+int xpir_batcher_stats(xpir_batcher* b, uint64_t* requests, uint64_t* batches, uint64_t* max_batch_seen);
+
+/* ------------------------------------------------------------------------ */
 /* Intra-box peer memory for the sharded reduce (CUDA IPC over NVLink).       */
 /* ------------------------------------------------------------------------ */
 #define XPIR_IPC_HANDLE_BYTES 64

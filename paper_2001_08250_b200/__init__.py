@@ -21,6 +21,7 @@ cuckoo::Table              ``Table``
 notify::Window             ``Window``
 crypto::prf                ``prf_batch``
 notify::make_interest      ``make_interest_batch``
+answer_share batching      ``Batcher`` (concurrent single requests -> one scan)
 =========================  ==================================================
 """
 from __future__ import annotations
@@ -139,6 +140,10 @@ _SIGS = {
     "xpir_server_seal": ([_vp, _u64p], C.c_int),
     "xpir_server_snapshot": ([_vp, C.c_uint64, C.POINTER(_vp)], C.c_int),
     "xpir_server_info": ([_vp, _u64p, _u64p, _u64p, C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
+    "xpir_batcher_create": ([_vp, C.c_uint32, C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "xpir_batcher_destroy": ([_vp], C.c_int),
+    "xpir_batcher_answer": ([_vp, _u8p, C.c_uint32, _u8p, _u8p], C.c_int),
+    "xpir_batcher_stats": ([_vp, _u64p, _u64p, _u64p], C.c_int),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
@@ -373,6 +378,40 @@ class Store:
         bounds = np.ascontiguousarray(row_bounds, np.uint32)
         _check(lib().xpir_answer_batch_seeded_peer_dev(self.h, _ptr(d_seeds), B, ptrs, _p(bounds, _u32p),
                                                        len(out_ptrs), _stream(stream)))
+
+
+class Batcher:
+    """Read batcher over a store (include/xpir.h): ``answer`` is safe to call from
+    many threads at once — concurrent single requests (server::answer_share,
+    server.cpp:115-135) are coalesced into one scan of up to ``max_batch``
+    requests, sealed ``max_wait_us`` after its first request."""
+
+    def __init__(self, store: Store, max_batch: int = 1024, max_wait_us: int = 200):
+        h = _vp()
+        _check(lib().xpir_batcher_create(store.h, max_batch, max_wait_us, C.byref(h)))
+        self.h, self.store = h, store
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().xpir_batcher_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def answer(self, q, mask_seed: bytes | None = None, q_bits: int | None = None) -> np.ndarray:
+        """pir::answer(snapshot, q), or mask_answer(answer(..), mask_seed) (pir.cpp:29-39, 65-69)."""
+        qa = _u8(q).reshape(-1)
+        if qa.size < (self.store.N + 7) // 8:
+            raise InvalidArgument(XPIR_EINVAL, "answer: query length mismatch")
+        out = np.empty(self.store.S, np.uint8)
+        ms = _p(_u8(mask_seed)) if mask_seed is not None else None
+        _check(lib().xpir_batcher_answer(self.h, _p(qa), self.store.N if q_bits is None else q_bits, ms, _p(out)))
+        return out
+
+    def stats(self) -> dict:
+        r, b, m = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().xpir_batcher_stats(self.h, C.byref(r), C.byref(b), C.byref(m)))
+        return {"requests": r.value, "batches": b.value, "max_batch_seen": m.value}
 
 
 def init_rows_dev(d_out, r0: int, r1: int, S: int, d_mask=None, device: int = 0, stream=None) -> None:

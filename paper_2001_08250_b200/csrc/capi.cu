@@ -22,6 +22,7 @@
 namespace xpir {
 static std::atomic<uint64_t> g_launches{0};
 void count_launches(uint64_t n) { g_launches += n; }
+int set_error(int code, const std::string& msg);
 }  // namespace xpir
 
 using namespace xpir;
@@ -37,6 +38,12 @@ int fail(int code, const std::string& msg) {
     g_err = msg;
     return code;
 }
+
+}  // namespace
+
+int xpir::set_error(int code, const std::string& msg) { return fail(code, msg); }
+
+namespace {
 
 #define XCK(expr)                                                                       \
     do {                                                                                \
@@ -425,7 +432,12 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
     const bool q_ok = (st->S % 32) == 0;
     if (k == 4 || k == 5) k = 2;  // forced M4RM variants (registers-only / TMEM accumulators)
     if (k == 0) {
-        if (q_ok && B >= g_q_min_batch) return 8;
+        // B >= 2048: quad tables (8) or the half-TMEM 128-byte-column kernel (2 -> 5),
+        // whichever the sweep-calibrated cost model says is faster for this B
+        if (q_ok && B >= g_q_min_batch) {
+            const double c5 = m4_ok ? double((uint64_t(B) + 2047) / 2048 * 2048) / 3.12 : 1e300;
+            return m4rm_q_cost(B, nullptr) < c5 ? 8 : 2;
+        }
         k = !m4_ok ? 1 : B >= g_m4_min_batch ? 2 : B >= g_k4_min_batch ? 7 : B >= g_nib_min_batch ? 6 : 1;
     }
     if ((k == 2 || k == 6 || k == 7) && !m4_ok) k = 1;

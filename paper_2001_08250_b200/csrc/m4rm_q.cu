@@ -308,20 +308,30 @@ cudaError_t launch_q(const M4Args& a, int num_sms) {
 
 }  // namespace
 
-// Request-tile size for a batch: the tile (2048 / 4096 / 8192 requests) with the
-// least modelled pipe time, ceil(B/Rc) * (1.06 Rc + 400) wavefronts per set.
-int m4rm_q_tile(uint32_t B) {
-    int best = 2048;
-    double best_cost = 1e300;
-    for (int rc : {2048, 4096, 8192}) {
-        const double tiles = double((uint64_t(B) + rc - 1) / rc);
-        const double cost = tiles * (1.06 * rc + 400.0);
-        if (cost < best_cost * 0.999) {
-            best_cost = cost;
-            best = rc;
+// Modelled time of a batch (arbitrary units: padded requests / measured
+// efficiency) for each tile size; the efficiencies are the config-5 sweep's
+// fractions of the dense-ALU roofline at full tiles (profiles/r01_config5_sweep*):
+// 2048 -> 2.65, 4096 -> 3.02, 8192 -> 3.33 (the half-TMEM 128-byte-column kernel: 3.12).
+double m4rm_q_cost(uint32_t B, int* tile) {
+    static const int rcs[3] = {2048, 4096, 8192};
+    static const double eff[3] = {2.65, 3.02, 3.33};
+    double best = 1e300;
+    int best_rc = 2048;
+    for (int k = 0; k < 3; ++k) {
+        const double cost = double((uint64_t(B) + rcs[k] - 1) / rcs[k] * rcs[k]) / eff[k];
+        if (cost < best * 0.999) {
+            best = cost;
+            best_rc = rcs[k];
         }
     }
+    if (tile) *tile = best_rc;
     return best;
+}
+
+int m4rm_q_tile(uint32_t B) {
+    int t = 2048;
+    m4rm_q_cost(B, &t);
+    return t;
 }
 
 cudaError_t launch_scan_m4rm_q(const M4Args& a, int num_sms) {

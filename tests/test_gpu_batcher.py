@@ -1,0 +1,80 @@
+"""GPU parity of the read batcher (xpir_batcher_*): concurrent single requests —
+server::answer_share's scan + mask step (server.cpp:115-135) issued from many
+host threads as node.cpp does — are coalesced into device batches, and every
+caller gets exactly pir::answer / pir::mask_answer(pir::answer(..)) of its own
+query (pir.cpp:29-39, 65-69). Bit-exact against the oracle."""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_threads(fn, n):
+    errs = []
+
+    def wrap(t):
+        try:
+            fn(t)
+        except BaseException as e:  # noqa: BLE001 - surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=wrap, args=(t,)) for t in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+
+
+@pytest.mark.parametrize("N,S,max_batch,wait_us", [(4096, 512, 64, 2000), (1001, 128, 7, 500), (257, 4096, 1, 0)])
+def test_concurrent_answers_match_oracle(xp, port, cuda, N, S, max_batch, wait_us):
+    g = np.random.default_rng(N + S + max_batch)
+    db = g.integers(0, 256, N * S, dtype=np.uint8)
+    st = xp.Store(N, S)
+    st.upload(db)
+    bt = xp.Batcher(st, max_batch=max_batch, max_wait_us=wait_us)
+    T, R = 24, 5
+    nb = (N + 7) // 8
+    qs = g.integers(0, 256, (T, R, nb), dtype=np.uint8)
+    if N % 8:
+        qs[..., -1] &= (1 << (N % 8)) - 1
+    seeds = g.integers(0, 256, (T, R, 32), dtype=np.uint8)
+    got = np.zeros((T, R, S), np.uint8)
+
+    def worker(t):
+        for r in range(R):
+            masked = (t + r) % 2 == 0
+            got[t, r] = bt.answer(qs[t, r], mask_seed=seeds[t, r].tobytes() if masked else None)
+
+    _run_threads(worker, T)
+    plain = port.answer_batch(db, N, S, qs.reshape(T * R, nb), T * R).reshape(T, R, S)
+    for t in range(T):
+        for r in range(R):
+            want = plain[t, r].tobytes()
+            if (t + r) % 2 == 0:
+                want = port.mask_answer(want, seeds[t, r].tobytes())
+            assert got[t, r].tobytes() == want, (t, r)
+    s = bt.stats()
+    assert s["requests"] == T * R
+    assert s["max_batch_seen"] <= max_batch
+    if max_batch > 1:
+        assert s["batches"] < T * R  # requests were coalesced
+    bt.close()
+    st.close()
+
+
+def test_query_length_mismatch_raises(xp, cuda):
+    st = xp.Store(64, 32)
+    st.upload(np.zeros(64 * 32, np.uint8))
+    bt = xp.Batcher(st, max_batch=8, max_wait_us=100)
+    with pytest.raises(xp.InvalidArgument):
+        bt.answer(np.zeros(8, np.uint8), q_bits=63)  # pir.cpp:30-31
+    # the batcher keeps serving after a rejected call
+    q = np.zeros(8, np.uint8)
+    q[0] = 1
+    assert bt.answer(q).tobytes() == bytes(32)
+    bt.close()
+    st.close()
