@@ -12,6 +12,11 @@
 // (server.hpp:70-71). The first answer against a snapshot uploads
 // it to HBM; later calls reuse the device copy, keyed by (data pointer, size,
 // geometry, epoch, content fingerprint). Thread-safe.
+//
+// Single answers (pir::answer — what server::answer_share calls per client
+// read, from node.cpp's session and link threads concurrently) go through a
+// read batcher per resident snapshot (xpir_batcher_*), so concurrent reads are
+// coalesced into one device scan instead of one scan each.
 #include <cstring>
 #include <list>
 #include <memory>
@@ -56,11 +61,21 @@ struct Resident {
     uint32_t buckets = 0, bucket_size = 0;
     uint64_t epoch = 0, fp = 0;
     xpir_store* st = nullptr;
+    std::once_flag batcher_once;
+    xpir_batcher* batcher = nullptr;
     Resident() = default;
     Resident(const Resident&) = delete;
     Resident& operator=(const Resident&) = delete;
     ~Resident() {
+        if (batcher) xpir_batcher_destroy(batcher);
         if (st) xpir_store_destroy(st);
+    }
+    xpir_batcher* reads() {
+        std::call_once(batcher_once, [this] {
+            // up to 1024 reads per scan; a batch is sealed 200 us after its first read
+            xpir_check(xpir_batcher_create(st, 1024, 200, &batcher), "pir: batcher_create");
+        });
+        return batcher;
     }
 };
 
@@ -147,7 +162,11 @@ std::vector<bytes> answer_batch(const Snapshot& snap, const std::vector<QueryVec
 
 bytes answer(const Snapshot& snap, const QueryVector& q) {
     if (q.bit_count != snap.bucket_count) throw std::invalid_argument("answer: query length mismatch");
-    return answer_batch(snap, {q}).front();
+    bytes out(snap.bucket_size, 0);
+    if (snap.bucket_count == 0 || snap.bucket_size == 0) return out;
+    auto res = cache().get(snap);
+    xpir_check(xpir_batcher_answer(res->reads(), q.data.data(), snap.bucket_count, nullptr, out.data()), "answer");
+    return out;
 }
 
 // pir.cpp:54-63 (client / leader side)

@@ -49,3 +49,14 @@ def test_reference_suite_against_dropin(suite, cuda):
     assert out_b.returncode == out_r.returncode
     if suite != "test_server":
         assert out_b.returncode == 0 and sum_b.group(3) == "0"
+
+
+def test_concurrent_reads_through_dropin(cuda):
+    """64 threads x 12 pir::answer + mask_answer calls on one Snapshot through the
+    drop-in TU (the read batcher coalesces them); host-XOR checker."""
+    exe = os.path.join(DROPIN, "dropin_mt_b200")
+    if not os.path.exists(exe):
+        pytest.skip("drop-in binaries not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(out.stdout, out.stderr[-2000:])
+    assert out.returncode == 0 and "0 mismatches" in out.stdout
