@@ -15,19 +15,22 @@
 
 #include <cstdint>
 
+#include "ptx.cuh"
 #include "scan.cuh"
 
 namespace xpir {
 
+using ptx::red_xor64;
+
 constexpr int DIRECT_NT = 256;
 
-template <int RPT>
+template <int RPT, int W>
 __global__ void __launch_bounds__(DIRECT_NT)
 k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ q,
               uint64_t q_stride, uint32_t B, uint8_t* __restrict__ out, uint32_t bpc, uint32_t cw) {
-    constexpr int RB = RPT < 8 ? RPT : 8;  // requests reduced per shared-memory round
-    __shared__ uint4 red[DIRECT_NT * RB];
-    const uint32_t ncol = S / 16;
+    constexpr int RB = RPT < 4 ? RPT : 4;  // requests reduced per shared-memory round
+    __shared__ uint4 red[DIRECT_NT * RB * W];
+    const uint32_t ncol = S / (16 * W);  // thread columns of W x 16 bytes
     const uint32_t tid = threadIdx.x;
     const uint32_t phases = DIRECT_NT / cw;
     const uint32_t p = tid / cw;
@@ -41,12 +44,31 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
     const uint32_t jb = split * bpc + p * L;
     const uint32_t je = min(nb, jb + L);
 
-    uint4 acc[RPT];
+    uint4 acc[RPT][W];
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[i] = make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < RPT; ++i)
+#pragma unroll
+        for (int w = 0; w < W; ++w) acc[i][w] = make_uint4(0, 0, 0, 0);
+
+    // acc ^= bucket when the request selects it: one predicate per (request, bucket)
+    // shared by the W x 4 predicated XORs (the bucket's 16W bytes in this thread)
+    auto step = [&](const uint4 (&v)[W], const uint32_t (&qw)[RPT], uint32_t bit) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i)
+            if (qw[i] & bit) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    acc[i][w].x ^= v[w].x;
+                    acc[i][w].y ^= v[w].y;
+                    acc[i][w].z ^= v[w].z;
+                    acc[i][w].w ^= v[w].w;
+                }
+            }
+    };
 
     if (active) {
-        const uint4* col = reinterpret_cast<const uint4*>(db) + c;
+        const uint4* col = reinterpret_cast<const uint4*>(db) + uint64_t(c) * W;
+        const uint64_t stride = S / 16;
         for (uint32_t jc = jb; jc < je; jc += 32) {
             const uint32_t n = min(32u, je - jc);
             uint32_t qw[RPT];
@@ -60,53 +82,45 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                         if (8 * k < n) w |= uint32_t(__ldg(qp + k)) << (8 * k);
                 }
                 if (n < 32) w &= (1u << n) - 1u;
-                qw[i] = __brev(w);  // bucket jc+jj -> bit 31-jj
+                qw[i] = w;  // bucket jc+jj -> bit jj (pir.hpp:25)
             }
             if (n == 32) {
 #pragma unroll 8
                 for (uint32_t jj = 0; jj < 32; ++jj) {
-                    const uint4 v = __ldcs(col + uint64_t(jc + jj) * ncol);
+                    uint4 v[W];
 #pragma unroll
-                    for (int i = 0; i < RPT; ++i) {
-                        const uint32_t m = uint32_t(int32_t(qw[i]) >> 31);
-                        qw[i] <<= 1;
-                        acc[i].x ^= v.x & m;
-                        acc[i].y ^= v.y & m;
-                        acc[i].z ^= v.z & m;
-                        acc[i].w ^= v.w & m;
-                    }
+                    for (int w = 0; w < W; ++w) v[w] = __ldcs(col + uint64_t(jc + jj) * stride + w);
+                    step(v, qw, 1u << jj);
                 }
             } else {
                 for (uint32_t jj = 0; jj < n; ++jj) {
-                    const uint4 v = __ldcs(col + uint64_t(jc + jj) * ncol);
+                    uint4 v[W];
 #pragma unroll
-                    for (int i = 0; i < RPT; ++i) {
-                        const uint32_t m = uint32_t(int32_t(qw[i]) >> 31);
-                        qw[i] <<= 1;
-                        acc[i].x ^= v.x & m;
-                        acc[i].y ^= v.y & m;
-                        acc[i].z ^= v.z & m;
-                        acc[i].w ^= v.w & m;
-                    }
+                    for (int w = 0; w < W; ++w) v[w] = __ldcs(col + uint64_t(jc + jj) * stride + w);
+                    step(v, qw, 1u << jj);
                 }
             }
         }
     }
-    // XOR-reduce the phases that share a column, then one plain store per (request, column)
+    // XOR-reduce the phases that share a column, then one atomic XOR per (request, word pair)
     if (phases > 1) {
 #pragma unroll
         for (int i0 = 0; i0 < RPT; i0 += RB) {
 #pragma unroll
-            for (int i = 0; i < RB; ++i) red[i * DIRECT_NT + tid] = acc[i0 + i];
+            for (int i = 0; i < RB; ++i)
+#pragma unroll
+                for (int w = 0; w < W; ++w) red[(i * W + w) * DIRECT_NT + tid] = acc[i0 + i][w];
             __syncthreads();
             if (p == 0 && active) {
                 for (uint32_t ph = 1; ph < phases; ++ph)
 #pragma unroll
-                    for (int i = 0; i < RB; ++i) {
-                        const uint4 v = red[i * DIRECT_NT + ph * cw + tid];
-                        acc[i0 + i].x ^= v.x; acc[i0 + i].y ^= v.y;
-                        acc[i0 + i].z ^= v.z; acc[i0 + i].w ^= v.w;
-                    }
+                    for (int i = 0; i < RB; ++i)
+#pragma unroll
+                        for (int w = 0; w < W; ++w) {
+                            const uint4 v = red[(i * W + w) * DIRECT_NT + ph * cw + tid];
+                            acc[i0 + i][w].x ^= v.x; acc[i0 + i][w].y ^= v.y;
+                            acc[i0 + i][w].z ^= v.z; acc[i0 + i][w].w ^= v.w;
+                        }
             }
             __syncthreads();
         }
@@ -115,22 +129,23 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
             if (r0 + i < B) {
-                unsigned long long* o =
-                    reinterpret_cast<unsigned long long*>(out + uint64_t(r0 + i) * S + uint64_t(c) * 16);
-                atomicXor(o, (unsigned long long)acc[i].y << 32 | acc[i].x);
-                atomicXor(o + 1, (unsigned long long)acc[i].w << 32 | acc[i].z);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    uint8_t* o = out + uint64_t(r0 + i) * S + (uint64_t(c) * W + w) * 16;
+                    red_xor64(o, (unsigned long long)acc[i][w].y << 32 | acc[i][w].x);
+                    red_xor64(o + 8, (unsigned long long)acc[i][w].w << 32 | acc[i][w].z);
+                }
             }
     }
 }
 
-template <int RPT>
+template <int RPT, int W>
 static cudaError_t launch_direct_t(const ScanArgs& a, int num_sms, uint32_t* nsplit_out) {
-    const uint32_t ncol = a.S / 16;
-    const uint32_t cw = ncol >= DIRECT_NT ? DIRECT_NT : ncol;  // columns per CTA
+    const uint32_t ncol = a.S / (16 * W);
+    const uint32_t cw = ncol >= DIRECT_NT ? DIRECT_NT : ncol;  // thread columns per CTA
     const uint32_t phases = DIRECT_NT / cw;
     const uint32_t gx = (ncol + cw - 1) / cw;
     const uint32_t gz = (a.B + RPT - 1) / RPT;
-    const uint64_t out_bytes = uint64_t(a.B) * a.S;
     // ~8 CTAs per SM; each phase gets a multiple of 32 buckets
     const uint64_t per = uint64_t(gx) * gz;
     uint64_t nsplit = (uint64_t(num_sms) * 8 + per - 1) / per;
@@ -142,19 +157,22 @@ static cudaError_t launch_direct_t(const ScanArgs& a, int num_sms, uint32_t* nsp
     bpc = (bpc + unit - 1) / unit * unit;
     nsplit = (a.nb + bpc - 1) / bpc;
     if (nsplit < 1) nsplit = 1;
-    k_scan_direct<RPT><<<dim3(gz, gx, uint32_t(nsplit)), DIRECT_NT, 0, a.stream>>>(
+    k_scan_direct<RPT, W><<<dim3(gz, gx, uint32_t(nsplit)), DIRECT_NT, 0, a.stream>>>(
         a.db, a.nb, a.S, a.q, a.q_stride, a.B, a.out, uint32_t(bpc), cw);
     *nsplit_out = uint32_t(nsplit);
-    (void)out_bytes;
     return cudaGetLastError();
 }
 
 cudaError_t launch_scan_direct(const ScanArgs& a, int num_sms, uint32_t* nsplit_out) {
-    if (a.B <= 1) return launch_direct_t<1>(a, num_sms, nsplit_out);
-    if (a.B <= 2) return launch_direct_t<2>(a, num_sms, nsplit_out);
-    if (a.B <= 4) return launch_direct_t<4>(a, num_sms, nsplit_out);
-    if (a.B <= 8) return launch_direct_t<8>(a, num_sms, nsplit_out);
-    return launch_direct_t<16>(a, num_sms, nsplit_out);
+    // B > 4: 32 bytes per thread (one predicate feeds 8 XORs) when the bucket allows
+    // it; request tiles of at most 8 keep the accumulators in 64 registers
+    // (HBM-bound batches of <= 4 keep 16-byte columns: more threads per bucket row)
+    if (a.S % 32 == 0 && a.B > 4) return launch_direct_t<8, 2>(a, num_sms, nsplit_out);
+    if (a.B <= 1) return launch_direct_t<1, 1>(a, num_sms, nsplit_out);
+    if (a.B <= 2) return launch_direct_t<2, 1>(a, num_sms, nsplit_out);
+    if (a.B <= 4) return launch_direct_t<4, 1>(a, num_sms, nsplit_out);
+    if (a.B <= 8) return launch_direct_t<8, 1>(a, num_sms, nsplit_out);
+    return launch_direct_t<16, 1>(a, num_sms, nsplit_out);
 }
 
 }  // namespace xpir

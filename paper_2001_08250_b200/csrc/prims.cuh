@@ -185,4 +185,26 @@ XP_HD uint32_t bloom_position(const uint8_t* item, uint32_t len, uint32_t i, uin
 #endif
 }
 
+// bloom_positions for the make_interest item (notify.cpp:30-35): LogId (16 B) ||
+// BE64(seq), then LE32(i) — 28 message bytes, so m[4..15] are compile-time zero
+// and the message words never touch local memory. w0/w1 = the LogId as LE words,
+// w2 = the BE64 sequence number read as an LE word.
+XP_HD uint32_t bloom_position_interest(uint64_t w0, uint64_t w1, uint64_t w2, uint32_t i, uint32_t m_bits) {
+    uint64_t m[16];
+    m[0] = w0;
+    m[1] = w1;
+    m[2] = w2;
+    m[3] = uint64_t(i);
+#ifdef __CUDA_ARCH__
+#pragma unroll
+#endif
+    for (int k = 4; k < 16; ++k) m[k] = 0;
+    const uint64_t v = blake2b64_oneblock(m, 28);
+#ifdef __CUDA_ARCH__
+    return uint32_t(__umul64hi(v, uint64_t(m_bits)));
+#else
+    return uint32_t((unsigned __int128)v * m_bits >> 64);
+#endif
+}
+
 }  // namespace xpir

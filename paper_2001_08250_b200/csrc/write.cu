@@ -100,13 +100,16 @@ __global__ void k_interest(Id16 id, const uint64_t* __restrict__ seqs, uint64_t 
     if (t >= n * h) return;
     const uint64_t w = t / h;
     const uint32_t k = uint32_t(t - w * h);
-    uint8_t item[24];
+    uint64_t w0 = 0, w1 = 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) item[i] = id.b[i];
-    const uint64_t seq = seqs[w];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) item[16 + i] = uint8_t(seq >> (56 - 8 * i));  // BE64 (notify.cpp:33)
-    const uint32_t pos = bloom_position(item, 24, k, m_bits);
+    for (int i = 0; i < 8; ++i) {
+        w0 |= uint64_t(id.b[i]) << (8 * i);
+        w1 |= uint64_t(id.b[8 + i]) << (8 * i);
+    }
+    // item = LogId || BE64(seq) (notify.cpp:33): the BE64 bytes read as an LE word
+    const uint64_t w2 = __byte_perm(uint32_t(seqs[w] >> 32), 0, 0x0123) |
+                        uint64_t(__byte_perm(uint32_t(seqs[w]), 0, 0x0123)) << 32;
+    const uint32_t pos = bloom_position_interest(w0, w1, w2, k, m_bits);
     if (pos_out) pos_out[t] = pos;
     if (words) atomicOr(words + (pos >> 6), 1ull << (pos & 63));
 }
