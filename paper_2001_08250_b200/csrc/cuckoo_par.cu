@@ -124,6 +124,11 @@ __global__ void k_par_write(CuckooDev d, uint64_t limit, const uint32_t* __restr
 // Runs on the first `n` inserts of a batch whose walk state is `h` (host copy,
 // batch_id set, n_touched == 0, no GC possible within n). Returns the length k
 // of the eviction-free prefix it applied (0 if it declined) and advances h.
+// Keys are (bucket << 32 | 2*insert + which), written in ascending insert order,
+// and CUB's radix sort is stable: sorting the bucket field alone (bits 32 ..
+// end_bit) yields the (bucket, insert, which) order in ceil(log2(buckets+1)) / 8
+// passes instead of 6. The field is one bit wider than the largest bucket so the
+// ~0 "no claim" keys sort after every real bucket.
 static int sort_end_bit(uint32_t buckets) {
     int end_bit = 32;
     while (end_bit < 64 && (uint64_t(1) << (end_bit - 32)) <= buckets) ++end_bit;
@@ -151,7 +156,7 @@ cudaError_t cuckoo_reserve(CuckooParScratch& sc, uint64_t n, uint32_t buckets, c
     if (e != cudaSuccess) return e;
     size_t tmp = 0;
     e = cub::DeviceRadixSort::SortKeys(nullptr, tmp, static_cast<unsigned long long*>(sc.keys_a),
-                                       static_cast<unsigned long long*>(sc.keys_b), int(m), 0,
+                                       static_cast<unsigned long long*>(sc.keys_b), int(m), 32,
                                        sort_end_bit(buckets), s);
     if (e != cudaSuccess) return e;
     grow(&sc.cub_tmp, tmp, sc.cub_cap);
@@ -176,19 +181,22 @@ cudaError_t cuckoo_parallel_prefix(const CuckooDev& d, CuckooState& h, const uin
     if ((e = cudaMemsetAsync(outcome, 1, n, s)) != cudaSuccess) return e;
     uint64_t k = 0;
     bool converged = false;
-    for (int it = 0; it < 48; ++it) {
-        k_par_keys<<<gn, 256, 0, s>>>(n, b1, b2, outcome, keys_in);
-        size_t tb = sc.cub_cap;
-        e = cub::DeviceRadixSort::SortKeys(sc.cub_tmp, tb, keys_in, keys, int(m), 0, end_bit, s);
-        if (e != cudaSuccess) return e;
-        k_par_rank<<<gm, 256, 0, s>>>(keys, m, d.used, d.depth, succ);
-        unsigned long long init[2] = {~0ull, ~0ull};
-        if ((e = cudaMemcpyAsync(flags, init, 16, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
-        k_par_update<<<gn, 256, 0, s>>>(n, outcome, succ, flags);
+    // Iterations run in pairs between host checks: once the fixed point is reached
+    // a further iteration changes nothing, so the pair's last flags decide.
+    for (int it = 0; it < 48; it += 2) {
+        for (int rep = 0; rep < 2; ++rep) {
+            k_par_keys<<<gn, 256, 0, s>>>(n, b1, b2, outcome, keys_in);
+            size_t tb = sc.cub_cap;
+            e = cub::DeviceRadixSort::SortKeys(sc.cub_tmp, tb, keys_in, keys, int(m), 32, end_bit, s);
+            if (e != cudaSuccess) return e;
+            k_par_rank<<<gm, 256, 0, s>>>(keys, m, d.used, d.depth, succ);
+            if ((e = cudaMemsetAsync(flags, 0xff, 16, s)) != cudaSuccess) return e;
+            k_par_update<<<gn, 256, 0, s>>>(n, outcome, succ, flags);
+        }
         unsigned long long f[2];
         if ((e = cudaMemcpyAsync(f, flags, 16, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
         if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-        count_launches(4);
+        count_launches(8);
         const uint64_t first_evict = f[1] == ~0ull ? n : f[1];
         const uint64_t first_change = f[0] == ~0ull ? n : f[0];
         if (first_change >= first_evict) {
