@@ -271,6 +271,21 @@ int xpir_window_info(const xpir_window* win, uint64_t* size, uint64_t* base);
 int xpir_window_delta(const xpir_window* win, uint64_t i, uint64_t* out_words);
 /* Window::digest (notify.cpp:87-107). */
 int xpir_window_digest(const xpir_window* win, uint8_t out[32]);
+/* Window::digest(count) over the oldest `count` deltas (notify.cpp:91-107). */
+int xpir_window_digest_n(const xpir_window* win, uint64_t count, uint8_t out[32]);
+/* notify::encode_delta (notify.cpp:131-149) of delta i (0 = oldest), encoded on
+ * device: varint(m) || varint(ones) || varint(first position) || varint(gaps).
+ * out == NULL: *len = size only. EINVAL when cap < *len. */
+int xpir_window_encode_delta(xpir_window* win, uint64_t i, uint8_t* out, uint64_t cap, uint64_t* len);
+/* The same from device buffers: d_words holds ceil(m_bits/64) LE words; d_out may
+ * be NULL (size query). */
+int xpir_encode_delta_dev(int device, const uint64_t* d_words, uint32_t m_bits, uint8_t* d_out, uint64_t cap,
+                          uint64_t* len, void* stream);
+/* notify::decode_delta (notify.cpp:151-170), decoded on device. XPIR_EINVAL is the
+ * reference's std::nullopt (malformed input). words == NULL: header only
+ * (*m_bits); else words receives ceil(m/64) words (EINVAL if words_cap is short). */
+int xpir_decode_delta(int device, const uint8_t* buf, uint64_t len, uint32_t* m_bits, uint64_t* words,
+                      uint64_t words_cap);
 
 /* ------------------------------------------------------------------------ */
 /* Replica state machine — server::ServerCore (server.hpp:57-98,             */
@@ -296,6 +311,10 @@ int xpir_server_seal(xpir_server* sv, uint64_t* epoch);            /* seal_epoch
 /* snapshot_at (server.cpp:83-87); epoch 0 = latest. The store stays owned by the
  * server and valid until its epoch leaves the ring. */
 int xpir_server_snapshot(xpir_server* sv, uint64_t epoch, xpir_store** st);
+/* ServerCore::make_freeze (server.cpp:45-56): base, newest (= window newest - 1),
+ * digest over the frozen deltas and their count; their wire bytes are
+ * xpir_window_encode_delta(window, k, ...) for k < count. */
+int xpir_server_freeze(xpir_server* sv, uint64_t* base, uint64_t* newest, uint8_t digest[32], uint64_t* count);
 int xpir_server_info(xpir_server* sv, uint64_t* writes, uint64_t* latest_epoch, uint64_t* oldest_epoch,
                      xpir_table** table, xpir_window** window);
 

@@ -93,10 +93,17 @@ class Port:
         L.xo_window_absorb.argtypes = [C.c_void_p, _u32p, C.c_uint64]
         L.xo_window_rotate.argtypes = [C.c_void_p]
         L.xo_window_digest.argtypes = [C.c_void_p, _u8p]
+        L.xo_window_digest_n.argtypes = [C.c_void_p, C.c_uint64, _u8p]
+        L.xo_window_base.argtypes = [C.c_void_p]
+        L.xo_window_base.restype = C.c_uint64
         L.xo_window_size.argtypes = [C.c_void_p]
         L.xo_window_size.restype = C.c_uint64
         L.xo_window_delta.argtypes = [C.c_void_p, C.c_uint64]
         L.xo_window_delta.restype = C.c_void_p
+        L.xo_encode_delta.argtypes = [C.c_uint32, _u64p, _u8p, C.c_uint64]
+        L.xo_encode_delta.restype = C.c_uint64
+        L.xo_decode_delta.argtypes = [_u8p, C.c_uint64, _u32p, _u64p, C.c_uint64]
+        L.xo_decode_delta.restype = C.c_int
 
     # primitives
     def chacha20(self, key: bytes, nonce: bytes, n: int, block0: int = 0) -> bytes:
@@ -160,6 +167,24 @@ class Port:
 
     def window(self, m, h, w) -> "PortWindow":
         return PortWindow(self, m, h, w)
+
+    # interest-delta codecs (notify.cpp:131-170)
+    def encode_delta(self, m: int, words: np.ndarray) -> bytes:
+        w = np.ascontiguousarray(words, np.uint64)
+        n = self.lib.xo_encode_delta(m, _p(w, _u64p), None, 0)
+        out = np.zeros(max(n, 1), np.uint8)
+        self.lib.xo_encode_delta(m, _p(w, _u64p), _p(out), n)
+        return out[:n].tobytes()
+
+    def decode_delta(self, buf: bytes):
+        """(m_bits, words) or None (the reference's nullopt)."""
+        b = _u8(buf) if len(buf) else np.zeros(1, np.uint8)
+        m = C.c_uint32()
+        if not self.lib.xo_decode_delta(_p(b), len(buf), C.byref(m), None, 0):
+            return None
+        w = np.zeros((m.value + 63) // 64, np.uint64)
+        self.lib.xo_decode_delta(_p(b), len(buf), C.byref(m), _p(w, _u64p), len(w))
+        return m.value, w
 
 
 class PortRng:
@@ -261,6 +286,14 @@ class PortWindow:
         self.port.lib.xo_window_digest(self.h, _p(out))
         return out.tobytes()
 
+    def base(self) -> int:
+        return self.port.lib.xo_window_base(self.h)
+
+    def digest_n(self, count: int) -> bytes:
+        out = np.zeros(32, np.uint8)
+        self.port.lib.xo_window_digest_n(self.h, count, _p(out))
+        return out.tobytes()
+
     def size(self) -> int:
         return self.port.lib.xo_window_size(self.h)
 
@@ -325,6 +358,11 @@ class Ref:
         L.ref_window_size.argtypes = [C.c_void_p]
         L.ref_window_size.restype = C.c_uint64
         L.ref_window_delta_words.argtypes = [C.c_void_p, C.c_uint64, _u64p]
+        L.ref_encode_delta.argtypes = [C.c_uint32, _u64p, _u8p, C.c_uint64]
+        L.ref_encode_delta.restype = C.c_int64
+        L.ref_decode_delta.argtypes = [_u8p, C.c_uint64, _u32p, _u64p, C.c_uint64]
+        L.ref_decode_delta.restype = C.c_int
+        L.ref_window_digest_n.argtypes = [C.c_void_p, C.c_uint64, _u8p]
 
     def _chk(self, rc):
         if rc == -1:
@@ -386,6 +424,22 @@ class Ref:
 
     def window(self, m, h, w) -> "RefWindow":
         return RefWindow(self, m, h, w)
+
+    def encode_delta(self, m: int, words: np.ndarray) -> bytes:
+        w = np.ascontiguousarray(words, np.uint64)
+        n = self.lib.ref_encode_delta(m, _p(w, _u64p), None, 0)
+        out = np.zeros(max(n, 1), np.uint8)
+        self.lib.ref_encode_delta(m, _p(w, _u64p), _p(out), n)
+        return out[:n].tobytes()
+
+    def decode_delta(self, buf: bytes):
+        b = _u8(buf) if len(buf) else np.zeros(1, np.uint8)
+        m = C.c_uint32()
+        if not self.lib.ref_decode_delta(_p(b), len(buf), C.byref(m), None, 0):
+            return None
+        w = np.zeros((m.value + 63) // 64, np.uint64)
+        self.lib.ref_decode_delta(_p(b), len(buf), C.byref(m), _p(w, _u64p), len(w))
+        return m.value, w
 
 
 class RefRng:
@@ -498,9 +552,12 @@ class RefWindow:
     def rotate(self):
         self.ref.lib.ref_window_rotate(self.h)
 
-    def digest(self) -> bytes:
+    def digest(self, count: int | None = None) -> bytes:
         out = np.zeros(32, np.uint8)
-        self.ref.lib.ref_window_digest(self.h, _p(out))
+        if count is None:
+            self.ref.lib.ref_window_digest(self.h, _p(out))
+        else:
+            self.ref.lib.ref_window_digest_n(self.h, count, _p(out))
         return out.tobytes()
 
     def size(self) -> int:

@@ -284,4 +284,25 @@ void ref_window_delta_words(void* w, uint64_t i, uint64_t* out) {
     std::memcpy(out, d.words.data(), d.words.size() * 8);
 }
 
+// notify::encode_delta / decode_delta (notify.cpp:131-170), Window::digest(count)
+int64_t ref_encode_delta(uint32_t m, const uint64_t* words, uint8_t* out, uint64_t cap) {
+    notify::DeltaFilter d = notify::DeltaFilter::empty(m);
+    std::memcpy(d.words.data(), words, d.words.size() * 8);
+    bytes enc = notify::encode_delta(d);
+    if (out && enc.size() <= cap) std::memcpy(out, enc.data(), enc.size());
+    return int64_t(enc.size());
+}
+// 1 ok (m, words filled when words_cap suffices), 0 nullopt
+int ref_decode_delta(const uint8_t* buf, uint64_t len, uint32_t* m, uint64_t* words, uint64_t words_cap) {
+    auto d = notify::decode_delta(byte_view(buf, len));
+    if (!d) return 0;
+    *m = d->m_bits;
+    if (words && d->words.size() <= words_cap) std::memcpy(words, d->words.data(), d->words.size() * 8);
+    return 1;
+}
+void ref_window_digest_n(void* w, uint64_t count, uint8_t* out32) {
+    auto d = static_cast<notify::Window*>(w)->digest(count);
+    std::memcpy(out32, d.data(), 32);
+}
+
 }  // extern "C"

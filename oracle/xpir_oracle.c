@@ -539,6 +539,10 @@ void xo_window_rotate(xo_window* x) { /* :67-73 */
 }
 
 void xo_window_digest(const xo_window* x, uint8_t out[32]) { /* :89-107 */
+    xo_window_digest_n(x, x->n, out);
+}
+
+void xo_window_digest_n(const xo_window* x, uint64_t count, uint8_t out[32]) { /* Window::digest(count), :91-107 */
     xo_blake2b_state h;
     xo_blake2b_init(&h, 32);
     xo_blake2b_update(&h, (const uint8_t*)"interest-window-v1", 18);
@@ -546,8 +550,8 @@ void xo_window_digest(const xo_window* x, uint8_t out[32]) { /* :89-107 */
     upd_u64be(&h, x->h);
     upd_u64be(&h, x->w);
     upd_u64be(&h, x->base);
-    upd_u64be(&h, x->n);
-    for (uint64_t i = 0; i < x->n; ++i) {
+    upd_u64be(&h, count);
+    for (uint64_t i = 0; i < count && i < x->n; ++i) {
         /* raw words in host (little-endian) order, notify.cpp:103-104 */
         uint8_t b[8];
         for (uint64_t k = 0; k < x->words; ++k) {
@@ -561,3 +565,91 @@ void xo_window_digest(const xo_window* x, uint8_t out[32]) { /* :89-107 */
 uint64_t xo_window_size(const xo_window* x) { return x->n; }
 uint64_t xo_window_base(const xo_window* x) { return x->base; }
 const uint64_t* xo_window_delta(const xo_window* x, uint64_t i) { return x->deltas[i]; }
+
+/* ---- interest-delta codecs (notify.cpp:110-170) ---------------------------- */
+static uint64_t xo_put_varint(uint8_t* out, uint64_t at, uint64_t cap, uint64_t v) { /* :110-116 */
+    while (v >= 0x80) {
+        if (out && at < cap) out[at] = (uint8_t)(v | 0x80);
+        ++at;
+        v >>= 7;
+    }
+    if (out && at < cap) out[at] = (uint8_t)v;
+    return at + 1;
+}
+
+static int xo_get_varint(const uint8_t* buf, uint64_t len, uint64_t* at, uint64_t* out) { /* :118-129 */
+    uint64_t v = 0;
+    int shift = 0;
+    while (*at < len && shift < 64) {
+        uint8_t b = buf[(*at)++];
+        v |= (uint64_t)(b & 0x7f) << shift;
+        if (!(b & 0x80)) {
+            *out = v;
+            return 1;
+        }
+        shift += 7;
+    }
+    return 0;
+}
+
+uint64_t xo_encode_delta(uint32_t m_bits, const uint64_t* words, uint8_t* out, uint64_t cap) { /* :131-149 */
+    const uint64_t nw = ((uint64_t)m_bits + 63) / 64;
+    uint64_t ones = 0;
+    for (uint64_t w = 0; w < nw; ++w) ones += (uint64_t)__builtin_popcountll(words[w]);
+    uint64_t need = xo_put_varint(NULL, 0, 0, m_bits);
+    need = xo_put_varint(NULL, need, 0, ones);
+    uint64_t prev = 0;
+    int first = 1;
+    for (uint64_t w = 0; w < nw; ++w) {
+        uint64_t x = words[w];
+        while (x) {
+            uint64_t pos = w * 64 + (uint64_t)__builtin_ctzll(x);
+            need = xo_put_varint(NULL, need, 0, first ? pos : pos - prev);
+            prev = pos;
+            first = 0;
+            x &= x - 1;
+        }
+    }
+    if (!out || cap < need) return need;
+    uint64_t at = xo_put_varint(out, 0, cap, m_bits);
+    at = xo_put_varint(out, at, cap, ones);
+    prev = 0;
+    first = 1;
+    for (uint64_t w = 0; w < nw; ++w) {
+        uint64_t x = words[w];
+        while (x) {
+            uint64_t pos = w * 64 + (uint64_t)__builtin_ctzll(x);
+            at = xo_put_varint(out, at, cap, first ? pos : pos - prev);
+            prev = pos;
+            first = 0;
+            x &= x - 1;
+        }
+    }
+    return need;
+}
+
+int xo_decode_delta(const uint8_t* buf, uint64_t len, uint32_t* m_bits, uint64_t* words,
+                    uint64_t words_cap) { /* :151-170 */
+    uint64_t at = 0, m = 0, count = 0;
+    if (!xo_get_varint(buf, len, &at, &m) || !xo_get_varint(buf, len, &at, &count)) return 0;
+    if (m == 0 || m > 0xffffffffull) return 0;
+    const uint64_t nw = (m + 63) / 64;
+    int fill = words && words_cap >= nw;
+    if (fill) memset(words, 0, nw * 8);
+    uint64_t pos = 0;
+    for (uint64_t i = 0; i < count; ++i) {
+        uint64_t gap;
+        if (!xo_get_varint(buf, len, &at, &gap)) return 0;
+        if (i == 0)
+            pos = gap;
+        else {
+            if (gap == 0) return 0;
+            pos += gap;
+        }
+        if (pos >= m) return 0;
+        if (fill) words[pos >> 6] |= 1ull << (pos & 63);
+    }
+    if (at != len) return 0;
+    *m_bits = (uint32_t)m;
+    return 1;
+}

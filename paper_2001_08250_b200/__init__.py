@@ -140,6 +140,11 @@ _SIGS = {
     "xpir_server_seal": ([_vp, _u64p], C.c_int),
     "xpir_server_snapshot": ([_vp, C.c_uint64, C.POINTER(_vp)], C.c_int),
     "xpir_server_info": ([_vp, _u64p, _u64p, _u64p, C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
+    "xpir_window_digest_n": ([_vp, C.c_uint64, _u8p], C.c_int),
+    "xpir_window_encode_delta": ([_vp, C.c_uint64, _u8p, C.c_uint64, _u64p], C.c_int),
+    "xpir_encode_delta_dev": ([C.c_int, _vp, C.c_uint32, _vp, C.c_uint64, _u64p, _vp], C.c_int),
+    "xpir_decode_delta": ([C.c_int, _u8p, C.c_uint64, _u32p, _u64p, C.c_uint64], C.c_int),
+    "xpir_server_freeze": ([_vp, _u64p, _u64p, _u8p, _u64p], C.c_int),
     "xpir_batcher_create": ([_vp, C.c_uint32, C.c_uint32, C.POINTER(_vp)], C.c_int),
     "xpir_batcher_destroy": ([_vp], C.c_int),
     "xpir_batcher_answer": ([_vp, _u8p, C.c_uint32, _u8p, _u8p], C.c_int),
@@ -631,10 +636,50 @@ class Window:
         _check(lib().xpir_window_delta(self.h, i, _p(out, _u64p)))
         return out
 
-    def digest(self) -> bytes:
+    def digest(self, count: int | None = None) -> bytes:
+        """Window::digest() / digest(count) (notify.cpp:89-107)."""
         out = np.empty(32, np.uint8)
-        _check(lib().xpir_window_digest(self.h, _p(out)))
+        if count is None:
+            _check(lib().xpir_window_digest(self.h, _p(out)))
+        else:
+            _check(lib().xpir_window_digest_n(self.h, count, _p(out)))
         return out.tobytes()
+
+    def encode_delta(self, i: int) -> bytes:
+        """notify::encode_delta(delta(i)) (notify.cpp:131-149), encoded on device."""
+        return _window_encode(self.h, i)
+
+
+def _window_encode(h, i: int) -> bytes:
+    n = C.c_uint64()
+    _check(lib().xpir_window_encode_delta(h, i, None, 0, C.byref(n)))
+    out = np.empty(max(n.value, 1), np.uint8)
+    _check(lib().xpir_window_encode_delta(h, i, _p(out), n.value, C.byref(n)))
+    return out[:n.value].tobytes()
+
+
+def decode_delta(buf: bytes, device: int = 0):
+    """notify::decode_delta (notify.cpp:151-170) on device: (m_bits, words) or None
+    for malformed input (the reference's std::nullopt)."""
+    b = _u8(buf) if len(buf) else np.zeros(1, np.uint8)
+    m = C.c_uint32()
+    rc = lib().xpir_decode_delta(device, _p(b), len(buf), C.byref(m), None, 0)
+    if rc == XPIR_EINVAL:
+        return None
+    _check(rc)
+    w = np.zeros(max((m.value + 63) // 64, 1), np.uint64)
+    rc = lib().xpir_decode_delta(device, _p(b), len(buf), C.byref(m), _p(w, _u64p), len(w))
+    if rc == XPIR_EINVAL:
+        return None
+    _check(rc)
+    return m.value, w[:(m.value + 63) // 64]
+
+
+def encode_delta_dev(d_words, m_bits: int, d_out=None, cap: int = 0, device: int = 0, stream=None) -> int:
+    """Device-buffer encode; returns the encoded length (d_out None: size query)."""
+    n = C.c_uint64()
+    _check(lib().xpir_encode_delta_dev(device, _ptr(d_words), m_bits, _ptr(d_out), cap, C.byref(n), _stream(stream)))
+    return n.value
 
 
 # ---------------------------------------------------------------------------
@@ -712,3 +757,13 @@ class Server:
         out = np.empty(32, np.uint8)
         _check(lib().xpir_table_state_digest(self._handles()[0], _p(out)))
         return out.tobytes()
+
+    def freeze(self) -> dict:
+        """ServerCore::make_freeze (server.cpp:45-56): base, newest, digest and the
+        device-encoded frozen deltas (notify::encode_delta)."""
+        base, newest, count = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        dg = np.empty(32, np.uint8)
+        _check(lib().xpir_server_freeze(self.h, C.byref(base), C.byref(newest), _p(dg), C.byref(count)))
+        w = self._handles()[1]
+        return {"base": base.value, "newest": newest.value, "digest": dg.tobytes(),
+                "deltas": [_window_encode(w, k) for k in range(count.value)]}

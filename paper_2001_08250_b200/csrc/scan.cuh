@@ -93,6 +93,15 @@ cudaError_t launch_absorb(const uint32_t* pos, uint64_t n, uint32_t m_bits,
 cudaError_t launch_draws(const uint8_t* key_host32, uint64_t nonce0, uint32_t count, uint64_t* out,
                          cudaStream_t s);
 
+// Interest-delta codecs (codec.cu): notify::encode_delta / decode_delta.
+size_t encode_delta_scratch_bytes(uint64_t nwords);
+size_t decode_delta_scratch_bytes(uint64_t len);
+cudaError_t launch_encode_delta(const uint64_t* words, uint64_t nwords, uint32_t m_bits, uint8_t* out, uint64_t cap,
+                                unsigned long long* len_out, void* scratch, size_t scratch_bytes, cudaStream_t s);
+// hdr: 5 x u64 of device memory; hdr[0] = 0 ok / 1 malformed / 2 words_cap too small, hdr[1] = m
+cudaError_t launch_decode_delta(const uint8_t* buf, uint64_t len, uint64_t* words, uint64_t words_cap,
+                                unsigned long long* hdr, void* scratch, size_t scratch_bytes, cudaStream_t s);
+
 // Device-resident cuckoo metadata (one per table).
 struct CuckooDev {
     uint32_t buckets, depth;

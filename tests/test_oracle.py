@@ -202,3 +202,46 @@ def test_port_vs_reference_cuckoo(port, ref):
         A, B = port.table(nb, depth, cap, 16, seed), ref.table(nb, depth, cap, 16, seed)
         assert np.array_equal(A.insert_batch(b1, b2, pl), B.insert_batch(b1, b2, pl))
         assert A.state_digest() == B.state_digest()
+
+
+# --- interest-delta codecs (notify.cpp:131-170), pinned by tests/golden/codec.json --------
+def _codec_words(c):
+    if c.get("words_zero"):
+        return np.zeros((c["m"] + 63) // 64, np.uint64)
+    return np.frombuffer(bytes.fromhex(c["words"]), np.uint64)
+
+
+def test_codec_golden(port):
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "codec.json")) as f:
+        G = json.load(f)
+    for c in G["cases"]:
+        if "words_sha256" in c:
+            continue  # config-3 delta: checked on the GPU path
+        w = _codec_words(c)
+        enc = port.encode_delta(c["m"], w)
+        assert enc.hex() == c["enc"], c["name"]
+        m, back = port.decode_delta(enc)
+        assert m == c["m"] and np.array_equal(back, w), c["name"]
+    assert len(bytes.fromhex([c for c in G["cases"] if c["name"] == "empty_2p23"][0]["enc"])) <= 8  # test_notify.cpp:135-139
+    for d in G["decode"]:
+        r = port.decode_delta(bytes.fromhex(d["buf"]))
+        assert (r is not None) == d["valid"], d["name"]
+        if r is not None:
+            assert r[0] == d["m"] and r[1].tobytes().hex() == d["words"], d["name"]
+
+
+def test_codec_port_vs_reference(port, ref):
+    g = np.random.default_rng(77)
+    for m in (1, 7, 64, 129, 5000, 1 << 16):
+        for density in (0.0, 0.001, 0.2, 0.7):
+            w = np.zeros((m + 63) // 64, np.uint64)
+            for p in np.nonzero(g.random(m) < density)[0]:
+                w[p >> 6] |= np.uint64(1) << np.uint64(p & 63)
+            enc = port.encode_delta(m, w)
+            assert enc == ref.encode_delta(m, w)
+            for cut in (0, 1, len(enc) // 2, len(enc) - 1):
+                bad = enc[:cut]
+                assert (port.decode_delta(bad) is None) == (ref.decode_delta(bad) is None)
