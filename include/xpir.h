@@ -88,6 +88,14 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
 int xpir_answer_batch_seeded(xpir_store* st, const uint8_t* seeds, uint32_t batch,
                              const uint8_t* mask_seeds, uint8_t* out);
 
+/* Seed-compressed read shares (l-1 of a read's l shares as 32-byte PRG seeds, only
+ * the last explicit): request r is a seed when is_seed[r], its vector then being
+ * prng_expand(seed, ceil(N/8)) (crypto.cpp:35-45), else an explicit vector.
+ * seeds holds the seeded requests' seeds and q (stride q_stride) the explicit
+ * requests' vectors, each compacted in request order. out / mask_seeds as above. */
+int xpir_answer_batch_mixed(xpir_store* st, uint32_t batch, const uint8_t* is_seed, const uint8_t* seeds,
+                            const uint8_t* q, uint64_t q_stride, uint32_t q_bits, const uint8_t* mask_seeds,
+                            uint8_t* out);
 /* Device-pointer variants. d_q rows hold the FULL ceil(N/8)-byte vector
  * (the shard reads bytes [lo/8, ceil(hi/8))). d_out is batch*S bytes. */
 int xpir_answer_batch_dev(xpir_store* st, const uint8_t* d_q, uint64_t q_stride,

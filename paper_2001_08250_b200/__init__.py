@@ -140,6 +140,7 @@ _SIGS = {
     "xpir_server_seal": ([_vp, _u64p], C.c_int),
     "xpir_server_snapshot": ([_vp, C.c_uint64, C.POINTER(_vp)], C.c_int),
     "xpir_server_info": ([_vp, _u64p, _u64p, _u64p, C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
+    "xpir_answer_batch_mixed": ([_vp, C.c_uint32, _u8p, _u8p, _u8p, C.c_uint64, C.c_uint32, _u8p, _u8p], C.c_int),
     "xpir_window_digest_n": ([_vp, C.c_uint64, _u8p], C.c_int),
     "xpir_window_encode_delta": ([_vp, C.c_uint64, _u8p, C.c_uint64, _u64p], C.c_int),
     "xpir_encode_delta_dev": ([C.c_int, _vp, C.c_uint32, _vp, C.c_uint64, _u64p, _vp], C.c_int),
@@ -364,6 +365,22 @@ class Store:
         out = np.empty((B, self.S), np.uint8)
         ms = None if mask_seeds is None else _u8(mask_seeds).reshape(B, 32)
         _check(lib().xpir_answer_batch_seeded(self.h, _p(s), B, None if ms is None else _p(ms), _p(out)))
+        return out
+
+    def answer_batch_mixed(self, is_seed, seeds, rows, mask_seeds=None) -> np.ndarray:
+        """Seed-compressed shares: request r is prng_expand(seed) when is_seed[r], else
+        an explicit vector; `seeds` (n_seeded x 32) and `rows` (n_explicit x ceil(N/8))
+        are compacted in request order."""
+        f = np.ascontiguousarray(is_seed, np.uint8).reshape(-1)
+        B = f.size
+        ns = int(f.sum())
+        sd = _u8(seeds).reshape(ns, 32) if ns else np.zeros((1, 32), np.uint8)
+        nb = (self.N + 7) // 8
+        q = _u8(rows).reshape(B - ns, -1) if B - ns else np.zeros((1, nb), np.uint8)
+        out = np.empty((B, self.S), np.uint8)
+        ms = None if mask_seeds is None else _u8(mask_seeds).reshape(B, 32)
+        _check(lib().xpir_answer_batch_mixed(self.h, B, _p(f), _p(sd), _p(q), q.shape[1], self.N,
+                                             None if ms is None else _p(ms), _p(out)))
         return out
 
     # device variants (torch tensors or raw pointers)

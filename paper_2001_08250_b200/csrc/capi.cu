@@ -158,7 +158,7 @@ struct xpir_store {
     uint64_t epoch = 0;
     uint8_t* data = nullptr;
     cudaStream_t stream = nullptr;
-    DevBuf q, out, seeds, masks, qwin;
+    DevBuf q, out, seeds, masks, qwin, qx, idx;
     std::mutex mu;
     uint32_t nb() const { return hi - lo; }
     uint64_t bytes() const { return uint64_t(nb()) * S; }
@@ -343,6 +343,8 @@ int xpir_store_destroy(xpir_store* st) {
     st->seeds.release();
     st->masks.release();
     st->qwin.release();
+    st->qx.release();
+    st->idx.release();
     cudaStreamDestroy(st->stream);
     delete st;
     return XPIR_OK;
@@ -583,6 +585,74 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
     XCK(st->q.ensure(ws * B));
     // H2D of the shard's window of every row (pitched copy); rows start at byte 0
     XCK(cudaMemcpy2DAsync(st->q.p, ws, q + blo, q_stride, nbw, B, cudaMemcpyHostToDevice, s));
+    const uint8_t* dm = nullptr;
+    if (mask_seeds) {
+        XCK(st->masks.ensure(uint64_t(B) * 32));
+        XCK(cudaMemcpyAsync(st->masks.p, mask_seeds, uint64_t(B) * 32, cudaMemcpyHostToDevice, s));
+        dm = st->masks.as<uint8_t>();
+    }
+    const uint64_t ob = uint64_t(B) * st->S;
+    XCK(st->out.ensure(ob));
+    uint8_t* dout = st->out.as<uint8_t>();
+    XCK(launch_init_out(dout, B, st->S, dm, false, s));
+    count_launches(1);
+    const int k = choose_kernel(st, B);
+    int rc;
+    if (k == 2 || k == 7 || k == 8) {
+        const uint64_t qs = m4rm_qstride(B);
+        XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
+        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s));
+        count_launches(1);
+        rc = run_m4(st, st->qwin.as<uint8_t>(), qs, B, dout, s, k);
+    } else {
+        rc = run_rows(st, k, st->q.as<uint8_t>(), ws, B, dout, s);
+    }
+    if (rc) return rc;
+    XCK(cudaMemcpyAsync(out, st->out.p, ob, cudaMemcpyDeviceToHost, s));
+    XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+// Seed-compressed read shares: a batch where request r is
+// either an explicit selection vector or a 32-byte PRG seed whose prng_expand is
+// the vector (crypto.cpp:35-45). Explicit rows and seeds arrive compacted, in
+// request order; only they cross PCIe. Both are placed into one row-major
+// window buffer on device (row scatter + row-mapped K2), then scanned as one batch.
+int xpir_answer_batch_mixed(xpir_store* st, uint32_t B, const uint8_t* is_seed, const uint8_t* seeds,
+                            const uint8_t* q, uint64_t q_stride, uint32_t q_bits, const uint8_t* mask_seeds,
+                            uint8_t* out) {
+    if (!st) return fail(XPIR_EINVAL, "answer_batch_mixed: null store");
+    if (q_bits != st->N) return fail(XPIR_EINVAL, "answer_batch_mixed: query length mismatch");
+    if (B == 0) return XPIR_OK;
+    if (!is_seed || !out) return fail(XPIR_EINVAL, "answer_batch_mixed: null buffer");
+    std::vector<uint32_t> idx(B);
+    uint32_t ns = 0, ne = 0;
+    for (uint32_t r = 0; r < B; ++r) (is_seed[r] ? ns : ne) += 1;
+    for (uint32_t r = 0, a = 0, b = 0; r < B; ++r) idx[is_seed[r] ? ne + a++ : b++] = r;  // [explicit | seeded]
+    if (ns && !seeds) return fail(XPIR_EINVAL, "answer_batch_mixed: seeded requests without seeds");
+    if (ne && (!q || q_stride < (uint64_t(st->N) + 7) / 8))
+        return fail(XPIR_EINVAL, "answer_batch_mixed: explicit rows missing or stride too short");
+    std::lock_guard<std::mutex> lk(st->mu);
+    DeviceGuard g(st->device);
+    cudaStream_t s = st->stream;
+    const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
+    const uint64_t ws = round16(nbw) + 16;
+    XCK(st->q.ensure(ws * B));
+    XCK(st->idx.ensure(4 * uint64_t(B)));
+    XCK(cudaMemcpyAsync(st->idx.p, idx.data(), 4 * uint64_t(B), cudaMemcpyHostToDevice, s));
+    const uint32_t* d_idx = st->idx.as<uint32_t>();
+    if (ne) {  // explicit rows: H2D of the shard window of each, then into their request rows
+        XCK(st->qx.ensure(ws * ne));
+        XCK(cudaMemcpy2DAsync(st->qx.p, ws, q + blo, q_stride, nbw, ne, cudaMemcpyHostToDevice, s));
+        XCK(launch_scatter_rows(st->qx.as<uint8_t>(), ws, ne, d_idx, st->q.as<uint8_t>(), ws, nbw, s));
+        count_launches(1);
+    }
+    if (ns) {  // seeded rows: K2 straight into their request rows (this shard's window only)
+        XCK(st->seeds.ensure(uint64_t(ns) * 32));
+        XCK(cudaMemcpyAsync(st->seeds.p, seeds, uint64_t(ns) * 32, cudaMemcpyHostToDevice, s));
+        XCK(launch_expand(st->seeds.as<uint8_t>(), ns, blo, nbw, st->q.as<uint8_t>(), ws, s, d_idx + ne));
+        count_launches(1);
+    }
     const uint8_t* dm = nullptr;
     if (mask_seeds) {
         XCK(st->masks.ensure(uint64_t(B) * 32));

@@ -120,8 +120,10 @@ __global__ void k_init_out(uint8_t* __restrict__ out, uint32_t B, uint32_t S,
 // K2: query expansion. d_q[r*stride + k] = prng_expand(seed_r)[byte_lo + k].
 // One thread per 64-byte ChaCha20 block of the window.
 // ---------------------------------------------------------------------------
+// rows == nullptr: seed r expands into row r; else into row rows[r] (mixed batches)
 __global__ void k_expand(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t byte_lo,
-                         uint64_t nbytes, uint8_t* __restrict__ qout, uint64_t stride) {
+                         uint64_t nbytes, uint8_t* __restrict__ qout, uint64_t stride,
+                         const uint32_t* __restrict__ rows) {
     const uint64_t blk_lo = byte_lo / 64, blk_hi = (byte_lo + nbytes + 63) / 64;
     const uint64_t nblk = blk_hi - blk_lo;
     const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -132,7 +134,7 @@ __global__ void k_expand(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t
     uint32_t ks[16];
     chacha20_block(key, blk, ks);
     const uint64_t b0 = blk * 64;
-    uint8_t* o = qout + uint64_t(r) * stride;
+    uint8_t* o = qout + uint64_t(rows ? rows[r] : r) * stride;
     if (b0 >= byte_lo && b0 + 64 <= byte_lo + nbytes && ((b0 - byte_lo) % 16) == 0 &&
         (stride % 16) == 0) {
         uint4* o4 = reinterpret_cast<uint4*>(o + (b0 - byte_lo));
@@ -275,11 +277,39 @@ cudaError_t launch_init_out(uint8_t* out, uint32_t B, uint32_t S, const uint8_t*
 }
 
 cudaError_t launch_expand(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
-                          uint8_t* qout, uint64_t stride, cudaStream_t s) {
+                          uint8_t* qout, uint64_t stride, cudaStream_t s, const uint32_t* rows) {
     const uint64_t nblk = (byte_lo + nbytes + 63) / 64 - byte_lo / 64;
     const uint64_t n = uint64_t(B) * nblk;
     if (n == 0) return cudaSuccess;
-    k_expand<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qout, stride);
+    k_expand<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qout, stride, rows);
+    return cudaGetLastError();
+}
+
+// row k of src (stride ss) -> row idx[k] of dst (stride ds), nbytes each; one warp per row
+__global__ void k_scatter_rows(const uint8_t* __restrict__ src, uint64_t ss, uint32_t n,
+                               const uint32_t* __restrict__ idx, uint8_t* __restrict__ dst, uint64_t ds,
+                               uint64_t nbytes) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n; k += nw) {
+        const uint8_t* a = src + uint64_t(k) * ss;
+        uint8_t* b = dst + uint64_t(idx[k]) * ds;
+        if ((ss % 16) == 0 && (ds % 16) == 0) {
+            for (uint64_t j = uint64_t(lane) * 16; j + 16 <= nbytes; j += 32 * 16)
+                *reinterpret_cast<uint4*>(b + j) = *reinterpret_cast<const uint4*>(a + j);
+            for (uint64_t j = nbytes / 16 * 16 + lane; j < nbytes; j += 32) b[j] = a[j];
+        } else {
+            for (uint64_t j = lane; j < nbytes; j += 32) b[j] = a[j];
+        }
+    }
+}
+
+cudaError_t launch_scatter_rows(const uint8_t* src, uint64_t ss, uint32_t n, const uint32_t* idx, uint8_t* dst,
+                                uint64_t ds, uint64_t nbytes, cudaStream_t s) {
+    if (!n || !nbytes) return cudaSuccess;
+    uint32_t g = (n + 7) / 8;
+    if (g > 148 * 16) g = 148 * 16;
+    k_scatter_rows<<<g, 256, 0, s>>>(src, ss, n, idx, dst, ds, nbytes);
     return cudaGetLastError();
 }
 

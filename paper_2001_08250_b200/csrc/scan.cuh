@@ -68,7 +68,9 @@ cudaError_t launch_scan_nib(const ScanArgs& a, int num_sms);  // nib.cu, S % 128
 cudaError_t launch_init_out(uint8_t* out, uint32_t B, uint32_t S, const uint8_t* mask_seeds,
                             bool xor_into, cudaStream_t s);
 cudaError_t launch_expand(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
-                          uint8_t* qout, uint64_t stride, cudaStream_t s);
+                          uint8_t* qout, uint64_t stride, cudaStream_t s, const uint32_t* rows = nullptr);
+cudaError_t launch_scatter_rows(const uint8_t* src, uint64_t ss, uint32_t n, const uint32_t* idx, uint8_t* dst,
+                                uint64_t ds, uint64_t nbytes, cudaStream_t s);
 cudaError_t launch_xor_reduce(uint8_t* dst, const uint8_t* const* d_srcs, uint32_t nsrc,
                               uint64_t bytes, int num_sms, cudaStream_t s);
 cudaError_t run_peak_kernels(int num_sms, double* lop3_per_s, double* smem_bps, cudaStream_t s);
