@@ -932,6 +932,7 @@ static void table_free_all(xpir_table* t) {
     cudaFree(t->d.touched_mark);
     cudaFree(t->d.touched);
     cudaFree(t->d.mod_batch);
+    cudaFree(t->d.chain_pre);
     cudaFree(t->d.fifo);
     cudaFree(t->d.draws);
     cudaFree(t->dstate);
@@ -985,6 +986,7 @@ int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t cap
     M(reinterpret_cast<void**>(&t->d.touched_mark), 4 * slots);
     M(reinterpret_cast<void**>(&t->d.touched), 4 * slots);
     M(reinterpret_cast<void**>(&t->d.mod_batch), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.chain_pre), 8 * 3 * 512);
     M(reinterpret_cast<void**>(&t->d.fifo), 8 * fc);
     M(reinterpret_cast<void**>(&t->d.draws), 8 * uint64_t(DRAW_CAP));
     M(reinterpret_cast<void**>(&t->dstate), sizeof(CuckooState));

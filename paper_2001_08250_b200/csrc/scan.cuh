@@ -121,6 +121,7 @@ struct CuckooDev {
     uint32_t draw_cap;
     uint8_t* gather;      // [slots*item] staging for moved pre-existing payloads
     uint32_t* mod_batch;  // [slots] last round (batch id) that rewrote the slot's payload
+    uint64_t* chain_pre;  // [3 * 512] pre-chain contents of an eviction chain (walk_x)
 };
 cudaError_t launch_seal_incremental(const CuckooDev& d, uint32_t since, const uint8_t* table, uint8_t* img,
                                     int num_sms, cudaStream_t s);
@@ -140,7 +141,11 @@ struct CuckooState {
 cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32_t* beta1,
                                const uint32_t* beta2, uint64_t i0, uint64_t n, uint32_t* reports,
                                cudaStream_t s);
-// warp-cooperative walk (walk.cu); used by launch_cuckoo_walk when supported
+// warp-cooperative walks: on-chip eviction control (walk_x.cu), or global
+// victim metadata (walk.cu); launch_cuckoo_walk picks the first supported
+bool walk_x_supported(const CuckooDev& d);
+cudaError_t launch_cuckoo_walk_x(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
+                                 uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s);
 bool walk_w_supported(const CuckooDev& d);
 cudaError_t launch_cuckoo_walk_w(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
                                  uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s);

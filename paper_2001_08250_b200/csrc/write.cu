@@ -515,11 +515,15 @@ cudaError_t launch_absorb(const uint32_t* pos, uint64_t n, uint32_t m_bits,
 cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32_t* beta1,
                                const uint32_t* beta2, uint64_t i0, uint64_t n, uint32_t* reports,
                                cudaStream_t s) {
-    static const bool legacy = [] {
-        const char* e = std::getenv("XPIR_CUCKOO_WALK");  // "1": the single-thread walk (A/B runs)
-        return e && e[0] == '1';
+    // XPIR_CUCKOO_WALK (A/B runs): "1" single-thread walk, "2" warp walk with global
+    // victim metadata, unset/other: on-chip eviction control when the table fits
+    static const int choice = [] {
+        const char* e = std::getenv("XPIR_CUCKOO_WALK");
+        return e ? e[0] - '0' : 0;
     }();
-    if (!legacy && walk_w_supported(d)) return launch_cuckoo_walk_w(d, st, beta1, beta2, i0, n, reports, s);
+    if (choice != 1 && choice != 2 && walk_x_supported(d))
+        return launch_cuckoo_walk_x(d, st, beta1, beta2, i0, n, reports, s);
+    if (choice != 1 && walk_w_supported(d)) return launch_cuckoo_walk_w(d, st, beta1, beta2, i0, n, reports, s);
     const uint64_t slots = uint64_t(d.buckets) * d.depth;
     const bool use_smem = slots <= WALK_SMEM_MAX_SLOTS;
     const size_t words = use_smem ? (slots + 31) / 32 : 0;
