@@ -359,10 +359,15 @@ class Store:
         """pir::answer (pir.cpp:29-39)."""
         return self.answer_batch(_u8(query).reshape(1, -1), q_bits)[0]
 
-    def answer_batch_seeded(self, seeds: np.ndarray, mask_seeds: np.ndarray | None = None) -> np.ndarray:
+    def answer_batch_seeded(self, seeds: np.ndarray, mask_seeds: np.ndarray | None = None,
+                            out: np.ndarray | None = None) -> np.ndarray:
+        """`out` (B x S uint8, e.g. a view of pinned host memory) is filled in place."""
         s = _u8(seeds).reshape(-1, 32)
         B = s.shape[0]
-        out = np.empty((B, self.S), np.uint8)
+        if out is None:
+            out = np.empty((B, self.S), np.uint8)
+        elif out.dtype != np.uint8 or out.shape != (B, self.S) or not out.flags.c_contiguous:
+            raise InvalidArgument(XPIR_EINVAL, "answer_batch_seeded: out must be a contiguous B x S uint8 array")
         ms = None if mask_seeds is None else _u8(mask_seeds).reshape(B, 32)
         _check(lib().xpir_answer_batch_seeded(self.h, _p(s), B, None if ms is None else _p(ms), _p(out)))
         return out
