@@ -4,20 +4,26 @@
 // coalesced into one device batch ("Read requests are batched and forwarded to
 // the GPU").
 //
-// Host-side only; it calls the public scan entry point xpir_answer_batch.
-// Two pinned staging batches alternate: while one is being scanned on the GPU,
-// callers join the other. A caller copies its own query (and mask seed) into
-// the forming batch's pinned rows and, when the batch is done, copies its own
-// answer out, so packing and unpacking run on the callers' threads in parallel;
-// the worker thread only seals a batch (full, or max_wait_us after its first
-// request) and runs the scan. Requests with and without a mask seed go to
-// separate batches (pir::answer vs pir::mask_answer(pir::answer(..)), pir.cpp:29-39, 65-69).
+// Host-side only; it calls the public device-pointer scan entry point
+// xpir_answer_batch_dev. Three pinned staging batches rotate through
+//   Idle -> Forming (callers join) -> Sealed (callers finish packing)
+//        -> InFlight (H2D, scan, D2H queued on the batch's own stream)
+//        -> Done (answers in pinned memory) -> Idle (last caller unpacked).
+// The worker thread only seals batches (full, or max_wait_us after their first
+// request) and queues them without waiting for the GPU; a completer thread waits
+// on each batch's event in order and publishes it. So one batch can be scanned
+// while the next one's transfers run and a third one forms. Callers copy their
+// own query (and mask seed) in and their own answer out, in parallel on their
+// threads; completion is a futex wait on the batch generation. Requests with and
+// without a mask seed go to separate batches (pir::answer vs
+// pir::mask_answer(pir::answer(..)), pir.cpp:29-39, 65-69).
 #include <cuda_runtime.h>
 
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -30,42 +36,56 @@ int set_error(int code, const std::string& msg);  // capi.cu: the thread's xpir_
 
 namespace {
 
-enum class BState { Idle, Forming, Sealed, Running, Done };
+enum class BState { Idle, Forming, Sealed, InFlight, Done };
+constexpr int NBUF = 3;
 
 struct BBuf {
-    uint8_t* rows = nullptr;
-    uint8_t* seeds = nullptr;
-    uint8_t* out = nullptr;
+    uint8_t* rows = nullptr;   // pinned
+    uint8_t* seeds = nullptr;  // pinned
+    uint8_t* out = nullptr;    // pinned
+    uint8_t *d_rows = nullptr, *d_seeds = nullptr, *d_out = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done_ev = nullptr;
     BState state = BState::Idle;
     bool masked = false;
     uint32_t count = 0, filled = 0;
     uint64_t gen = 0;
-    // completion without the mutex: the worker publishes rc/err, then stores the
-    // batch generation (release) and notifies; callers wait on it (futex) and
-    // count themselves out with `readers`
-    std::atomic<uint64_t> done_gen{0};
-    std::atomic<uint32_t> readers{0};
     std::chrono::steady_clock::time_point first;
     int rc = 0;
     std::string err;
+    std::atomic<uint64_t> done_gen{0};
+    std::atomic<uint32_t> readers{0};
 };
 
 }  // namespace
 
 struct xpir_batcher {
     xpir_store* st = nullptr;
+    int device = 0;
     uint32_t N = 0, S = 0, nb = 0, max_batch = 0, max_wait_us = 0;
     std::mutex mu;
-    // Separate wake-up channels so a state change wakes only the threads that wait
-    // for it (hundreds of callers may be blocked at once):
-    std::condition_variable cv_work;     // worker: a batch started / filled / packed
-    std::condition_variable cv_free;     // callers: a staging batch became idle
-    BBuf buf[2];
-    bool stop = false;
-    std::thread worker;
+    std::condition_variable cv_work;  // worker: a batch started / filled / packed, a slot freed
+    std::condition_variable cv_done;  // completer: a batch went in flight
+    std::condition_variable cv_free;  // callers: a staging batch became idle
+    BBuf buf[NBUF];
+    std::deque<BBuf*> inflight;  // in submission order
+    bool stop = false, completer_stop = false;
+    std::thread worker, completer;
     uint64_t n_requests = 0, n_batches = 0, max_seen = 0;
 
+    void publish(BBuf* b, int rc, const std::string& err) {  // under mu
+        b->rc = rc;
+        b->err = err;
+        b->readers.store(b->count, std::memory_order_relaxed);
+        b->state = BState::Done;
+        n_batches += 1;
+        if (b->count > max_seen) max_seen = b->count;
+        b->done_gen.store(b->gen, std::memory_order_release);
+        b->done_gen.notify_all();
+    }
+
     void run() {
+        cudaSetDevice(device);
         std::unique_lock<std::mutex> lk(mu);
         for (;;) {
             BBuf* b = nullptr;
@@ -74,34 +94,83 @@ struct xpir_batcher {
                     if (x.state == BState::Forming) return true;
                 return stop;
             });
-            for (auto& x : buf)  // the older forming batch first
+            for (auto& x : buf)  // the oldest forming batch first
                 if (x.state == BState::Forming && (!b || x.gen < b->gen)) b = &x;
-            if (!b) return;  // stop, nothing pending
+            if (!b) break;  // stop, nothing pending
             const auto deadline = b->first + std::chrono::microseconds(max_wait_us);
             cv_work.wait_until(lk, deadline, [&] { return stop || b->count >= max_batch; });
             b->state = BState::Sealed;  // no more joins
             cv_work.wait(lk, [&] { return b->filled == b->count; });
-            b->state = BState::Running;
+            b->state = BState::InFlight;
             const uint32_t B = b->count;
             const bool masked = b->masked;
             lk.unlock();
-            const int rc = xpir_answer_batch(st, b->rows, nb, N, B, masked ? b->seeds : nullptr, b->out);
-            const std::string err = rc ? std::string(xpir_last_error()) : std::string();
+            // queue H2D, scan, D2H on the batch's stream; do not wait
+            int rc = XPIR_OK;
+            std::string err;
+            cudaError_t e = cudaMemcpyAsync(b->d_rows, b->rows, size_t(B) * nb, cudaMemcpyHostToDevice, b->stream);
+            if (e == cudaSuccess && masked)
+                e = cudaMemcpyAsync(b->d_seeds, b->seeds, size_t(B) * 32, cudaMemcpyHostToDevice, b->stream);
+            if (e != cudaSuccess) {
+                rc = XPIR_ECUDA;
+                err = std::string("batcher H2D: ") + cudaGetErrorString(e);
+            }
+            if (!rc) {
+                rc = xpir_answer_batch_dev(st, b->d_rows, nb, N, B, masked ? b->d_seeds : nullptr, b->d_out, b->stream);
+                if (rc) err = xpir_last_error();
+            }
+            if (!rc) {
+                e = cudaMemcpyAsync(b->out, b->d_out, size_t(B) * S, cudaMemcpyDeviceToHost, b->stream);
+                if (e == cudaSuccess) e = cudaEventRecord(b->done_ev, b->stream);
+                if (e != cudaSuccess) {
+                    rc = XPIR_ECUDA;
+                    err = std::string("batcher D2H: ") + cudaGetErrorString(e);
+                }
+            }
             lk.lock();
-            b->rc = rc;
-            b->err = err;
-            b->readers.store(B, std::memory_order_relaxed);
-            b->state = BState::Done;
-            n_batches += 1;
-            if (B > max_seen) max_seen = B;
-            b->done_gen.store(b->gen, std::memory_order_release);
-            b->done_gen.notify_all();
+            if (rc) {
+                // earlier in-flight batches complete first; this one fails now
+                publish(b, rc, err);
+            } else {
+                inflight.push_back(b);
+                cv_done.notify_one();
+            }
+        }
+        // drain: the completer publishes what is still in flight, then exits
+        completer_stop = true;
+        cv_done.notify_one();
+    }
+
+    void complete() {
+        cudaSetDevice(device);
+        std::unique_lock<std::mutex> lk(mu);
+        for (;;) {
+            cv_done.wait(lk, [&] { return !inflight.empty() || completer_stop; });
+            if (inflight.empty()) break;
+            BBuf* b = inflight.front();
+            lk.unlock();
+            const cudaError_t e = cudaEventSynchronize(b->done_ev);
+            lk.lock();
+            inflight.pop_front();
+            publish(b, e == cudaSuccess ? XPIR_OK : XPIR_ECUDA,
+                    e == cudaSuccess ? std::string() : std::string("batcher: ") + cudaGetErrorString(e));
         }
     }
 };
 
 namespace {
 int bfail(int code, const std::string& m) { return xpir::set_error(code, m); }
+
+void free_bufs(xpir_batcher* b) {
+    for (auto& x : b->buf) {
+        for (uint8_t* p : {x.rows, x.seeds, x.out})
+            if (p) cudaFreeHost(p);
+        for (uint8_t* p : {x.d_rows, x.d_seeds, x.d_out})
+            if (p) cudaFree(p);
+        if (x.done_ev) cudaEventDestroy(x.done_ev);
+        if (x.stream) cudaStreamDestroy(x.stream);
+    }
+}
 }  // namespace
 
 extern "C" {
@@ -111,29 +180,52 @@ int xpir_batcher_create(xpir_store* st, uint32_t max_batch, uint32_t max_wait_us
     if (max_batch == 0) return bfail(XPIR_EINVAL, "batcher_create: max_batch must be positive");
     uint32_t N, S, lo, hi;
     uint64_t epoch;
-    int rc = xpir_store_info(st, &N, &S, &lo, &hi, &epoch, nullptr);
+    void* data = nullptr;
+    int rc = xpir_store_info(st, &N, &S, &lo, &hi, &epoch, &data);
     if (rc) return rc;
+    int dev = 0;
+    cudaPointerAttributes pa{};
+    if (data && cudaPointerGetAttributes(&pa, data) == cudaSuccess) dev = pa.device;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
     auto* b = new xpir_batcher;
     b->st = st;
+    b->device = dev;
     b->N = N;
     b->S = S;
     b->nb = (N + 7) / 8;
     b->max_batch = max_batch;
     b->max_wait_us = max_wait_us;
+    cudaError_t e = cudaSuccess;
     for (auto& x : b->buf) {
-        cudaError_t e = cudaHostAlloc(&x.rows, size_t(max_batch) * b->nb + 16, cudaHostAllocPortable);
-        if (e == cudaSuccess) e = cudaHostAlloc(&x.seeds, size_t(max_batch) * 32, cudaHostAllocPortable);
-        if (e == cudaSuccess) e = cudaHostAlloc(&x.out, size_t(max_batch) * S + 16, cudaHostAllocPortable);
-        if (e != cudaSuccess) {
-            for (auto& y : b->buf)
-                for (uint8_t* p : {y.rows, y.seeds, y.out})
-                    if (p) cudaFreeHost(p);
-            delete b;
-            return bfail(e == cudaErrorMemoryAllocation ? XPIR_ENOMEM : XPIR_ECUDA,
-                         std::string("batcher_create: ") + cudaGetErrorString(e));
-        }
+        auto H = [&](uint8_t** p, size_t n) {
+            if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void**>(p), n, cudaHostAllocPortable);
+        };
+        auto D = [&](uint8_t** p, size_t n) {
+            if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(p), n);
+        };
+        H(&x.rows, size_t(max_batch) * b->nb + 16);
+        H(&x.seeds, size_t(max_batch) * 32);
+        H(&x.out, size_t(max_batch) * S + 16);
+        D(&x.d_rows, size_t(max_batch) * b->nb + 16);
+        D(&x.d_seeds, size_t(max_batch) * 32);
+        D(&x.d_out, size_t(max_batch) * S + 16);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&x.stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x.done_ev, cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+        free_bufs(b);
+        delete b;
+        return bfail(e == cudaErrorMemoryAllocation ? XPIR_ENOMEM : XPIR_ECUDA,
+                     std::string("batcher_create: ") + cudaGetErrorString(e));
     }
     b->worker = std::thread([b] { b->run(); });
+    b->completer = std::thread([b] { b->complete(); });
     *out = b;
     return XPIR_OK;
 }
@@ -147,9 +239,8 @@ int xpir_batcher_destroy(xpir_batcher* b) {
     b->cv_work.notify_all();
     b->cv_free.notify_all();
     b->worker.join();
-    for (auto& x : b->buf)
-        for (uint8_t* p : {x.rows, x.seeds, x.out})
-            if (p) cudaFreeHost(p);
+    b->completer.join();
+    free_bufs(b);
     delete b;
     return XPIR_OK;
 }
@@ -203,6 +294,7 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
         buf->state = BState::Idle;
         lk.unlock();
         b->cv_free.notify_all();
+        b->cv_work.notify_one();
     }
     if (rc) return bfail(rc, err);
     return XPIR_OK;

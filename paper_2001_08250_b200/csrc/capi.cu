@@ -160,6 +160,18 @@ struct xpir_store {
     cudaStream_t stream = nullptr;
     DevBuf q, out, seeds, masks, qwin, qx, idx;
     std::mutex mu;
+    // Query-window scratch of the device-pointer entry points, one per caller
+    // stream, so calls on different streams may run concurrently (read batcher).
+    std::mutex scratch_mu;
+    std::vector<std::pair<cudaStream_t, DevBuf*>> qwin_by_stream;
+    DevBuf& qwin_for(cudaStream_t s) {
+        if (s == stream) return qwin;
+        std::lock_guard<std::mutex> lk(scratch_mu);
+        for (auto& e : qwin_by_stream)
+            if (e.first == s) return *e.second;
+        qwin_by_stream.emplace_back(s, new DevBuf);
+        return *qwin_by_stream.back().second;
+    }
     uint32_t nb() const { return hi - lo; }
     uint64_t bytes() const { return uint64_t(nb()) * S; }
     uint64_t byte_lo() const { return lo / 8; }
@@ -343,6 +355,10 @@ int xpir_store_destroy(xpir_store* st) {
     st->seeds.release();
     st->masks.release();
     st->qwin.release();
+    for (auto& e : st->qwin_by_stream) {
+        e.second->release();
+        delete e.second;
+    }
     st->qx.release();
     st->idx.release();
     cudaStreamDestroy(st->stream);
@@ -522,10 +538,11 @@ static int scan_rows(xpir_store* st, const uint8_t* rows, uint64_t stride, uint3
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
     if (k != 2 && k != 7 && k != 8) return run_rows(st, k, rows + blo, stride, B, d_out, s);
     const uint64_t qs = m4rm_qstride(B);
-    XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
-    XCK(launch_transpose_q(rows, stride, blo, nbw, B, st->qwin.as<uint8_t>(), qs, s));
+    DevBuf& qw = st->qwin_for(s);
+    XCK(qw.ensure(m4rm_qrows(nbw) * qs));
+    XCK(launch_transpose_q(rows, stride, blo, nbw, B, qw.as<uint8_t>(), qs, s));
     count_launches(1);
-    return run_m4(st, st->qwin.as<uint8_t>(), qs, B, d_out, s, k);
+    return run_m4(st, qw.as<uint8_t>(), qs, B, d_out, s, k);
 }
 
 extern "C" {
@@ -557,16 +574,18 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
     // straight into the layout the chosen scan kernel reads.
     if (k == 2 || k == 7 || k == 8) {
         const uint64_t qs = m4rm_qstride(B);
-        XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
-        XCK(launch_expand_T(d_seeds, B, blo, nbw, st->qwin.as<uint8_t>(), qs, s));
+        DevBuf& qw = st->qwin_for(s);
+        XCK(qw.ensure(m4rm_qrows(nbw) * qs));
+        XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s));
         count_launches(1);
-        return run_m4(st, st->qwin.as<uint8_t>(), qs, B, d_out, s, k);
+        return run_m4(st, qw.as<uint8_t>(), qs, B, d_out, s, k);
     }
     const uint64_t ws = xpir_query_window_bytes(st);
-    XCK(st->qwin.ensure(ws * B));
-    XCK(launch_expand(d_seeds, B, blo, nbw, st->qwin.as<uint8_t>(), ws, s));
+    DevBuf& qw = st->qwin_for(s);
+    XCK(qw.ensure(ws * B));
+    XCK(launch_expand(d_seeds, B, blo, nbw, qw.as<uint8_t>(), ws, s));
     count_launches(1);
-    return run_rows(st, k, st->qwin.as<uint8_t>(), ws, B, d_out, s);
+    return run_rows(st, k, qw.as<uint8_t>(), ws, B, d_out, s);
 }
 
 int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint32_t q_bits,
@@ -720,9 +739,10 @@ int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, ui
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
     const uint64_t qs = m4rm_qstride(B);
-    XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
-    XCK(launch_expand_T(d_seeds, B, blo, nbw, st->qwin.as<uint8_t>(), qs, s));
-    M4Args a{st->data, st->nb(), st->S, st->qwin.as<uint8_t>(), qs, B, out_ptrs[0], s};
+    DevBuf& qw = st->qwin_for(s);
+    XCK(qw.ensure(m4rm_qrows(nbw) * qs));
+    XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s));
+    M4Args a{st->data, st->nb(), st->S, qw.as<uint8_t>(), qs, B, out_ptrs[0], s};
     a.peers.n = n_ranks;
     for (uint32_t k = 0; k < n_ranks; ++k) {
         a.peers.ptr[k] = out_ptrs[k];
