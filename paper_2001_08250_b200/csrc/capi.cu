@@ -540,7 +540,7 @@ static int scan_rows(xpir_store* st, const uint8_t* rows, uint64_t stride, uint3
     const uint64_t qs = m4rm_qstride(B);
     DevBuf& qw = st->qwin_for(s);
     XCK(qw.ensure(m4rm_qrows(nbw) * qs));
-    XCK(launch_transpose_q(rows, stride, blo, nbw, B, qw.as<uint8_t>(), qs, s));
+    XCK(launch_transpose_q(rows, stride, blo, nbw, B, qw.as<uint8_t>(), qs, s, k == 8));
     count_launches(1);
     return run_m4(st, qw.as<uint8_t>(), qs, B, d_out, s, k);
 }
@@ -576,7 +576,7 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
         const uint64_t qs = m4rm_qstride(B);
         DevBuf& qw = st->qwin_for(s);
         XCK(qw.ensure(m4rm_qrows(nbw) * qs));
-        XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s));
+        XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s, k == 8));
         count_launches(1);
         return run_m4(st, qw.as<uint8_t>(), qs, B, d_out, s, k);
     }
@@ -620,7 +620,7 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
     if (k == 2 || k == 7 || k == 8) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
-        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s));
+        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s, k == 8));
         count_launches(1);
         rc = run_m4(st, st->qwin.as<uint8_t>(), qs, B, dout, s, k);
     } else {
@@ -688,7 +688,7 @@ int xpir_answer_batch_mixed(xpir_store* st, uint32_t B, const uint8_t* is_seed, 
     if (k == 2 || k == 7 || k == 8) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
-        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s));
+        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s, k == 8));
         count_launches(1);
         rc = run_m4(st, st->qwin.as<uint8_t>(), qs, B, dout, s, k);
     } else {
@@ -741,7 +741,7 @@ int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, ui
     const uint64_t qs = m4rm_qstride(B);
     DevBuf& qw = st->qwin_for(s);
     XCK(qw.ensure(m4rm_qrows(nbw) * qs));
-    XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s));
+    XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s, true));  // the fused path always runs kernel 8
     M4Args a{st->data, st->nb(), st->S, qw.as<uint8_t>(), qs, B, out_ptrs[0], s};
     a.peers.n = n_ranks;
     for (uint32_t k = 0; k < n_ranks; ++k) {

@@ -234,9 +234,16 @@ k_scan_m4rm(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8
 //   so each of the 64 byte stores per thread is a coalesced 32-byte warp store.
 // k_transpose_q: rows q[r*q_stride + byte_lo + k] -> qT (32x32 smem tiles).
 // ---------------------------------------------------------------------------
+// set4: the set-interleaved layout of k_scan_m4rm_q instead — byte k of request r
+// at (k >> 2) * 4 * qstride + 4 r + (k & 3), i.e. the four query bytes of a set
+// of four groups are one 32-bit word per request.
+__device__ __forceinline__ uint64_t qidx(uint64_t k, uint32_t r, uint64_t qstride, bool set4) {
+    return set4 ? (k >> 2) * 4 * qstride + uint64_t(r) * 4 + (k & 3) : k * qstride + r;
+}
+
 __global__ void __launch_bounds__(128)
 k_expand_T(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
-           uint8_t* __restrict__ qT, uint64_t qstride) {
+           uint8_t* __restrict__ qT, uint64_t qstride, bool set4) {
     const uint64_t blk_lo = byte_lo / 64;
     const uint64_t nblk = (byte_lo + nbytes + 63) / 64 - blk_lo;
     const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -250,15 +257,22 @@ k_expand_T(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t byte_lo, uint
     uint32_t ks[16];
     chacha20_block(key, blk, ks);
     const int64_t base = int64_t(blk * 64) - int64_t(byte_lo);
+    if (set4 && (base & 3) == 0 && base >= 0 && uint64_t(base) + 64 <= nbytes) {
+        // 16 whole sets: one coalesced 32-bit store each
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            *reinterpret_cast<uint32_t*>(qT + qidx(uint64_t(base) + 4 * j, r, qstride, true)) = ks[j];
+        return;
+    }
 #pragma unroll
     for (int j = 0; j < 64; ++j) {
         const int64_t k = base + j;
-        if (k >= 0 && uint64_t(k) < nbytes) qT[uint64_t(k) * qstride + r] = uint8_t(ks[j >> 2] >> (8 * (j & 3)));
+        if (k >= 0 && uint64_t(k) < nbytes) qT[qidx(uint64_t(k), r, qstride, set4)] = uint8_t(ks[j >> 2] >> (8 * (j & 3)));
     }
 }
 
 __global__ void k_transpose_q(const uint8_t* __restrict__ q, uint64_t q_stride, uint64_t byte_lo,
-                              uint64_t nbytes, uint32_t B, uint8_t* __restrict__ qT, uint64_t qstride) {
+                              uint64_t nbytes, uint32_t B, uint8_t* __restrict__ qT, uint64_t qstride, bool set4) {
     __shared__ uint8_t tile[32][33];
     const uint64_t k0 = uint64_t(blockIdx.x) * 32;  // byte (group) tile
     const uint32_t r0 = blockIdx.y * 32;            // request tile
@@ -271,7 +285,7 @@ __global__ void k_transpose_q(const uint8_t* __restrict__ q, uint64_t q_stride, 
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {
         const uint64_t k = k0 + y;
         const uint32_t r = r0 + threadIdx.x;
-        if (k < nbytes && r < B) qT[k * qstride + r] = tile[threadIdx.x][y];
+        if (k < nbytes && r < B) qT[qidx(k, r, qstride, set4)] = tile[threadIdx.x][y];
     }
 }
 
@@ -307,19 +321,19 @@ uint64_t m4rm_qstride(uint32_t B) { return (uint64_t(B) + 15) & ~uint64_t(15); }
 uint64_t m4rm_qrows(uint64_t n_groups) { return (n_groups + 15) & ~uint64_t(15); }
 
 cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
-                            uint8_t* qT, uint64_t qstride, cudaStream_t s) {
+                            uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4) {
     const uint64_t nblk = (byte_lo + nbytes + 63) / 64 - byte_lo / 64;
     const uint64_t n = uint64_t((B + 31) & ~31u) * nblk;
     if (n == 0) return cudaSuccess;
-    k_expand_T<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qT, qstride);
+    k_expand_T<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qT, qstride, set4);
     return cudaGetLastError();
 }
 
 cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
-                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s) {
+                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4) {
     if (!B || !nbytes) return cudaSuccess;
     dim3 grid(uint32_t((nbytes + 31) / 32), (B + 31) / 32);
-    k_transpose_q<<<grid, dim3(32, 8), 0, s>>>(q, q_stride, byte_lo, nbytes, B, qT, qstride);
+    k_transpose_q<<<grid, dim3(32, 8), 0, s>>>(q, q_stride, byte_lo, nbytes, B, qT, qstride, set4);
     return cudaGetLastError();
 }
 

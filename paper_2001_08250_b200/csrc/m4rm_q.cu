@@ -21,13 +21,16 @@
 //    so TMEM traffic is half the lookup bytes. Rc = 8192 requests per tile.
 //  * Shared-memory wavefronts per set (per SM, Rc = 8192): 8192 lookups,
 //    384 table build (4 tables x 256 rows x 32 B + bucket reads), 256 query
-//    index loads, 264 staging fills: lookups are 90% of the pipe (the 128-byte
+//    index loads, 8 bucket fills: lookups are 93% of the pipe (the 128-byte
 //    column kernel: 82%), because the table build is amortised over 4x more
 //    requests and each index byte now serves 32 bytes of lookup instead of 16.
 //    Measured (ncu, 1 GiB, B = 8192): LSU data pipe 95% busy, 0 load bank
 //    conflicts, lookups 89% of the shared wavefronts; 0.87 of the LDS.128 peak.
-//  * Query index bytes arrive by 1-D bulk async copy (TMA engine) on a
-//    per-stage mbarrier; bucket slices by cp.async (zero-fill past the shard).
+//  * Query index bytes come in a set-interleaved layout (one 32-bit word of the
+//    set's four group bytes per request, written so by k_expand_T /
+//    k_transpose_q) and are read straight from L2 into registers one set ahead
+//    (LDG.128 = 4 requests per lane), so they never pass through shared memory;
+//    bucket slices are staged by cp.async (zero-fill past the shard).
 //
 // TMEM map (one CTA per SM): warp w uses lanes 32*(w%4)..+31 and columns
 // 128*(w/4) + 8*s for its request slot s < 4*NQ.
@@ -51,11 +54,9 @@ constexpr int Q_NST = 4;          // staging ring depth (sets)
 template <int NQ>
 struct QCfg {
     static constexpr int RC = Q_NT * 4 * NQ;  // requests per tile
-    static constexpr int QB = 4 * RC;         // query index bytes per set
-    static constexpr int STG = QB + 1024;     // + 32 buckets x 32 B
+    static constexpr int STG = 1024;          // 32 buckets x 32 B per staged set
     static constexpr int OFF_STG = 2 * Q_TAB;
-    static constexpr int OFF_MBAR = OFF_STG + Q_NST * STG;  // one mbarrier per stage
-    static constexpr int OFF_ADDR = OFF_MBAR + 8 * Q_NST;
+    static constexpr int OFF_ADDR = OFF_STG + Q_NST * STG;
     static constexpr int SMEM = OFF_ADDR + 16;
     static constexpr int TCOLS = 128 * NQ;  // TMEM columns (power of two >= 32)
     static_assert(SMEM <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
@@ -81,6 +82,14 @@ __device__ __forceinline__ void tm_wait_ld8(uint32_t (&v)[8]) {
                  : "memory");
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+// query words: read once per CTA, reused through L2 by the other column tiles
+__device__ __forceinline__ uint4 ldg_q(const uint8_t* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
 
 }  // namespace
 
@@ -105,21 +114,17 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
-    if (tid == 0) {
-        for (int b = 0; b < Q_NST; ++b) mbar_init(sbase + C::OFF_MBAR + 8 * b, 1);
-        mbar_init_fence();
-    }
-    __syncthreads();
     const uint32_t tbase = *reinterpret_cast<const uint32_t*>(smem + C::OFF_ADDR);
     const uint32_t tcol = tbase + (uint32_t((warp & 3) * 32) << 16) + uint32_t(warp >> 2) * (32 * NQ);
 
-    // lookup constants: step kk reads table (lp + kk) & 3, own half first
-    uint32_t toff[4], qrow[4];
+    // lookup constants: step kk reads table (lp + kk) & 3, own half first; its index
+    // is byte t of the request's set word (PRMT selector 0x4440 | t)
+    uint32_t toff[4], bsel[4];
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
         const uint32_t t = uint32_t(lp + kk) & 3u;
         toff[kk] = 32 * t + 16 * uint32_t(i8 & 1);
-        qrow[kk] = t * C::RC;
+        bsel[kk] = 0x4440u | t;
     }
     const uint32_t dhalf = (i8 & 1) ? 0xfffffff0u : 16u;  // address of the other half: +16 / -16
     // build constants: lane -> (table bt, 32-bit word bw); warp -> high nibble of the row
@@ -130,7 +135,7 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
     const uint32_t n_rtiles = (B + C::RC - 1) / C::RC;
     const uint64_t units = uint64_t(n_ctiles) * n_rtiles * n_seg;
     // Staging sequence number of a set over the CTA's lifetime: stage buffer
-    // seq % Q_NST, mbarrier phase parity (seq / Q_NST) & 1, table buffer seq & 1.
+    // seq % Q_NST, table buffer seq & 1.
     uint32_t seq0 = 0;
 
     for (uint64_t v = blockIdx.x; v < units; v += gridDim.x) {
@@ -150,30 +155,30 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
             tm_wait_st();
         }
 
-        // Query index bytes of a set (rows 4j..4j+3 of qT, requests [r_base, r_base + RC))
-        // arrive by bulk async copy on the stage's mbarrier; the 32 bucket slices of
-        // column tile c (laid out [i][t][32 B]) by cp.async with zero-fill past the shard.
-        const uint32_t qbytes = uint32_t(min(uint64_t(C::RC), qstride - r_base));
+        // The bucket slices of column tile c for set j (laid out [i][t][32 B]) are
+        // staged by cp.async with zero-fill past the shard. The query words of a set
+        // (set-interleaved layout: one 32-bit word of four group bytes per request)
+        // are read straight from L2 into registers, one set ahead.
         auto stage = [&](uint32_t j, uint32_t sq) {
             const int buf = int(sq % Q_NST);
             const uint32_t dst = sbase + C::OFF_STG + buf * C::STG;
-            if (tid == 0) {
-                const uint32_t mb = sbase + C::OFF_MBAR + 8 * buf;
-                mbar_expect_tx(mb, 4 * qbytes);
-#pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    bulk_g2s(dst + t * C::RC, qT + (uint64_t(j) * 4 + t) * qstride + r_base, qbytes, mb);
-            }
             if (tid < 64) {
                 const uint32_t i = tid >> 3, t = (tid >> 1) & 3, part = tid & 1;
                 const uint32_t bucket = (j * 4 + t) * 8 + i;
                 const bool ok = bucket < nb;
                 const uint8_t* src = db + (ok ? uint64_t(bucket) * S : 0) + uint64_t(c) * 32 + part * 16;
-                cp_async16(dst + C::QB + tid * 16, src, ok ? 16u : 0u);
+                cp_async16(dst + tid * 16, src, ok ? 16u : 0u);
+            }
+        };
+        auto load_q = [&](uint32_t j, uint4 (&w)[NQ]) {
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const uint32_t r4 = r_base + 4 * uint32_t(q * Q_NT + tid);
+                w[q] = r4 < qstride ? ldg_q(qT + uint64_t(j) * 4 * qstride + uint64_t(r4) * 4) : make_uint4(0, 0, 0, 0);
             }
         };
         auto build = [&](int buf, int tb) {
-            const uint32_t src = sbase + C::OFF_STG + buf * C::STG + C::QB + bt * 32 + bw * 4;
+            const uint32_t src = sbase + C::OFF_STG + buf * C::STG + bt * 32 + bw * 4;
             uint32_t b[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) b[i] = lds32(src + i * 128);
@@ -186,15 +191,11 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                 sts32(row0 + uint32_t(m ^ (m >> 1)) * 128, h);
             }
         };
-        auto lookups = [&](int buf, int tb) {
-            const uint32_t qb = sbase + C::OFF_STG + buf * C::STG;
+        auto lookups = [&](const uint4 (&wq)[NQ], int tb) {
             const uint32_t tab = sbase + tb * Q_TAB;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const uint32_t r0 = 4 * uint32_t(q * Q_NT + tid);
-                uint32_t W[4];
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) W[kk] = lds32(qb + qrow[kk] + r0);
+                const uint32_t wk[4] = {wq[q].x, wq[q].y, wq[q].z, wq[q].w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const uint32_t ta = tcol + 8 * (4 * q + k);
@@ -203,7 +204,7 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                     uint4 v0[4], v1[4];
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t a0 = tab + toff[kk] + ((W[kk] >> (8 * k)) & 0xffu) * 128;
+                        const uint32_t a0 = tab + toff[kk] + __byte_perm(wk[k], 0, bsel[kk]) * 128;
                         v0[kk] = lds128(a0);
                         v1[kk] = lds128(a0 + dhalf);
                     }
@@ -221,7 +222,9 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
             }
         };
 
-        // prologue: sets s0 .. s0+2 in flight, T(s0) built
+        // prologue: sets s0 .. s0+2 in flight, T(s0) built, query words of s0 loading
+        uint4 wn[NQ];
+        load_q(s0, wn);
 #pragma unroll
         for (int p = 0; p < Q_NST - 1; ++p) {
             if (s0 + p < s1) stage(s0 + p, seq0 + p);
@@ -234,11 +237,14 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
 #pragma unroll 1
         for (uint32_t j = s0; j < s1; ++j) {
             const uint32_t sq = seq0 + (j - s0);
+            uint4 wc[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) wc[q] = wn[q];
+            if (j + 1 < s1) load_q(j + 1, wn);
             if (j + Q_NST - 1 < s1) stage(j + Q_NST - 1, sq + Q_NST - 1);
             cp_async_commit();
             if (j + 1 < s1) build(int((sq + 1) % Q_NST), int((sq + 1) & 1));
-            mbar_wait(sbase + C::OFF_MBAR + 8 * (sq % Q_NST), (sq / Q_NST) & 1);
-            lookups(int(sq % Q_NST), int(sq & 1));
+            lookups(wc, int(sq & 1));
             tm_wait_st();
             cp_async_wait<Q_NST - 3>();
             __syncthreads();

@@ -58,10 +58,11 @@ double m4rm_q_cost(uint32_t B, int* tile);  // vs the half-TMEM kernel: ceil(B/2
 cudaError_t launch_scan_m4rm4(const M4Args& a, int num_sms);  // nibble tables (m4rm4.cu)
 uint64_t m4rm_qstride(uint32_t B);
 uint64_t m4rm_qrows(uint64_t n_groups);  // rows to allocate (staging reads 16-row chunks)
+// set4 = true: the set-interleaved layout of k_scan_m4rm_q (kernel 8)
 cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
-                            uint8_t* qT, uint64_t qstride, cudaStream_t s);
+                            uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4 = false);
 cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
-                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s);
+                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4 = false);
 cudaError_t launch_scan_direct(const ScanArgs& a, int num_sms, uint32_t* nsplit_out);
 cudaError_t launch_scan_bytes(const ScanArgs& a);
 cudaError_t launch_scan_nib(const ScanArgs& a, int num_sms);  // nib.cu, S % 128 == 0
