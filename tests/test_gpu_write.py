@@ -181,3 +181,48 @@ def test_parallel_prefix_matches_sequential(xp, port, cuda, nb, depth, cap, n, s
     b2 = g.integers(0, nb, n).astype(np.uint32)
     assert np.array_equal(T.insert_batch(b1, b2, pl), P.insert_batch(b1, b2, pl))
     _compare_tables(T, P)
+
+
+@pytest.mark.parametrize("nb,depth,cap_frac,load,same_frac,walk", [
+    (25000, 4, 1.0, 0.97, 0.02, "x"),   # 100,000 slots: alt index partly in TMEM
+    (33000, 3, 1.0, 0.95, 0.0, "x"),    # depth 3: uniform(depth) with rejection, TMEM part
+    (16384, 8, 0.9, 1.3, 0.01, "x"),    # 131,072 slots at capacity: FIFO GC on every insert past it
+    (20000, 4, 1.0, 0.96, 0.0, "w"),    # the warp walk with global victim metadata (A/B)
+])
+def test_walk_kernels_large_tables(xp, port, cuda, nb, depth, cap_frac, load, same_frac, walk):
+    """The warp-cooperative walks on tables whose alt index spills into TMEM
+    (k_cuckoo_walk_x) or that run the global-metadata walk (k_cuckoo_walk_w), at
+    high load with long eviction chains, beta1 == beta2 items, non-power-of-two
+    depth and GC: reports, table bytes, metadata and state digest equal the
+    oracle's sequential cuckoo::Table::insert (cuckoo.cpp:56-126)."""
+    import subprocess
+    import sys
+
+    code = f"""
+import numpy as np, sys
+sys.path.insert(0, {repr(str(__import__('os').path.dirname(__import__('os').path.dirname(__file__))))})
+import oracle, paper_2001_08250_b200 as xp
+nb, depth, cap_frac, load, same_frac = {nb}, {depth}, {cap_frac}, {load}, {same_frac}
+g = np.random.default_rng(nb + depth)
+slots = nb * depth
+cap = int(slots * cap_frac)
+n = int(slots * load)
+seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+b1 = g.integers(0, nb, n).astype(np.uint32)
+b2 = g.integers(0, nb, n).astype(np.uint32)
+same = g.random(n) < same_frac
+b2[same] = b1[same]
+pl = g.integers(0, 256, (n, 8), dtype=np.uint8)
+port = oracle.Port()
+T, P = xp.Table(nb, depth, cap, 8, seed), port.table(nb, depth, cap, 8, seed)
+half = n // 2
+for a, b in ((0, half), (half, n)):
+    assert np.array_equal(T.insert_batch(b1[a:b], b2[a:b], pl[a:b]), P.insert_batch(b1[a:b], b2[a:b], pl[a:b]))
+assert T.state_digest() == P.state_digest()
+assert np.array_equal(T.snapshot(), P.data())
+print("ok")
+"""
+    env = dict(__import__("os").environ)
+    env["XPIR_CUCKOO_WALK"] = "2" if walk == "w" else "0"
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
