@@ -241,10 +241,30 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* beta1, const uint32_t
 int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_beta1, const uint32_t* d_beta2,
                                 const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
                                 void* stream);
+/* Bucket-range payload shards (the payload scatter goes to the GPU
+ * owning each bucket range). A shard table keeps the whole metadata (the walk
+ * is replicated: every shard runs the same insert_walk) and the payloads of
+ * buckets [lo, hi) only. A round is: insert_walk on every shard; apply_gather on
+ * every shard (it reads the pre-round payloads that move into its range, from
+ * whichever shard holds them — map.data may be CUDA-IPC peer pointers); a
+ * barrier; apply_scatter on every shard (every shard gets all n payloads).
+ * xpir_table_insert_batch[_dev] = the three steps on an unsharded table. */
+typedef struct {
+    uint32_t n;              /* shards, 1..8 */
+    uint32_t bucket_lo[9];   /* shard g holds buckets [bucket_lo[g], bucket_lo[g+1]) */
+    const uint8_t* data[8];  /* shard g's payload array (xpir_table_device_data) */
+} xpir_shard_map;
+int xpir_table_create_shard(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
+                            const uint8_t seed[32], uint32_t lo, uint32_t hi, xpir_table** out);
+int xpir_table_shard(const xpir_table* t, uint32_t* lo, uint32_t* hi);
+int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_beta1, const uint32_t* d_beta2, uint64_t n,
+                               uint32_t* d_reports, void* stream);
+int xpir_table_apply_gather_dev(xpir_table* t, const xpir_shard_map* map, void* stream);
+int xpir_table_apply_scatter_dev(xpir_table* t, const uint8_t* d_payload, void* stream);
 /* Pre-size the per-round scratch (claim sort buffers, payload staging) for
  * batches of up to max_batch writes, so no allocation happens inside a round. */
 int xpir_table_reserve(xpir_table* t, uint64_t max_batch);
-/* Table::snapshot bytes (cuckoo.cpp:128-135). */
+/* Table::snapshot bytes (cuckoo.cpp:128-135); of a payload shard: its buckets only. */
 int xpir_table_snapshot(const xpir_table* t, uint8_t* host_out);
 /* Seal into a store covering the whole table or a bucket range of it (device copy). */
 int xpir_table_seal(const xpir_table* t, xpir_store* st, uint64_t epoch, void* stream);
@@ -252,7 +272,7 @@ int xpir_table_meta(const xpir_table* t, uint8_t* used, uint32_t* beta1, uint32_
                     uint64_t* stamp);
 int xpir_table_counters(const xpir_table* t, uint64_t* writes, uint64_t* live,
                         uint64_t* next_stamp);
-/* Table::state_digest (cuckoo.cpp:137-149). */
+/* Table::state_digest (cuckoo.cpp:137-149); whole tables only. */
 int xpir_table_state_digest(const xpir_table* t, uint8_t out[32]);
 /* Table::slot_used (cuckoo.cpp:160-163). */
 int xpir_table_slot_used(const xpir_table* t, uint32_t bucket, uint32_t slot);

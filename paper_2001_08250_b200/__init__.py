@@ -140,6 +140,12 @@ _SIGS = {
     "xpir_server_seal": ([_vp, _u64p], C.c_int),
     "xpir_server_snapshot": ([_vp, C.c_uint64, C.POINTER(_vp)], C.c_int),
     "xpir_server_info": ([_vp, _u64p, _u64p, _u64p, C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
+    "xpir_table_create_shard": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _u8p, C.c_uint32,
+                                 C.c_uint32, C.POINTER(_vp)], C.c_int),
+    "xpir_table_shard": ([_vp, _u32p, _u32p], C.c_int),
+    "xpir_table_insert_walk_dev": ([_vp, _vp, _vp, C.c_uint64, _vp, _vp], C.c_int),
+    "xpir_table_apply_gather_dev": ([_vp, _vp, _vp], C.c_int),
+    "xpir_table_apply_scatter_dev": ([_vp, _vp, _vp], C.c_int),
     "xpir_answer_batch_mixed": ([_vp, C.c_uint32, _u8p, _u8p, _u8p, C.c_uint64, C.c_uint32, _u8p, _u8p], C.c_int),
     "xpir_window_digest_n": ([_vp, C.c_uint64, _u8p], C.c_int),
     "xpir_window_encode_delta": ([_vp, C.c_uint64, _u8p, C.c_uint64, _u64p], C.c_int),
@@ -529,13 +535,32 @@ def blake2b(data: bytes, outlen: int = 32) -> bytes:
 # ---------------------------------------------------------------------------
 # cuckoo::Table
 # ---------------------------------------------------------------------------
+class _ShardMap(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("bucket_lo", C.c_uint32 * 9), ("data", _vp * 8)]
+
+
+def shard_map(tables: list["Table"]) -> _ShardMap:
+    """xpir_shard_map over payload shards (in bucket order) — their device pointers,
+    or CUDA-IPC-mapped peer pointers in a multi-process deployment."""
+    m = _ShardMap()
+    m.n = len(tables)
+    for g, t in enumerate(tables):
+        m.bucket_lo[g] = t.lo
+        m.data[g] = t.device_ptr()
+    m.bucket_lo[len(tables)] = tables[-1].hi
+    return m
+
+
 class Table:
     def __init__(self, buckets: int, depth: int, capacity: int, item_size: int, seed32: bytes,
-                 device: int = 0):
+                 device: int = 0, lo: int = 0, hi: int | None = None):
+        """cuckoo::Table; with lo/hi a payload shard holding buckets [lo, hi) (metadata whole)."""
         h = _vp()
-        _check(lib().xpir_table_create(device, buckets, depth, capacity, item_size, _p(_u8(seed32)),
-                                       C.byref(h)))
+        hi = buckets if hi is None else hi
+        _check(lib().xpir_table_create_shard(device, buckets, depth, capacity, item_size, _p(_u8(seed32)), lo, hi,
+                                             C.byref(h)))
         self.h, self.buckets, self.depth, self.item, self.device = h, buckets, depth, item_size, device
+        self.lo, self.hi = lo, hi
 
     def close(self):
         if getattr(self, "h", None):
@@ -566,11 +591,23 @@ class Table:
         _check(lib().xpir_table_insert_batch_dev(self.h, _ptr(d_b1), _ptr(d_b2), _ptr(d_payload), n,
                                                  _ptr(d_reports), _stream(stream)))
 
+    # the three steps of a round on payload shards (see include/xpir.h)
+    def insert_walk_dev(self, d_b1, d_b2, n: int, d_reports=None, stream=None) -> None:
+        _check(lib().xpir_table_insert_walk_dev(self.h, _ptr(d_b1), _ptr(d_b2), n, _ptr(d_reports), _stream(stream)))
+
+    def apply_gather_dev(self, smap: "_ShardMap | None" = None, stream=None) -> None:
+        _check(lib().xpir_table_apply_gather_dev(self.h, C.byref(smap) if smap is not None else None,
+                                                 _stream(stream)))
+
+    def apply_scatter_dev(self, d_payload, stream=None) -> None:
+        _check(lib().xpir_table_apply_scatter_dev(self.h, _ptr(d_payload), _stream(stream)))
+
     def reserve(self, max_batch: int) -> None:
         _check(lib().xpir_table_reserve(self.h, max_batch))
 
     def snapshot(self) -> np.ndarray:
-        out = np.empty(self.buckets * self.depth * self.item, np.uint8)
+        """Payload bytes (of buckets [lo, hi) for a shard)."""
+        out = np.empty((self.hi - self.lo) * self.depth * self.item, np.uint8)
         _check(lib().xpir_table_snapshot(self.h, _p(out)))
         return out
 

@@ -932,13 +932,16 @@ struct xpir_table {
     CuckooDev d{};
     CuckooState h{};
     CuckooState* dstate = nullptr;
-    uint8_t* data = nullptr;
+    uint8_t* data = nullptr;  // payloads of buckets [lo, hi)
+    uint32_t lo = 0, hi = 0;  // a payload shard of the logical table (metadata is whole)
     cudaStream_t stream = nullptr;
     DevBuf in_b1, in_b2, in_payload, in_reports, gather;
     CuckooParScratch par;
     bool parallel_prefix = true;  // XPIR_CUCKOO_SEQUENTIAL=1 disables (A/B checks)
     std::mutex mu;
     uint64_t slots() const { return uint64_t(d.buckets) * d.depth; }
+    uint64_t data_bytes() const { return uint64_t(hi - lo) * d.depth * d.item; }
+    bool sharded() const { return lo != 0 || hi != d.buckets; }
 };
 
 static const uint32_t DRAW_CAP = 1u << 16;
@@ -970,6 +973,11 @@ extern "C" {
 
 int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t capacity,
                       uint64_t item_size, const uint8_t seed[32], xpir_table** out) {
+    return xpir_table_create_shard(device, buckets, depth, capacity, item_size, seed, 0, buckets, out);
+}
+
+int xpir_table_create_shard(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
+                            const uint8_t seed[32], uint32_t lo, uint32_t hi, xpir_table** out) {
     if (!out || !seed) return fail(XPIR_EINVAL, "table_create: null argument");
     if (buckets == 0 || depth == 0 || item_size == 0)  // cuckoo.cpp:15-16
         return fail(XPIR_EINVAL, "cuckoo: table dimensions must be positive");
@@ -977,6 +985,7 @@ int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t cap
         return fail(XPIR_EINVAL, "cuckoo: capacity must be in [1, buckets*depth]");
     if (uint64_t(buckets) * depth >= (uint64_t(1) << 32))
         return fail(XPIR_EINVAL, "cuckoo: more than 2^32 slots");
+    if (lo >= hi || hi > buckets) return fail(XPIR_EINVAL, "table_create: bad shard bucket range");
     int ndev = 0;
     XCK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(XPIR_EINVAL, "table_create: bad device");
@@ -1010,7 +1019,9 @@ int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t cap
     M(reinterpret_cast<void**>(&t->d.fifo), 8 * fc);
     M(reinterpret_cast<void**>(&t->d.draws), 8 * uint64_t(DRAW_CAP));
     M(reinterpret_cast<void**>(&t->dstate), sizeof(CuckooState));
-    M(reinterpret_cast<void**>(&t->data), slots * item_size);
+    t->lo = lo;
+    t->hi = hi;
+    M(reinterpret_cast<void**>(&t->data), uint64_t(hi - lo) * depth * item_size);
     if (e == cudaSuccess) e = cudaMemset(t->d.fifo, 0xff, 8 * fc);  // -1: no entry
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
@@ -1040,6 +1051,18 @@ int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint3
     if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
     if (n == 0) return XPIR_OK;
     if (!d_b1 || !d_b2 || !d_payload) return fail(XPIR_EINVAL, "table_insert: null buffer");
+    if (t->sharded())
+        return fail(XPIR_EINVAL, "table_insert: payload shard: use insert_walk + apply_gather (all shards) + apply_scatter");
+    int rc = xpir_table_insert_walk_dev(t, d_b1, d_b2, n, d_reports, stream);
+    if (rc) return rc;
+    rc = xpir_table_apply_gather_dev(t, nullptr, stream);
+    if (rc) return rc;
+    return xpir_table_apply_scatter_dev(t, d_payload, stream);
+}
+
+int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n,
+                               uint32_t* d_reports, void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
     DeviceGuard g(t->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
     t->h.batch_id += 1;
@@ -1073,11 +1096,48 @@ int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint3
         i = t->h.resume_at;
         if (t->h.status == 1) t->h.draw_count = 0;  // force a refill
     }
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_table_apply_gather_dev(xpir_table* t, const xpir_shard_map* map, void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_apply: null table");
+    ShardMap m{};
+    if (map) {
+        if (map->n > 8) return fail(XPIR_EINVAL, "table_apply: at most 8 shards");
+        m.n = map->n;
+        for (uint32_t k = 0; k <= map->n; ++k) m.lo[k] = map->bucket_lo[k];
+        for (uint32_t k = 0; k < map->n; ++k) m.data[k] = map->data[k];
+        if (m.n && (m.lo[0] != 0 || m.lo[m.n] != t->d.buckets))
+            return fail(XPIR_EINVAL, "table_apply: shard map must cover every bucket");
+    } else if (t->sharded()) {
+        return fail(XPIR_EINVAL, "table_apply: a payload shard needs the shard map");
+    }
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
     XCK(t->gather.ensure(uint64_t(t->h.n_touched) * t->d.item));
     t->d.gather = t->gather.as<uint8_t>();
-    XCK(launch_cuckoo_apply(t->d, &t->h, t->data, d_payload, s));
-    count_launches(2);
+    XCK(launch_cuckoo_gather_sharded(t->d, &t->h, t->lo, t->hi, t->data, m, s));
+    count_launches(1);
     if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_table_apply_scatter_dev(xpir_table* t, const uint8_t* d_payload, void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_apply: null table");
+    if (t->h.n_touched && !d_payload) return fail(XPIR_EINVAL, "table_apply: null payload");
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    XCK(launch_cuckoo_scatter_sharded(t->d, &t->h, t->lo, t->hi, t->data, d_payload, s));
+    count_launches(1);
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_table_shard(const xpir_table* t, uint32_t* lo, uint32_t* hi) {
+    if (!t) return fail(XPIR_EINVAL, "table_shard: null table");
+    if (lo) *lo = t->lo;
+    if (hi) *hi = t->hi;
     return XPIR_OK;
 }
 
@@ -1135,7 +1195,7 @@ int xpir_table_snapshot(const xpir_table* t, uint8_t* host_out) {
     if (!t || !host_out) return fail(XPIR_EINVAL, "table_snapshot: null argument");
     DeviceGuard g(t->device);
     XCK(cudaStreamSynchronize(t->stream));
-    XCK(cudaMemcpy(host_out, t->data, t->slots() * t->d.item, cudaMemcpyDeviceToHost));
+    XCK(cudaMemcpy(host_out, t->data, t->data_bytes(), cudaMemcpyDeviceToHost));
     return XPIR_OK;
 }
 
@@ -1146,9 +1206,10 @@ int xpir_table_seal(const xpir_table* t, xpir_store* st, uint64_t epoch, void* s
     if (st->N != t->d.buckets || uint64_t(st->S) != uint64_t(t->d.depth) * t->d.item)
         return fail(XPIR_EINVAL, "table_seal: store geometry differs from the table");
     if (st->device != t->device) return fail(XPIR_EINVAL, "table_seal: different devices");
+    if (st->lo < t->lo || st->hi > t->hi) return fail(XPIR_EINVAL, "table_seal: store range outside the payload shard");
     DeviceGuard g(t->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
-    XCK(cudaMemcpyAsync(st->data, t->data + uint64_t(st->lo) * st->S, st->bytes(),
+    XCK(cudaMemcpyAsync(st->data, t->data + uint64_t(st->lo - t->lo) * st->S, st->bytes(),
                         cudaMemcpyDeviceToDevice, s));
     if (!stream) XCK(cudaStreamSynchronize(s));
     st->epoch = epoch;
@@ -1188,6 +1249,7 @@ int xpir_table_slot_used(const xpir_table* t, uint32_t bucket, uint32_t slot) {
 
 int xpir_table_state_digest(const xpir_table* t, uint8_t out[32]) {
     if (!t || !out) return fail(XPIR_EINVAL, "state_digest: null argument");
+    if (t->sharded()) return fail(XPIR_EINVAL, "state_digest: needs the whole table (this is a payload shard)");
     const uint64_t n = t->slots();
     std::vector<uint8_t> data(n * t->d.item), used(n);
     std::vector<uint32_t> b1(n), b2(n);

@@ -153,6 +153,22 @@ cudaError_t launch_cuckoo_walk_w(const CuckooDev& d, CuckooState* st, const uint
 cudaError_t launch_cuckoo_apply(const CuckooDev& d, const CuckooState* st_host_copy,
                                 uint8_t* table, const uint8_t* payload, cudaStream_t s);
 
+// Bucket-range payload shards of one logical table (metadata replicated on every
+// shard, each shard holds the payloads of buckets [lo[g], lo[g+1])). data[g] may
+// be a CUDA-IPC-mapped peer pointer (NVLink).
+struct ShardMap {
+    uint32_t n;
+    uint32_t lo[9];
+    const uint8_t* data[8];
+};
+// Phase 1: stage the pre-round payloads that move INTO this shard's range (from
+// any shard); phase 2 (after every shard's phase 1): write this shard's touched
+// slots. The payload array `table` holds buckets [lo, hi) of this shard.
+cudaError_t launch_cuckoo_gather_sharded(const CuckooDev& d, const CuckooState* st, uint32_t lo, uint32_t hi,
+                                         const uint8_t* table, const ShardMap& map, cudaStream_t s);
+cudaError_t launch_cuckoo_scatter_sharded(const CuckooDev& d, const CuckooState* st, uint32_t lo, uint32_t hi,
+                                          uint8_t* table, const uint8_t* payload, cudaStream_t s);
+
 // Grow-only scratch of the parallel eviction-free prefix (cuckoo_par.cu).
 struct CuckooParScratch {
     void *keys_a = nullptr, *keys_b = nullptr, *outcome = nullptr, *succ = nullptr;

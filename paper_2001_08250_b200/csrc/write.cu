@@ -413,6 +413,81 @@ __global__ void k_cuckoo_scatter(CuckooDev d, uint32_t n_touched, uint8_t* __res
     }
 }
 
+// ---- bucket-range payload shards ("payload scatter goes to the GPU
+// owning each bucket range"). The walk is replicated, so every shard knows every
+// touched slot and its origin; a shard only materialises the slots of its range.
+__global__ void k_cuckoo_gather_sharded(CuckooDev d, uint32_t n_touched, uint64_t f_lo, uint64_t f_hi,
+                                        const uint8_t* __restrict__ table, ShardMap map) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_touched; k += nw) {
+        const uint32_t f = d.touched[k];
+        if (f < f_lo || f >= f_hi) continue;
+        const int64_t o = d.origin[f];
+        if (o > -2) continue;
+        const uint64_t src = uint64_t(-o - 2);  // pre-round slot of the moved item
+        const uint8_t* s = nullptr;
+        if (src >= f_lo && src < f_hi) {
+            s = table + (src - f_lo) * d.item;
+        } else {
+            const uint32_t b = uint32_t(src / d.depth);
+            for (uint32_t g = 0; g < map.n; ++g)
+                if (b >= map.lo[g] && b < map.lo[g + 1]) s = map.data[g] + (src - uint64_t(map.lo[g]) * d.depth) * d.item;
+        }
+        uint8_t* gdst = d.gather + uint64_t(k) * d.item;
+        if ((d.item & 15) == 0) {
+            for (uint64_t b = lane * 16; b < d.item; b += 32 * 16)
+                *reinterpret_cast<uint4*>(gdst + b) = s ? *reinterpret_cast<const uint4*>(s + b) : make_uint4(0, 0, 0, 0);
+        } else {
+            for (uint64_t b = lane; b < d.item; b += 32) gdst[b] = s ? s[b] : 0;
+        }
+    }
+}
+
+__global__ void k_cuckoo_scatter_sharded(CuckooDev d, uint32_t n_touched, uint64_t f_lo, uint64_t f_hi,
+                                         uint8_t* __restrict__ table, const uint8_t* __restrict__ payload,
+                                         uint32_t batch_id) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_touched; k += nw) {
+        const uint32_t f = d.touched[k];
+        if (lane == 0) d.mod_batch[f] = batch_id;  // replicated metadata: every shard records it
+        if (f < f_lo || f >= f_hi) continue;
+        const int64_t o = d.origin[f];
+        uint8_t* dst = table + (f - f_lo) * d.item;
+        const uint8_t* src = o >= 0 ? payload + uint64_t(o) * d.item
+                            : o == -1 ? nullptr
+                                      : d.gather + uint64_t(k) * d.item;
+        if ((d.item & 15) == 0) {
+            for (uint64_t b = lane * 16; b < d.item; b += 32 * 16)
+                *reinterpret_cast<uint4*>(dst + b) =
+                    src ? *reinterpret_cast<const uint4*>(src + b) : make_uint4(0, 0, 0, 0);
+        } else {
+            for (uint64_t b = lane; b < d.item; b += 32) dst[b] = src ? src[b] : 0;
+        }
+    }
+}
+
+cudaError_t launch_cuckoo_gather_sharded(const CuckooDev& d, const CuckooState* st, uint32_t lo, uint32_t hi,
+                                         const uint8_t* table, const ShardMap& map, cudaStream_t s) {
+    if (!st->n_touched) return cudaSuccess;
+    uint32_t g = (st->n_touched + 7) / 8;
+    if (g > 148 * 16) g = 148 * 16;
+    k_cuckoo_gather_sharded<<<g, 256, 0, s>>>(d, st->n_touched, uint64_t(lo) * d.depth, uint64_t(hi) * d.depth,
+                                              table, map);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cuckoo_scatter_sharded(const CuckooDev& d, const CuckooState* st, uint32_t lo, uint32_t hi,
+                                          uint8_t* table, const uint8_t* payload, cudaStream_t s) {
+    if (!st->n_touched) return cudaSuccess;
+    uint32_t g = (st->n_touched + 7) / 8;
+    if (g > 148 * 16) g = 148 * 16;
+    k_cuckoo_scatter_sharded<<<g, 256, 0, s>>>(d, st->n_touched, uint64_t(lo) * d.depth, uint64_t(hi) * d.depth,
+                                               table, payload, st->batch_id);
+    return cudaGetLastError();
+}
+
 // Incremental seal (ServerCore::seal_epoch, server.cpp:75-81, without the full
 // copy): bring a sealed image last synchronised at round `since` up to date by
 // copying only the slots a later round modified. One warp per slot range.

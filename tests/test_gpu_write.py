@@ -226,3 +226,50 @@ print("ok")
     env["XPIR_CUCKOO_WALK"] = "2" if walk == "w" else "0"
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=900)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+@pytest.mark.parametrize("G,nb,depth,item,load", [(2, 4096, 4, 64, 0.93), (4, 1000, 4, 32, 0.97), (3, 512, 2, 48, 1.4)])
+def test_payload_shards_match_whole_table(xp, port, cuda, G, nb, depth, item, load):
+    """Bucket-range payload shards: every shard runs the replicated
+    walk, gathers the payloads that move into its range from whichever shard holds
+    them, then scatters; the union of the shards equals the whole table after
+    every round (high load: evictions cross shard boundaries; load > 1: GC), and
+    the metadata of every replica equals the oracle's."""
+    import torch
+
+    g = np.random.default_rng(G * 1000 + nb)
+    seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+    cap = nb * depth * 9 // 10 if load > 1 else nb * depth
+    bounds = [0] + [((nb * k // G) // 8) * 8 for k in range(1, G)] + [nb]
+    shards = [xp.Table(nb, depth, cap, item, seed, lo=bounds[k], hi=bounds[k + 1]) for k in range(G)]
+    smap = xp.shard_map(shards)
+    P = port.table(nb, depth, cap, item, seed)
+    n_total = int(nb * depth * load)
+    for rnd in range(3):
+        n = n_total // 3
+        b1 = g.integers(0, nb, n).astype(np.uint32)
+        b2 = g.integers(0, nb, n).astype(np.uint32)
+        pl = g.integers(0, 256, (n, item), dtype=np.uint8)
+        want_rep = P.insert_batch(b1, b2, pl)
+        d1, d2 = torch.from_numpy(b1.view(np.int32)).cuda(), torch.from_numpy(b2.view(np.int32)).cuda()
+        dp = torch.from_numpy(pl).cuda()
+        reps = [torch.zeros((n, 4), dtype=torch.int32, device="cuda") for _ in shards]
+        for t, r in zip(shards, reps):
+            t.insert_walk_dev(d1, d2, n, r)
+        for t in shards:
+            t.apply_gather_dev(smap)
+        torch.cuda.synchronize()  # the barrier between the phases
+        for t in shards:
+            t.apply_scatter_dev(dp)
+        torch.cuda.synchronize()
+        for r in reps:
+            assert np.array_equal(r.cpu().numpy().view(np.uint32), want_rep), rnd
+        whole = np.concatenate([t.snapshot() for t in shards])
+        assert np.array_equal(whole, P.data()), rnd
+        used, m1, m2, st = shards[G - 1].meta()
+        pu, p1, p2, pst = P.meta()
+        assert np.array_equal(used, pu) and np.array_equal(m1, p1) and np.array_equal(st, pst)
+    with pytest.raises(xp.InvalidArgument):
+        shards[0].state_digest()  # needs the whole table
+    with pytest.raises(xp.InvalidArgument):
+        shards[0].insert_batch([0], [0], np.zeros(item, np.uint8))  # the one-call path is whole-table only
