@@ -37,3 +37,17 @@ def test_sharded_ipc_reduce(cuda, world, N, S, B, fused):
     print(out.stdout[-2000:], out.stderr[-3000:])
     assert out.returncode == 0
     assert "SHARDED_IPC_OK" in out.stdout
+
+
+@pytest.mark.parametrize("world,nb", [(2, 2048), (3, 1000), (4, 4096)])
+def test_sharded_write_path_ipc(cuda, world, nb):
+    """Payload shards in separate processes: cross-shard moves of pre-round payloads
+    read through CUDA-IPC-mapped peer memory; union == the oracle's table."""
+    env = dict(os.environ, XP_NB=str(nb))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           os.path.join(ROOT, "tests", "mgpu_write_check.py")]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    print(out.stdout[-2000:], out.stderr[-3000:])
+    assert out.returncode == 0
+    assert "SHARDED_WRITE_OK" in out.stdout
