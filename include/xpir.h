@@ -328,6 +328,13 @@ typedef struct xpir_server xpir_server;
 int xpir_server_create(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
                        const uint8_t seed[32], uint32_t m_bits, uint32_t h, uint32_t window_deltas,
                        uint32_t rotate_writes, uint32_t epoch_ring, xpir_server** out);
+/* A server whose table and sealed stores hold the payloads of buckets [lo, hi)
+ * (one rank of a bucket-range sharded deployment; the walk, the interest window
+ * and the epoch numbering are replicated on every rank). */
+int xpir_server_create_shard(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
+                             const uint8_t seed[32], uint32_t m_bits, uint32_t h, uint32_t window_deltas,
+                             uint32_t rotate_writes, uint32_t epoch_ring, uint32_t lo, uint32_t hi,
+                             xpir_server** out);
 int xpir_server_destroy(xpir_server* sv);
 /* n calls of ServerCore::apply_write (server.cpp:58-73) in order — insert,
  * absorb the write's h_per_write interest positions, rotate every rotate_writes
@@ -335,6 +342,14 @@ int xpir_server_destroy(xpir_server* sv);
 int xpir_server_apply_round(xpir_server* sv, const uint32_t* beta1, const uint32_t* beta2, const uint8_t* payload,
                             const uint32_t* interest, uint32_t h_per_write, uint64_t n, int seal_after,
                             uint32_t* reports, uint64_t* sealed_epoch);
+/* apply_round on one rank of a sharded deployment: every rank calls it with the
+ * same writes; barrier(ctx) must return once every rank has reached it (between
+ * the payload gather and scatter phases, see xpir_table_apply_gather_dev). */
+int xpir_server_apply_round_sharded(xpir_server* sv, const uint32_t* beta1, const uint32_t* beta2,
+                                    const uint8_t* payload, const uint32_t* interest, uint32_t h_per_write,
+                                    uint64_t n, int seal_after, const xpir_shard_map* map,
+                                    void (*barrier)(void*), void* barrier_ctx, uint32_t* reports,
+                                    uint64_t* sealed_epoch);
 int xpir_server_seal(xpir_server* sv, uint64_t* epoch);            /* seal_epoch, server.cpp:75-81 */
 /* snapshot_at (server.cpp:83-87); epoch 0 = latest. The store stays owned by the
  * server and valid until its epoch leaves the ring. */

@@ -146,6 +146,11 @@ _SIGS = {
     "xpir_table_insert_walk_dev": ([_vp, _vp, _vp, C.c_uint64, _vp, _vp], C.c_int),
     "xpir_table_apply_gather_dev": ([_vp, _vp, _vp], C.c_int),
     "xpir_table_apply_scatter_dev": ([_vp, _vp, _vp], C.c_int),
+    "xpir_server_create_shard": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint64, _u8p, C.c_uint32,
+                                  C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                  C.POINTER(_vp)], C.c_int),
+    "xpir_server_apply_round_sharded": ([_vp, _u32p, _u32p, _u8p, _u32p, C.c_uint32, C.c_uint64, C.c_int, _vp,
+                                         _vp, _vp, _u32p, _u64p], C.c_int),
     "xpir_answer_batch_mixed": ([_vp, C.c_uint32, _u8p, _u8p, _u8p, C.c_uint64, C.c_uint32, _u8p, _u8p], C.c_int),
     "xpir_window_digest_n": ([_vp, C.c_uint64, _u8p], C.c_int),
     "xpir_window_encode_delta": ([_vp, C.c_uint64, _u8p, C.c_uint64, _u64p], C.c_int),
@@ -747,8 +752,8 @@ def encode_delta_dev(d_words, m_bits: int, d_out=None, cap: int = 0, device: int
 class _BorrowedStore(Store):
     """A sealed store owned by a Server (valid while its epoch is in the ring)."""
 
-    def __init__(self, handle, N: int, S: int, device: int):  # noqa: D401 - no super().__init__
-        self.h, self.N, self.S, self.lo, self.hi, self.device = handle, N, S, 0, N, device
+    def __init__(self, handle, N: int, S: int, device: int, lo: int = 0, hi: int | None = None):  # noqa: D401
+        self.h, self.N, self.S, self.lo, self.hi, self.device = handle, N, S, lo, N if hi is None else hi, device
 
     def close(self):
         self.h = None
@@ -756,16 +761,38 @@ class _BorrowedStore(Store):
     __del__ = close
 
 
+_BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
+
+
+def server_shard_map(servers: list["Server"], ptrs: list[int] | None = None) -> "_ShardMap":
+    """Shard map over the ranks' payload arrays (ptrs: IPC-mapped pointers, in rank order)."""
+    m = _ShardMap()
+    m.n = len(servers)
+    for g, sv in enumerate(servers):
+        m.bucket_lo[g] = sv.lo
+        m.data[g] = ptrs[g] if ptrs is not None else sv.payload_ptr()
+    m.bucket_lo[len(servers)] = servers[-1].hi
+    return m
+
+
 class Server:
     """Device ServerCore: Table + Window + ring of sealed stores (server.cpp:28-91)."""
 
     def __init__(self, buckets: int, depth: int, capacity: int, item_size: int, seed32: bytes, m_bits: int, h: int,
-                 window_deltas: int, rotate_writes: int, epoch_ring: int, device: int = 0):
+                 window_deltas: int, rotate_writes: int, epoch_ring: int, device: int = 0, lo: int = 0,
+                 hi: int | None = None):
+        """With lo/hi: one rank of a bucket-range sharded deployment (payloads and
+        sealed stores of buckets [lo, hi); walk, window and epochs replicated)."""
         hd = _vp()
-        _check(lib().xpir_server_create(device, buckets, depth, capacity, item_size, _p(_u8(seed32)), m_bits, h,
-                                        window_deltas, rotate_writes, epoch_ring, C.byref(hd)))
+        hi = buckets if hi is None else hi
+        _check(lib().xpir_server_create_shard(device, buckets, depth, capacity, item_size, _p(_u8(seed32)), m_bits,
+                                              h, window_deltas, rotate_writes, epoch_ring, lo, hi, C.byref(hd)))
         self.h, self.buckets, self.depth, self.item, self.device = hd, buckets, depth, item_size, device
-        self.nh = h
+        self.nh, self.lo, self.hi = h, lo, hi
+
+    def payload_ptr(self) -> int:
+        """Device pointer of this rank's payload shard (for the shard map / IPC)."""
+        return lib().xpir_table_device_data(self._handles()[0])
 
     def close(self):
         if getattr(self, "h", None):
@@ -774,7 +801,9 @@ class Server:
 
     __del__ = close
 
-    def apply_round(self, beta1, beta2, payload, interest, seal_after: bool = False):
+    def apply_round(self, beta1, beta2, payload, interest, seal_after: bool = False, smap=None, barrier=None):
+        """ServerCore::apply_write for each write (+ seal). On a shard rank pass the
+        shard map of all ranks' payload arrays and a barrier() over the ranks."""
         b1 = np.ascontiguousarray(beta1, np.uint32)
         b2 = np.ascontiguousarray(beta2, np.uint32)
         n = len(b1)
@@ -782,9 +811,16 @@ class Server:
         pos = np.ascontiguousarray(interest, np.uint32).reshape(n, -1) if n else np.zeros((0, self.nh), np.uint32)
         rep = np.zeros((max(n, 1), 4), np.uint32)
         ep = C.c_uint64()
-        _check(lib().xpir_server_apply_round(self.h, _p(b1, _u32p), _p(b2, _u32p), _p(pl),
-                                             _p(pos, _u32p) if pos.size else None, pos.shape[1] if n else 0, n,
-                                             1 if seal_after else 0, _p(rep, _u32p), C.byref(ep)))
+        if smap is None:
+            _check(lib().xpir_server_apply_round(self.h, _p(b1, _u32p), _p(b2, _u32p), _p(pl),
+                                                 _p(pos, _u32p) if pos.size else None, pos.shape[1] if n else 0, n,
+                                                 1 if seal_after else 0, _p(rep, _u32p), C.byref(ep)))
+        else:
+            cb = _BARRIER_FN(lambda _ctx: barrier())
+            _check(lib().xpir_server_apply_round_sharded(
+                self.h, _p(b1, _u32p), _p(b2, _u32p), _p(pl), _p(pos, _u32p) if pos.size else None,
+                pos.shape[1] if n else 0, n, 1 if seal_after else 0, C.cast(C.pointer(smap), _vp),
+                C.cast(cb, _vp), None, _p(rep, _u32p), C.byref(ep)))
         return rep[:n], ep.value
 
     def seal(self) -> int:
@@ -795,7 +831,7 @@ class Server:
     def snapshot(self, epoch: int = 0) -> Store:
         st = _vp()
         _check(lib().xpir_server_snapshot(self.h, epoch, C.byref(st)))
-        return _BorrowedStore(st, self.buckets, self.depth * self.item, self.device)
+        return _BorrowedStore(st, self.buckets, self.depth * self.item, self.device, self.lo, self.hi)
 
     def info(self):
         w, l, o = C.c_uint64(), C.c_uint64(), C.c_uint64()

@@ -1578,11 +1578,11 @@ static int server_seal(xpir_server* sv, uint64_t* epoch_out) {  // server.cpp:75
         // reuse the oldest image: only slots rewritten since it was sealed are copied
         e = sv->ring.front();
         sv->ring.pop_front();
-        XCK(launch_seal_incremental(t->d, e.since_batch, t->data, e.st->data, num_sms(sv->device), t->stream));
+        XCK(launch_seal_incremental(t->d, t->lo, t->hi, e.since_batch, t->data, e.st->data, num_sms(sv->device),
+                                    t->stream));
         count_launches(1);
     } else {
-        int rc = xpir_store_create(sv->device, t->d.buckets, uint32_t(t->d.depth * t->d.item), 0, t->d.buckets,
-                                   &e.st);
+        int rc = xpir_store_create(sv->device, t->d.buckets, uint32_t(t->d.depth * t->d.item), t->lo, t->hi, &e.st);
         if (rc) return rc;
         XCK(cudaMemcpyAsync(e.st->data, t->data, e.st->bytes(), cudaMemcpyDeviceToDevice, t->stream));
     }
@@ -1600,6 +1600,14 @@ extern "C" {
 int xpir_server_create(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
                        const uint8_t seed[32], uint32_t m_bits, uint32_t h, uint32_t window_deltas,
                        uint32_t rotate_writes, uint32_t epoch_ring, xpir_server** out) {
+    return xpir_server_create_shard(device, buckets, depth, capacity, item_size, seed, m_bits, h, window_deltas,
+                                    rotate_writes, epoch_ring, 0, buckets, out);
+}
+
+int xpir_server_create_shard(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
+                             const uint8_t seed[32], uint32_t m_bits, uint32_t h, uint32_t window_deltas,
+                             uint32_t rotate_writes, uint32_t epoch_ring, uint32_t lo, uint32_t hi,
+                             xpir_server** out) {
     if (!out) return fail(XPIR_EINVAL, "server_create: null out");
     if (rotate_writes == 0) return fail(XPIR_EINVAL, "server_create: rotate_writes must be positive");
     if (epoch_ring == 0) return fail(XPIR_EINVAL, "server_create: epoch_ring must be positive");
@@ -1607,7 +1615,7 @@ int xpir_server_create(int device, uint32_t buckets, uint32_t depth, uint64_t ca
     sv->device = device;
     sv->rotate_writes = rotate_writes;
     sv->epoch_ring = epoch_ring;
-    int rc = xpir_table_create(device, buckets, depth, capacity, item_size, seed, &sv->table);
+    int rc = xpir_table_create_shard(device, buckets, depth, capacity, item_size, seed, lo, hi, &sv->table);
     if (!rc) rc = xpir_window_create(device, m_bits, h, window_deltas, &sv->window);
     if (!rc) rc = xpir_window_rotate(sv->window);  // server.cpp:40
     if (!rc) rc = server_seal(sv, nullptr);          // server.cpp:42, epoch 1 (all zeros)
@@ -1632,7 +1640,46 @@ int xpir_server_destroy(xpir_server* sv) {
 int xpir_server_apply_round(xpir_server* sv, const uint32_t* beta1, const uint32_t* beta2, const uint8_t* payload,
                             const uint32_t* interest, uint32_t h_per_write, uint64_t n, int seal_after,
                             uint32_t* reports, uint64_t* sealed_epoch) {
+    return xpir_server_apply_round_sharded(sv, beta1, beta2, payload, interest, h_per_write, n, seal_after, nullptr,
+                                           nullptr, nullptr, reports, sealed_epoch);
+}
+
+// The table insert of a round on a payload shard: H2D, replicated walk, gather
+// (peer shards), the caller's barrier, scatter.
+static int table_insert_sharded(xpir_table* t, const uint32_t* b1, const uint32_t* b2, const uint8_t* payload,
+                                uint64_t n, uint32_t* reports, const xpir_shard_map* map,
+                                void (*barrier)(void*), void* ctx) {
+    std::lock_guard<std::mutex> lk(t->mu);
+    DeviceGuard g(t->device);
+    cudaStream_t s = t->stream;
+    XCK(t->in_b1.ensure(4 * n));
+    XCK(t->in_b2.ensure(4 * n));
+    XCK(t->in_payload.ensure(n * t->d.item));
+    XCK(t->in_reports.ensure(16 * n));
+    XCK(cudaMemcpyAsync(t->in_b1.p, b1, 4 * n, cudaMemcpyHostToDevice, s));
+    XCK(cudaMemcpyAsync(t->in_b2.p, b2, 4 * n, cudaMemcpyHostToDevice, s));
+    XCK(cudaMemcpyAsync(t->in_payload.p, payload, n * t->d.item, cudaMemcpyHostToDevice, s));
+    int rc = xpir_table_insert_walk_dev(t, t->in_b1.as<uint32_t>(), t->in_b2.as<uint32_t>(), n,
+                                        t->in_reports.as<uint32_t>(), s);
+    if (!rc) rc = xpir_table_apply_gather_dev(t, map, s);
+    if (rc) return rc;
+    XCK(cudaStreamSynchronize(s));
+    if (barrier) barrier(ctx);  // every shard has staged what moves into its range
+    rc = xpir_table_apply_scatter_dev(t, t->in_payload.as<uint8_t>(), s);
+    if (rc) return rc;
+    if (reports) XCK(cudaMemcpyAsync(reports, t->in_reports.p, 16 * n, cudaMemcpyDeviceToHost, s));
+    XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_server_apply_round_sharded(xpir_server* sv, const uint32_t* beta1, const uint32_t* beta2,
+                                    const uint8_t* payload, const uint32_t* interest, uint32_t h_per_write,
+                                    uint64_t n, int seal_after, const xpir_shard_map* map,
+                                    void (*barrier)(void*), void* barrier_ctx, uint32_t* reports,
+                                    uint64_t* sealed_epoch) {
     if (!sv) return fail(XPIR_EINVAL, "server_apply: null server");
+    if (sv->table->sharded() && (!map || !barrier))
+        return fail(XPIR_EINVAL, "server_apply: a payload shard needs the shard map and a barrier");
     if (sealed_epoch) *sealed_epoch = 0;
     if (n && (!beta1 || !beta2 || !payload || (h_per_write && !interest)))
         return fail(XPIR_EINVAL, "server_apply: null buffer");
@@ -1646,7 +1693,9 @@ int xpir_server_apply_round(xpir_server* sv, const uint32_t* beta1, const uint32
             break;
         }
     if (ok) {
-        int rc = xpir_table_insert_batch(sv->table, beta1, beta2, payload, ok, reports);
+        int rc = sv->table->sharded()
+                     ? table_insert_sharded(sv->table, beta1, beta2, payload, ok, reports, map, barrier, barrier_ctx)
+                     : xpir_table_insert_batch(sv->table, beta1, beta2, payload, ok, reports);
         if (rc) return rc;
         // interest positions per rotation segment, then rotate (server.cpp:64-70)
         uint64_t a = 0;

@@ -124,8 +124,9 @@ struct CuckooDev {
     uint32_t* mod_batch;  // [slots] last round (batch id) that rewrote the slot's payload
     uint64_t* chain_pre;  // [3 * 512] pre-chain contents of an eviction chain (walk_x)
 };
-cudaError_t launch_seal_incremental(const CuckooDev& d, uint32_t since, const uint8_t* table, uint8_t* img,
-                                    int num_sms, cudaStream_t s);
+// buckets [lo, hi) of the table (the payload shard / store shard range)
+cudaError_t launch_seal_incremental(const CuckooDev& d, uint32_t lo, uint32_t hi, uint32_t since,
+                                    const uint8_t* table, uint8_t* img, int num_sms, cudaStream_t s);
 
 // Scalars the walk reads and advances (device memory, one struct).
 struct CuckooState {

@@ -491,13 +491,15 @@ cudaError_t launch_cuckoo_scatter_sharded(const CuckooDev& d, const CuckooState*
 // Incremental seal (ServerCore::seal_epoch, server.cpp:75-81, without the full
 // copy): bring a sealed image last synchronised at round `since` up to date by
 // copying only the slots a later round modified. One warp per slot range.
-__global__ void k_seal_incremental(const uint32_t* __restrict__ mod_batch, uint64_t slots, uint64_t item,
-                                   uint32_t since, const uint8_t* __restrict__ table, uint8_t* __restrict__ img) {
+// slots [f_lo, f_lo + slots) of the logical table; table and img hold exactly them
+__global__ void k_seal_incremental(const uint32_t* __restrict__ mod_batch, uint64_t f_lo, uint64_t slots,
+                                   uint64_t item, uint32_t since, const uint8_t* __restrict__ table,
+                                   uint8_t* __restrict__ img) {
     const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
     for (uint64_t f = warp; f < slots; f += nwarps) {
-        if (mod_batch[f] <= since) continue;
+        if (mod_batch[f_lo + f] <= since) continue;
         const uint8_t* s = table + f * item;
         uint8_t* dst = img + f * item;
         if ((item & 15) == 0) {
@@ -509,13 +511,14 @@ __global__ void k_seal_incremental(const uint32_t* __restrict__ mod_batch, uint6
     }
 }
 
-cudaError_t launch_seal_incremental(const CuckooDev& d, uint32_t since, const uint8_t* table, uint8_t* img,
-                                    int num_sms, cudaStream_t s) {
-    const uint64_t slots = uint64_t(d.buckets) * d.depth;
+cudaError_t launch_seal_incremental(const CuckooDev& d, uint32_t lo, uint32_t hi, uint32_t since,
+                                    const uint8_t* table, uint8_t* img, int num_sms, cudaStream_t s) {
+    const uint64_t slots = uint64_t(hi - lo) * d.depth;
     if (!slots) return cudaSuccess;
     uint64_t g = (slots * 32 + 255) / 256;
     if (g > uint64_t(num_sms) * 16) g = uint64_t(num_sms) * 16;
-    k_seal_incremental<<<uint32_t(g), 256, 0, s>>>(d.mod_batch, slots, d.item, since, table, img);
+    k_seal_incremental<<<uint32_t(g), 256, 0, s>>>(d.mod_batch, uint64_t(lo) * d.depth, slots, d.item, since,
+                                                   table, img);
     return cudaGetLastError();
 }
 

@@ -65,3 +65,56 @@ def test_server_rounds_and_epoch_ring(xp, port, cuda, nb, depth, item, ring, R):
     img = sealed[max(sealed)].reshape(nb, depth * item)
     assert np.array_equal(out[0], img[0])
     assert np.array_equal(out[1], np.bitwise_xor.reduce(img, axis=0))
+
+
+@pytest.mark.parametrize("G,nb,ring,R", [(2, 512, 3, 40), (4, 1024, 2, 150)])
+def test_sharded_servers_match_whole_server(xp, port, cuda, G, nb, ring, R):
+    """G bucket-range shard ranks of one replica (threads here, one rank per GPU in
+    a deployment): same writes on every rank, payload gather/scatter across the
+    shards with a barrier between the phases. After every round the union of the
+    ranks' sealed shard stores equals the whole server's sealed store for every
+    epoch in the ring, and the replicated window digests agree."""
+    import threading
+
+    depth, item, m, h, W = 4, 32, 2048, 3, 3
+    g = np.random.default_rng(G + nb)
+    seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+    cap = nb * depth
+    bounds = [0] + [((nb * k // G) // 8) * 8 for k in range(1, G)] + [nb]
+    whole = xp.Server(nb, depth, cap, item, seed, m, h, W, R, ring)
+    ranks = [xp.Server(nb, depth, cap, item, seed, m, h, W, R, ring, lo=bounds[k], hi=bounds[k + 1])
+             for k in range(G)]
+    smap = xp.server_shard_map(ranks)
+    bar = threading.Barrier(G)
+    for rnd in range(6):
+        n = int(g.integers(nb // 2, nb * 2))
+        b1 = g.integers(0, nb, n).astype(np.uint32)
+        b2 = g.integers(0, nb, n).astype(np.uint32)
+        pl = g.integers(0, 256, (n, item), dtype=np.uint8)
+        pos = g.integers(0, m, (n, h)).astype(np.uint32)
+        seal = rnd % 2 == 0
+        want_rep, want_ep = whole.apply_round(b1, b2, pl, pos, seal_after=seal)
+        res = [None] * G
+        errs = []
+
+        def run(k):
+            try:
+                res[k] = ranks[k].apply_round(b1, b2, pl, pos, seal_after=seal, smap=smap, barrier=bar.wait)
+            except BaseException as e:  # noqa: BLE001
+                errs.append(e)
+                bar.abort()
+
+        ts = [threading.Thread(target=run, args=(k,)) for k in range(G)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert not errs, errs
+        for rep, ep in res:
+            assert np.array_equal(rep, want_rep) and ep == want_ep
+        info = whole.info()
+        for e in range(info["oldest_epoch"], info["latest_epoch"] + 1):
+            full = whole.snapshot(e).download()
+            parts = np.concatenate([r.snapshot(e).download() for r in ranks])
+            assert np.array_equal(parts, full), (rnd, e)
+        assert all(r.window_digest() == whole.window_digest() for r in ranks)
