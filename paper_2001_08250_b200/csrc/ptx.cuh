@@ -42,30 +42,5 @@ __device__ __forceinline__ void red_xor64(void* p, uint64_t v) {
     asm volatile("red.relaxed.gpu.global.xor.b64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
 }
 
-// mbarrier + 1-D bulk async copy (TMA engine, no tensor map)
-__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_init_fence() {
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(mbar)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "MBW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra MBW%=;\n}\n" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-
 }  // namespace ptx
 }  // namespace xpir

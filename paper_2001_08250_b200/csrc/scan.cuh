@@ -151,9 +151,6 @@ cudaError_t launch_cuckoo_walk_x(const CuckooDev& d, CuckooState* st, const uint
 bool walk_w_supported(const CuckooDev& d);
 cudaError_t launch_cuckoo_walk_w(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
                                  uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s);
-cudaError_t launch_cuckoo_apply(const CuckooDev& d, const CuckooState* st_host_copy,
-                                uint8_t* table, const uint8_t* payload, cudaStream_t s);
-
 // Bucket-range payload shards of one logical table (metadata replicated on every
 // shard, each shard holds the payloads of buckets [lo[g], lo[g+1])). data[g] may
 // be a CUDA-IPC-mapped peer pointer (NVLink).

@@ -25,7 +25,7 @@
 // draw, rng.cpp:9-31) between inserts, so the kernel only returns to the host
 // when the global window (64 Ki draws) is exhausted.
 // Payload bytes are not moved here: each touched slot records where its final
-// content comes from (origin, see k_cuckoo_walk) for k_cuckoo_gather/scatter.
+// content comes from (origin, see k_cuckoo_walk) for the gather/scatter kernels.
 #include <cuda_runtime.h>
 
 #include <cstdint>

@@ -151,14 +151,7 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 tm_st1(tbase + c, v);
             }
         }
-        // alt[] accessors (warp-uniform slot for the TMEM path)
-        auto alt_get = [&](uint32_t f) -> uint32_t {
-            if (f < X_SM_SLOTS) return alt[f];
-            const uint32_t i = f - X_SM_SLOTS;
-            __syncwarp();
-            const uint32_t v = __shfl_sync(FULLM, tm_ld1(tbase + (i >> 6)), (i >> 1) & 31);
-            return (i & 1) ? v >> 16 : v & 0xffffu;
-        };
+        // alt[] accessor (warp-uniform slot for the TMEM path):
         // returns the old value and stores x (one read-modify-write)
         auto alt_swap = [&](uint32_t f, uint32_t x) -> uint32_t {
             if (f < X_SM_SLOTS) {

@@ -139,7 +139,8 @@ __global__ void k_absorb(const uint32_t* __restrict__ pos, uint64_t n,
 // occupancy bitmap into shared memory first so the common path (free slot in
 // beta1/beta2) never waits on global memory. Payload bytes are not moved here:
 // each touched slot records where its final content comes from (origin) and
-// k_cuckoo_gather/scatter move the bytes in parallel afterwards.
+// k_cuckoo_gather_sharded / k_cuckoo_scatter_sharded move the bytes in parallel
+// afterwards.
 //   origin >= 0   : payload row `origin` of this batch
 //   origin == -1  : cleared (zero)
 //   origin <= -2  : the pre-batch content of flat slot (-origin - 2)
@@ -368,51 +369,6 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
     }
 }
 
-// phase 1: stage pre-existing payloads that moved (origin <= -2) into d.gather[k].
-// One warp per touched slot (grid-stride): most touched slots take an incoming
-// payload, so this pass is mostly a metadata read.
-__global__ void k_cuckoo_gather(CuckooDev d, uint32_t n_touched, const uint8_t* __restrict__ table) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_touched; k += nw) {
-        const uint32_t f = d.touched[k];
-        const int64_t o = d.origin[f];
-        if (o > -2) continue;
-        const uint64_t src = uint64_t(-o - 2);
-        const uint8_t* s = table + src * d.item;
-        uint8_t* g = d.gather + uint64_t(k) * d.item;
-        if ((d.item & 15) == 0) {
-            for (uint64_t b = lane * 16; b < d.item; b += 32 * 16)
-                *reinterpret_cast<uint4*>(g + b) = *reinterpret_cast<const uint4*>(s + b);
-        } else {
-            for (uint64_t b = lane; b < d.item; b += 32) g[b] = s[b];
-        }
-    }
-}
-
-// phase 2: write each touched slot's final content (one warp per slot, grid-stride)
-__global__ void k_cuckoo_scatter(CuckooDev d, uint32_t n_touched, uint8_t* __restrict__ table,
-                                 const uint8_t* __restrict__ payload, uint32_t batch_id) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_touched; k += nw) {
-        const uint32_t f = d.touched[k];
-        const int64_t o = d.origin[f];
-        if (lane == 0) d.mod_batch[f] = batch_id;  // for incremental seals
-        uint8_t* dst = table + uint64_t(f) * d.item;
-        const uint8_t* src = o >= 0 ? payload + uint64_t(o) * d.item
-                            : o == -1 ? nullptr
-                                      : d.gather + uint64_t(k) * d.item;
-        if ((d.item & 15) == 0) {
-            for (uint64_t b = lane * 16; b < d.item; b += 32 * 16)
-                *reinterpret_cast<uint4*>(dst + b) =
-                    src ? *reinterpret_cast<const uint4*>(src + b) : make_uint4(0, 0, 0, 0);
-        } else {
-            for (uint64_t b = lane; b < d.item; b += 32) dst[b] = src ? src[b] : 0;
-        }
-    }
-}
-
 // ---- bucket-range payload shards ("payload scatter goes to the GPU
 // owning each bucket range"). The walk is replicated, so every shard knows every
 // touched slot and its origin; a shard only materialises the slots of its range.
@@ -612,15 +568,5 @@ cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32
     return cudaGetLastError();
 }
 
-cudaError_t launch_cuckoo_apply(const CuckooDev& d, const CuckooState* st, uint8_t* table,
-                                const uint8_t* payload, cudaStream_t s) {
-    if (!st->n_touched) return cudaSuccess;
-    // one warp per touched slot, grid-stride over at most 148 x 16 CTAs of 8 warps
-    uint32_t g = (st->n_touched + 7) / 8;
-    if (g > 148 * 16) g = 148 * 16;
-    k_cuckoo_gather<<<g, 256, 0, s>>>(d, st->n_touched, table);
-    k_cuckoo_scatter<<<g, 256, 0, s>>>(d, st->n_touched, table, payload, st->batch_id);
-    return cudaGetLastError();
-}
 
 }  // namespace xpir
