@@ -94,7 +94,7 @@ bool walk_x_supported(const CuckooDev& d) {
            XLayout(uint32_t(slots)).total <= 232448;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __restrict__ beta1,
                 const uint32_t* __restrict__ beta2, uint64_t i0, uint64_t n, uint32_t* __restrict__ reports) {
     extern __shared__ __align__(16) uint8_t smx[];
@@ -138,6 +138,7 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
     if (warp == 0) {
         const uint32_t depth = d.depth;
         const uint32_t dmask = depth >= 32 ? FULLM : (1u << depth) - 1u;
+        const bool dpow2 = (depth & (depth - 1)) == 0;
         const uint64_t fmask = d.fifo_cap - 1;
         const uint64_t gend = s.draw_base + s.draw_count;
         uint64_t dr_hi = s.rng_block;
@@ -193,8 +194,163 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
             d.touched_mark[f] = s.batch_id;
         };
 
+        // ---- resolve a finished chain: who ends where (see the header comment) ----
+        bool pend_chain = false;
+        uint32_t p_h = 0, p_final = FULLM, p_b1 = 0, p_b2 = 0;
+        uint64_t p_stamp = 0, p_i = 0;
+        auto resolve_chain = [&]() {
+            const uint32_t h = p_h, final_slot = p_final, b1 = p_b1, b2 = p_b2;
+            const uint64_t stamp = p_stamp, i = p_i;
+            const uint32_t my_v = lane < h && lane < 32 ? chain[lane] : (0x80000000u | lane);
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+            __syncwarp();
+            if (h <= 32) {
+                // ---- resolve a short chain in registers -------------------------
+                // lane k holds chain[k] and its pre-chain content; revisits by match_any
+                const uint8_t* mine = smx + L.o_pre + lane * 32;
+                const uint64_t my_st = *reinterpret_cast<const uint64_t*>(mine);
+                const int64_t my_org = *reinterpret_cast<const int64_t*>(mine + 8);
+                const uint32_t my_b1 = *reinterpret_cast<const uint32_t*>(mine + 16);
+                const uint32_t my_b2 = *reinterpret_cast<const uint32_t*>(mine + 20);
+                const uint32_t my_mark = *reinterpret_cast<const uint32_t*>(mine + 24);
+                const int64_t my_pre_org = my_mark == s.batch_id ? my_org : -int64_t(my_v) - 2;
+                const uint32_t mm = __match_any_sync(FULLM, my_v);
+                const uint32_t below = mm & ((1u << lane) - 1u);
+                const uint32_t above = mm & ~((2u << lane) - 1u);
+                const int prev = below ? 31 - __clz(int(below)) : -1;  // last earlier visit
+                // f(k) = the item carried out of hop k: the pre-content of chain[k] (= k),
+                // or the item placed at its previous visit p (INC if p == 0, else f(p - 1))
+                int cur = int(lane), res = -2;  // -2 pending, -1 incoming, j >= 0 pre(chain[j])
+                bool pend = lane < h;
+                if (!pend) res = int(lane);
+                while (__any_sync(FULLM, pend)) {
+                    const int p = __shfl_sync(FULLM, prev, cur & 31);
+                    if (pend) {
+                        if (p < 0) {
+                            res = cur;
+                            pend = false;
+                        } else if (p == 0) {
+                            res = -1;
+                            pend = false;
+                        } else {
+                            cur = p - 1;
+                        }
+                    }
+                }
+                // step k places item src(k) = (k == 0 ? incoming : f(k - 1)) at chain[k];
+                // step h places f(h - 1) at the final slot (or drops it)
+                const int srck_l = __shfl_up_sync(FULLM, res, 1);
+                const int src_here = lane == 0 ? -1 : srck_l;
+                const int src_final = h == 0 ? -1 : __shfl_sync(FULLM, res, (h - 1) & 31);
+                auto content = [&](int src, uint32_t& c1, uint32_t& c2, uint64_t& cst, int64_t& corg) {
+                    const int sl = src < 0 ? 0 : src;
+                    const uint32_t x1 = __shfl_sync(FULLM, my_b1, sl), x2 = __shfl_sync(FULLM, my_b2, sl);
+                    const uint64_t xs = __shfl_sync(FULLM, my_st, sl);
+                    const int64_t xo = __shfl_sync(FULLM, my_pre_org, sl);
+                    if (src < 0) {
+                        c1 = b1;
+                        c2 = b2;
+                        cst = stamp;
+                        corg = int64_t(i);
+                    } else {
+                        c1 = x1;
+                        c2 = x2;
+                        cst = xs;
+                        corg = xo;
+                    }
+                };
+                uint32_t c1, c2;
+                uint64_t cst;
+                int64_t corg;
+                content(src_here, c1, c2, cst, corg);
+                if (lane < h && above == 0) {  // last visit of chain[lane]: its final content
+                    d.beta1[my_v] = c1;
+                    d.beta2[my_v] = c2;
+                    d.stamp[my_v] = cst;
+                    d.fifo[cst & fmask] = int64_t(my_v);
+                    touch_store(my_v, corg);
+                }
+                content(src_final, c1, c2, cst, corg);
+                if (lane == 0) {
+                    if (final_slot == FULLM) {
+                        d.fifo[cst & fmask] = -1;  // the dropped item leaves the FIFO
+                    } else {
+                        d.beta1[final_slot] = c1;
+                        d.beta2[final_slot] = c2;
+                        d.stamp[final_slot] = cst;
+                        d.fifo[cst & fmask] = int64_t(final_slot);
+                        touch_store(final_slot, corg);
+                    }
+                }
+                __syncwarp();
+            } else {
+            // ---- resolve a long chain through global scratch ----------------
+            uint64_t* pre = d.chain_pre;  // [3 * X_CHAIN]: (b1 | b2 << 32), stamp, origin
+            for (uint32_t k = lane; k < h; k += 32) {
+                const uint32_t v = chain[k];
+                pre[3 * k] = uint64_t(d.beta1[v]) | uint64_t(d.beta2[v]) << 32;
+                pre[3 * k + 1] = d.stamp[v];
+                const int64_t o = d.origin[v];
+                pre[3 * k + 2] = uint64_t(d.touched_mark[v] == s.batch_id ? o : -int64_t(v) - 2);
+                uint16_t p = NONE16;
+                for (int32_t q = int32_t(k) - 1; q >= 0; --q)
+                    if (chain[q] == v) {
+                        p = uint16_t(q);
+                        break;
+                    }
+                prevk[k] = p;
+            }
+            __syncwarp();
+            // src[k]: the item placed at step k (NONE16 = the incoming one, j = pre-content of chain[j])
+            if (lane == 0) {
+                srck[0] = NONE16;
+                for (uint32_t k = 0; k < h; ++k) srck[k + 1] = prevk[k] != NONE16 ? srck[prevk[k]] : uint16_t(k);
+            }
+            __syncwarp();
+            for (uint32_t k = lane; k <= h; k += 32) {
+                const uint16_t src = srck[k];
+                uint32_t slot;
+                if (k < h) {
+                    slot = chain[k];
+                    bool last = true;
+                    for (uint32_t q = k + 1; q < h && last; ++q) last = chain[q] != slot;
+                    if (!last) continue;
+                } else {
+                    slot = final_slot;
+                }
+                uint32_t c1 = b1, c2 = b2;
+                uint64_t cst = stamp;
+                int64_t corg = int64_t(i);
+                if (src != NONE16) {
+                    const uint64_t bb = pre[3 * src];
+                    c1 = uint32_t(bb);
+                    c2 = uint32_t(bb >> 32);
+                    cst = pre[3 * src + 1];
+                    corg = int64_t(pre[3 * src + 2]);
+                }
+                if (slot == FULLM) {  // the dropped item leaves the FIFO
+                    d.fifo[cst & fmask] = -1;
+                    continue;
+                }
+                d.beta1[slot] = c1;
+                d.beta2[slot] = c2;
+                d.stamp[slot] = cst;
+                d.fifo[cst & fmask] = int64_t(slot);
+                touch_store(slot, corg);
+            }
+            __syncwarp();
+            }
+                };
+        auto resolve_pending = [&]() {
+            if (pend_chain) {
+                resolve_chain();
+                pend_chain = false;
+            }
+        };
+
         // the sequential path (warp-redundant: every lane runs it with the same values)
         auto insert_one = [&](uint64_t i, uint32_t b1, uint32_t b2) -> bool {
+            resolve_pending();  // the previous chain's metadata before this insert reads any
             if (dr_hi - s.rng_block < X_NEED) {
                 refill();
                 if (dr_hi - s.rng_block < X_NEED) {
@@ -251,9 +407,9 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 // lane k < 32 prefetches the pre-chain content of chain[k] into shared
                 // memory while the walk goes on (nothing is written to the global
                 // metadata during the walk); cp.async keeps the registers free
-                uint32_t my_v = 0x80000000u | lane;
                 const uint32_t pre_sm = smem_base + uint32_t(L.o_pre) + lane * 32;
                 for (;; ++h) {
+                    const uint64_t dnext = ring[s.rng_block & (X_RING - 1)];  // issued before the test
                     const uint32_t fm = free_mask(be);
                     if (fm) {
                         final_slot = be * depth + uint32_t(__ffs(int(fm)) - 1);
@@ -263,10 +419,16 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                         break;
                     }
                     if (h == XPIR_MAX_DISPLACEMENTS_DEV) break;
-                    const uint32_t vf = be * depth + uint32_t(uniform(depth));
+                    uint32_t vs;
+                    if (dpow2) {  // rng.cpp:9-16 without rejection
+                        vs = uint32_t(dnext) & (depth - 1);
+                        s.rng_block++;
+                    } else {
+                        vs = uint32_t(uniform(depth));
+                    }
+                    const uint32_t vf = be * depth + vs;
                     chain[h] = vf;
                     if (h < 32 && lane == h) {
-                        my_v = vf;
                         cp_async_ca<8>(pre_sm, d.stamp + vf);
                         cp_async_ca<8>(pre_sm + 8, d.origin + vf);
                         cp_async_ca<4>(pre_sm + 16, d.beta1 + vf);
@@ -280,144 +442,15 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 disp = final_slot == FULLM ? XPIR_MAX_DISPLACEMENTS_DEV : h;
                 dropped = final_slot == FULLM ? 1u : 0u;
                 __syncwarp();
-                asm volatile("cp.async.wait_all;\n" ::: "memory");
-                __syncwarp();
-                if (h <= 32) {
-                    // ---- resolve a short chain in registers -------------------------
-                    // lane k holds chain[k] and its pre-chain content; revisits by match_any
-                    const uint8_t* mine = smx + L.o_pre + lane * 32;
-                    const uint64_t my_st = *reinterpret_cast<const uint64_t*>(mine);
-                    const int64_t my_org = *reinterpret_cast<const int64_t*>(mine + 8);
-                    const uint32_t my_b1 = *reinterpret_cast<const uint32_t*>(mine + 16);
-                    const uint32_t my_b2 = *reinterpret_cast<const uint32_t*>(mine + 20);
-                    const uint32_t my_mark = *reinterpret_cast<const uint32_t*>(mine + 24);
-                    const int64_t my_pre_org = my_mark == s.batch_id ? my_org : -int64_t(my_v) - 2;
-                    const uint32_t mm = __match_any_sync(FULLM, my_v);
-                    const uint32_t below = mm & ((1u << lane) - 1u);
-                    const uint32_t above = mm & ~((2u << lane) - 1u);
-                    const int prev = below ? 31 - __clz(int(below)) : -1;  // last earlier visit
-                    // f(k) = the item carried out of hop k: the pre-content of chain[k] (= k),
-                    // or the item placed at its previous visit p (INC if p == 0, else f(p - 1))
-                    int cur = int(lane), res = -2;  // -2 pending, -1 incoming, j >= 0 pre(chain[j])
-                    bool pend = lane < h;
-                    if (!pend) res = int(lane);
-                    while (__any_sync(FULLM, pend)) {
-                        const int p = __shfl_sync(FULLM, prev, cur & 31);
-                        if (pend) {
-                            if (p < 0) {
-                                res = cur;
-                                pend = false;
-                            } else if (p == 0) {
-                                res = -1;
-                                pend = false;
-                            } else {
-                                cur = p - 1;
-                            }
-                        }
-                    }
-                    // step k places item src(k) = (k == 0 ? incoming : f(k - 1)) at chain[k];
-                    // step h places f(h - 1) at the final slot (or drops it)
-                    const int srck_l = __shfl_up_sync(FULLM, res, 1);
-                    const int src_here = lane == 0 ? -1 : srck_l;
-                    const int src_final = h == 0 ? -1 : __shfl_sync(FULLM, res, (h - 1) & 31);
-                    auto content = [&](int src, uint32_t& c1, uint32_t& c2, uint64_t& cst, int64_t& corg) {
-                        const int sl = src < 0 ? 0 : src;
-                        const uint32_t x1 = __shfl_sync(FULLM, my_b1, sl), x2 = __shfl_sync(FULLM, my_b2, sl);
-                        const uint64_t xs = __shfl_sync(FULLM, my_st, sl);
-                        const int64_t xo = __shfl_sync(FULLM, my_pre_org, sl);
-                        if (src < 0) {
-                            c1 = b1;
-                            c2 = b2;
-                            cst = stamp;
-                            corg = int64_t(i);
-                        } else {
-                            c1 = x1;
-                            c2 = x2;
-                            cst = xs;
-                            corg = xo;
-                        }
-                    };
-                    uint32_t c1, c2;
-                    uint64_t cst;
-                    int64_t corg;
-                    content(src_here, c1, c2, cst, corg);
-                    if (lane < h && above == 0) {  // last visit of chain[lane]: its final content
-                        d.beta1[my_v] = c1;
-                        d.beta2[my_v] = c2;
-                        d.stamp[my_v] = cst;
-                        d.fifo[cst & fmask] = int64_t(my_v);
-                        touch_store(my_v, corg);
-                    }
-                    content(src_final, c1, c2, cst, corg);
-                    if (lane == 0) {
-                        if (final_slot == FULLM) {
-                            d.fifo[cst & fmask] = -1;  // the dropped item leaves the FIFO
-                        } else {
-                            d.beta1[final_slot] = c1;
-                            d.beta2[final_slot] = c2;
-                            d.stamp[final_slot] = cst;
-                            d.fifo[cst & fmask] = int64_t(final_slot);
-                            touch_store(final_slot, corg);
-                        }
-                    }
-                    __syncwarp();
-                } else {
-                // ---- resolve a long chain through global scratch ----------------
-                uint64_t* pre = d.chain_pre;  // [3 * X_CHAIN]: (b1 | b2 << 32), stamp, origin
-                for (uint32_t k = lane; k < h; k += 32) {
-                    const uint32_t v = chain[k];
-                    pre[3 * k] = uint64_t(d.beta1[v]) | uint64_t(d.beta2[v]) << 32;
-                    pre[3 * k + 1] = d.stamp[v];
-                    const int64_t o = d.origin[v];
-                    pre[3 * k + 2] = uint64_t(d.touched_mark[v] == s.batch_id ? o : -int64_t(v) - 2);
-                    uint16_t p = NONE16;
-                    for (int32_t q = int32_t(k) - 1; q >= 0; --q)
-                        if (chain[q] == v) {
-                            p = uint16_t(q);
-                            break;
-                        }
-                    prevk[k] = p;
-                }
-                __syncwarp();
-                // src[k]: the item placed at step k (NONE16 = the incoming one, j = pre-content of chain[j])
-                if (lane == 0) {
-                    srck[0] = NONE16;
-                    for (uint32_t k = 0; k < h; ++k) srck[k + 1] = prevk[k] != NONE16 ? srck[prevk[k]] : uint16_t(k);
-                }
-                __syncwarp();
-                for (uint32_t k = lane; k <= h; k += 32) {
-                    const uint16_t src = srck[k];
-                    uint32_t slot;
-                    if (k < h) {
-                        slot = chain[k];
-                        bool last = true;
-                        for (uint32_t q = k + 1; q < h && last; ++q) last = chain[q] != slot;
-                        if (!last) continue;
-                    } else {
-                        slot = final_slot;
-                    }
-                    uint32_t c1 = b1, c2 = b2;
-                    uint64_t cst = stamp;
-                    int64_t corg = int64_t(i);
-                    if (src != NONE16) {
-                        const uint64_t bb = pre[3 * src];
-                        c1 = uint32_t(bb);
-                        c2 = uint32_t(bb >> 32);
-                        cst = pre[3 * src + 1];
-                        corg = int64_t(pre[3 * src + 2]);
-                    }
-                    if (slot == FULLM) {  // the dropped item leaves the FIFO
-                        d.fifo[cst & fmask] = -1;
-                        continue;
-                    }
-                    d.beta1[slot] = c1;
-                    d.beta2[slot] = c2;
-                    d.stamp[slot] = cst;
-                    d.fifo[cst & fmask] = int64_t(slot);
-                    touch_store(slot, corg);
-                }
-                __syncwarp();
-                }
+                // the chain's metadata is resolved later (before the next chain or at the
+                // end of the launch), so its prefetches have long landed by then
+                pend_chain = true;
+                p_h = h;
+                p_final = final_slot;
+                p_b1 = b1;
+                p_b2 = b2;
+                p_stamp = stamp;
+                p_i = i;
             }
             if (reports && lane == 0) reinterpret_cast<uint4*>(reports)[i] = make_uint4(1, dropped, gc, disp);
             return true;
@@ -491,6 +524,7 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 }
             }
         }
+        resolve_pending();
         s.resume_at = c;
         if (lane == 0) *gst = s;
         __threadfence_block();
