@@ -83,12 +83,18 @@ __device__ __forceinline__ void tm_wait_ld8(uint32_t (&v)[8]) {
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 // query words: read once per CTA, reused through L2 by the other column tiles
-__device__ __forceinline__ uint4 ldg_q(const uint8_t* p) {
+// (evict_last: the ~128 CTAs of a segment re-read each set from L2, not DRAM)
+__device__ __forceinline__ uint4 ldg_q(const uint8_t* p, uint64_t pol) {
     uint4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];\n"
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;\n"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
+                 : "l"(p), "l"(pol));
     return v;
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
 }
 
 }  // namespace
@@ -170,11 +176,12 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                 cp_async16(dst + tid * 16, src, ok ? 16u : 0u);
             }
         };
+        const uint64_t qpol = l2_evict_last_policy();
         auto load_q = [&](uint32_t j, uint4 (&w)[NQ]) {
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const uint32_t r4 = r_base + 4 * uint32_t(q * Q_NT + tid);
-                w[q] = r4 < qstride ? ldg_q(qT + uint64_t(j) * 4 * qstride + uint64_t(r4) * 4) : make_uint4(0, 0, 0, 0);
+                w[q] = r4 < qstride ? ldg_q(qT + uint64_t(j) * 4 * qstride + uint64_t(r4) * 4, qpol) : make_uint4(0, 0, 0, 0);
             }
         };
         auto build = [&](int buf, int tb) {
