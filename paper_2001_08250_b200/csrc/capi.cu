@@ -453,7 +453,7 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
         // B >= 2048: quad tables (8) or the half-TMEM 128-byte-column kernel (2 -> 5),
         // whichever the sweep-calibrated cost model says is faster for this B
         if (q_ok && B >= g_q_min_batch) {
-            const double c5 = m4_ok ? double((uint64_t(B) + 2047) / 2048 * 2048) / 3.12 : 1e300;
+            const double c5 = m4_ok ? double((uint64_t(B) + 2047) / 2048 * 2048) / 3.0 : 1e300;
             return m4rm_q_cost(B, nullptr) < c5 ? 8 : 2;
         }
         k = !m4_ok ? 1 : B >= g_m4_min_batch ? 2 : B >= g_k4_min_batch ? 7 : B >= g_nib_min_batch ? 6 : 1;

@@ -20,7 +20,7 @@
 //    (tcgen05.ld/st .32x32b.x8), read-modify-written once per set (4 groups),
 //    so TMEM traffic is half the lookup bytes. Rc = 8192 requests per tile.
 //  * Shared-memory wavefronts per set (per SM, Rc = 8192): 8192 lookups,
-//    384 table build (4 tables x 256 rows x 32 B + bucket reads), 256 query
+//    320 table build (4 tables x 256 rows x 32 B + bucket reads), 256 query
 //    index loads, 8 bucket fills: lookups are 93% of the pipe (the 128-byte
 //    column kernel: 82%), because the table build is amortised over 4x more
 //    requests and each index byte now serves 32 bytes of lookup instead of 16.
@@ -135,8 +135,7 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
     const uint32_t dhalf = (i8 & 1) ? 0xfffffff0u : 16u;  // address of the other half: +16 / -16
     // build constants: lane -> (table bt, 32-bit word bw); warp -> high nibble of the row
     const int bt = lane >> 3, bw = lane & 7;
-    const uint32_t hm0 = 0u - (warp & 1u), hm1 = 0u - ((warp >> 1) & 1u), hm2 = 0u - ((warp >> 2) & 1u),
-                   hm3 = 0u - ((warp >> 3) & 1u);
+    const uint32_t hm0 = 0u - (warp & 1u), hm1 = 0u - ((warp >> 1) & 1u), hm2 = 0u - ((warp >> 2) & 1u);
 
     const uint32_t n_rtiles = (B + C::RC - 1) / C::RC;
     const uint64_t units = uint64_t(n_ctiles) * n_rtiles * n_seg;
@@ -184,18 +183,25 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                 w[q] = r4 < qstride ? ldg_q(qT + uint64_t(j) * 4 * qstride + uint64_t(r4) * 4, qpol) : make_uint4(0, 0, 0, 0);
             }
         };
+        // Warps 0-7 build (warp w: the rows with high nibble w, then w + 8 — the same
+        // 8 bucket words serve both), so the bucket words are read by 8 warps, not 16.
         auto build = [&](int buf, int tb) {
+            if (warp >= 8) return;
             const uint32_t src = sbase + C::OFF_STG + buf * C::STG + bt * 32 + bw * 4;
             uint32_t b[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) b[i] = lds32(src + i * 128);
-            uint32_t h = (b[4] & hm0) ^ (b[5] & hm1) ^ (b[6] & hm2) ^ (b[7] & hm3);
-            const uint32_t row0 = sbase + tb * Q_TAB + uint32_t(warp << 4) * 128 + bt * 32 + bw * 4;
-            sts32(row0, h);
+            uint32_t h = (b[4] & hm0) ^ (b[5] & hm1) ^ (b[6] & hm2);
 #pragma unroll
-            for (int m = 1; m < 16; ++m) {
-                h ^= b[(m & 1) ? 0 : (m & 2) ? 1 : (m & 4) ? 2 : 3];  // ctz(m)
-                sts32(row0 + uint32_t(m ^ (m >> 1)) * 128, h);
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t row0 = sbase + tb * Q_TAB + uint32_t((warp + 8 * half) << 4) * 128 + bt * 32 + bw * 4;
+                uint32_t x = half ? h ^ b[7] : h;
+                sts32(row0, x);
+#pragma unroll
+                for (int m = 1; m < 16; ++m) {
+                    x ^= b[(m & 1) ? 0 : (m & 2) ? 1 : (m & 4) ? 2 : 3];  // ctz(m)
+                    sts32(row0 + uint32_t(m ^ (m >> 1)) * 128, x);
+                }
             }
         };
         auto lookups = [&](const uint4 (&wq)[NQ], int tb) {
@@ -322,12 +328,12 @@ cudaError_t launch_q(const M4Args& a, int num_sms) {
 }  // namespace
 
 // Modelled time of a batch (arbitrary units: padded requests / measured
-// efficiency) for each tile size; the efficiencies are the config-5 sweep's
-// fractions of the dense-ALU roofline at full tiles (profiles/r01_config5_sweep*):
-// 2048 -> 2.65, 4096 -> 3.02, 8192 -> 3.33 (the half-TMEM 128-byte-column kernel: 3.12).
+// efficiency) for each tile size; the efficiencies are measured fractions of the
+// dense-ALU roofline at full tiles on a 1 GiB store (prof_m4rm_tiles.py):
+// 2048 -> 2.89, 4096 -> 3.21, 8192 -> 3.38 (the half-TMEM 128-byte-column kernel: 3.0).
 double m4rm_q_cost(uint32_t B, int* tile) {
     static const int rcs[3] = {2048, 4096, 8192};
-    static const double eff[3] = {2.65, 3.02, 3.33};
+    static const double eff[3] = {2.89, 3.21, 3.38};
     double best = 1e300;
     int best_rc = 2048;
     for (int k = 0; k < 3; ++k) {
