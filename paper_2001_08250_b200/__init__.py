@@ -181,6 +181,15 @@ def lib() -> C.CDLL:
     return _lib
 
 
+def _destroy(fn) -> None:
+    """Release a handle; quietly skipped while the interpreter is shutting down
+    (module globals may already be gone when __del__ runs)."""
+    try:
+        fn()
+    except Exception:  # noqa: BLE001
+        pass
+
+
 def _check(rc: int) -> int:
     if rc >= 0:
         return rc
@@ -274,7 +283,7 @@ class DeviceBuffer:
 
     def close(self):
         if getattr(self, "ptr", None):
-            lib().xpir_dev_free(self.device, self.ptr)
+            _destroy(lambda: lib().xpir_dev_free(self.device, self.ptr))
             self.ptr = None
 
     __del__ = close
@@ -315,7 +324,7 @@ class Store:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().xpir_store_destroy(self.h)
+            _destroy(lambda: lib().xpir_store_destroy(self.h))
             self.h = None
 
     __del__ = close
@@ -431,7 +440,7 @@ class Batcher:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().xpir_batcher_destroy(self.h)
+            _destroy(lambda: lib().xpir_batcher_destroy(self.h))
             self.h = None
 
     __del__ = close
@@ -569,7 +578,7 @@ class Table:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().xpir_table_destroy(self.h)
+            _destroy(lambda: lib().xpir_table_destroy(self.h))
             self.h = None
 
     __del__ = close
@@ -662,7 +671,7 @@ class Window:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().xpir_window_destroy(self.h)
+            _destroy(lambda: lib().xpir_window_destroy(self.h))
             self.h = None
 
     __del__ = close
@@ -796,7 +805,7 @@ class Server:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().xpir_server_destroy(self.h)
+            _destroy(lambda: lib().xpir_server_destroy(self.h))
             self.h = None
 
     __del__ = close
