@@ -277,10 +277,17 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                 uint8_t* o = base + uint64_t(r) * S + uint64_t(c) * 32;
                 uint8_t* oa = o + 16 * (i8 & 1);
                 uint8_t* ob = o + 16 * ((i8 & 1) ^ 1);
-                red_xor64(oa, uint64_t(m[1]) << 32 | m[0]);
-                red_xor64(oa + 8, uint64_t(m[3]) << 32 | m[2]);
-                red_xor64(ob, uint64_t(m[5]) << 32 | m[4]);
-                red_xor64(ob + 8, uint64_t(m[7]) << 32 | m[6]);
+                if (peers.n) {  // the owner's rows take every rank's partials: system-scope RMWs
+                    red_xor64_sys(oa, uint64_t(m[1]) << 32 | m[0]);
+                    red_xor64_sys(oa + 8, uint64_t(m[3]) << 32 | m[2]);
+                    red_xor64_sys(ob, uint64_t(m[5]) << 32 | m[4]);
+                    red_xor64_sys(ob + 8, uint64_t(m[7]) << 32 | m[6]);
+                } else {
+                    red_xor64(oa, uint64_t(m[1]) << 32 | m[0]);
+                    red_xor64(oa + 8, uint64_t(m[3]) << 32 | m[2]);
+                    red_xor64(ob, uint64_t(m[5]) << 32 | m[4]);
+                    red_xor64(ob + 8, uint64_t(m[7]) << 32 | m[6]);
+                }
             }
         }
     }

@@ -283,8 +283,13 @@ k_scan_m4rm_tmem(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const 
                         // owner rank's answer buffer (NVLink peer atomics); otherwise locally
                         uint8_t* const base = peers.n ? peers.owner_out(r_base + rl) : out;
                         uint8_t* o = base + uint64_t(r_base + rl) * S + uint64_t(c) * 128 + l8 * 16;
-                        red_xor64(o, uint64_t(v[k].y) << 32 | v[k].x);
-                        red_xor64(o + 8, uint64_t(v[k].w) << 32 | v[k].z);
+                        if (peers.n) {  // rows every rank reduces into: system-scope RMWs
+                            red_xor64_sys(o, uint64_t(v[k].y) << 32 | v[k].x);
+                            red_xor64_sys(o + 8, uint64_t(v[k].w) << 32 | v[k].z);
+                        } else {
+                            red_xor64(o, uint64_t(v[k].y) << 32 | v[k].x);
+                            red_xor64(o + 8, uint64_t(v[k].w) << 32 | v[k].z);
+                        }
                     }
                 }
             }

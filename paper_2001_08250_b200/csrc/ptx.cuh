@@ -37,9 +37,14 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;\n" ::"r"(addr), "r"(v));
 }
-// 64-bit XOR reduction into global memory (local or NVLink peer address).
+// 64-bit XOR reduction into this GPU's global memory.
 __device__ __forceinline__ void red_xor64(void* p, uint64_t v) {
     asm volatile("red.relaxed.gpu.global.xor.b64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+// The same into memory other GPUs also reduce into (NVLink peer rows of the fused
+// cross-GPU reduce): system scope, so the RMWs of all GPUs are atomic together.
+__device__ __forceinline__ void red_xor64_sys(void* p, uint64_t v) {
+    asm volatile("red.relaxed.sys.global.xor.b64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
 }
 
 }  // namespace ptx
