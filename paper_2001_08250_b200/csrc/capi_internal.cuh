@@ -1,0 +1,214 @@
+// Internal header of the C-ABI TUs (capi*.cu): shared host helpers and the
+// handle structs behind include/xpir.h. Not part of the public interface.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/xpir.h"
+#include "prims.cuh"
+#include "scan.cuh"
+
+namespace xpir {
+void count_launches(uint64_t n);
+int set_error(int code, const std::string& msg);
+namespace capi {
+int fail(int code, const std::string& msg);   // sets the thread's xpir_last_error()
+const std::string& last_error_message();
+extern std::atomic<int> g_last_kernel;
+extern xpir_scan_opts g_opts;
+extern std::mutex g_opts_mu;
+}  // namespace capi
+}  // namespace xpir
+
+using namespace xpir;
+using xpir::capi::fail;
+
+namespace xpir {
+namespace capi {
+
+#define XCK(expr)                                                                       \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(XPIR_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+inline int num_sms(int dev) {
+    static int cache[64] = {0};
+    if (dev >= 0 && dev < 64 && cache[dev]) return cache[dev];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < 64) cache[dev] = n;
+    return n;
+}
+
+// Grow-only device scratch buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t n) {
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(n, size_t(256));
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+inline uint64_t round16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+
+// Host BLAKE2b (same algorithm as the device port in prims.cuh), incremental,
+// used for the digests that the reference computes over whole tables/windows.
+struct HostBlake2b {
+    uint64_t h[8];
+    uint64_t t = 0;
+    uint8_t buf[128];
+    size_t buflen = 0, outlen;
+    explicit HostBlake2b(size_t out) : outlen(out) {
+        for (int i = 0; i < 8; ++i) h[i] = b2_iv(i);
+        h[0] ^= 0x01010000ULL ^ out;
+    }
+    void block(bool last) {
+        uint64_t m[16];
+        for (int i = 0; i < 16; ++i) m[i] = ld64le(buf + 8 * i);
+        blake2b_compress(h, m, t, 0, last);
+    }
+    void update(const uint8_t* in, size_t len) {
+        while (len) {
+            if (buflen == 128) {
+                t += 128;
+                block(false);
+                buflen = 0;
+            }
+            size_t take = std::min(len, 128 - buflen);
+            std::memcpy(buf + buflen, in, take);
+            buflen += take;
+            in += take;
+            len -= take;
+        }
+    }
+    void update_u64be(uint64_t v) {
+        uint8_t b[8];
+        for (int i = 0; i < 8; ++i) b[i] = uint8_t(v >> (56 - 8 * i));
+        update(b, 8);
+    }
+    void final(uint8_t* out) {
+        t += buflen;
+        std::memset(buf + buflen, 0, 128 - buflen);
+        block(true);
+        uint8_t full[64];
+        for (int i = 0; i < 8; ++i)
+            for (int k = 0; k < 8; ++k) full[8 * i + k] = uint8_t(h[i] >> (8 * k));
+        std::memcpy(out, full, outlen);
+    }
+};
+
+}  // namespace capi
+}  // namespace xpir
+using namespace xpir::capi;
+
+// ---- handle structs ------------------------------------------------------
+struct xpir_store {
+    int device;
+    uint32_t N, S, lo, hi;
+    uint64_t epoch = 0;
+    uint8_t* data = nullptr;
+    cudaStream_t stream = nullptr;
+    DevBuf q, out, seeds, masks, qwin, qx, idx;
+    std::mutex mu;
+    // Query-window scratch of the device-pointer entry points, one per caller
+    // stream, so calls on different streams may run concurrently (read batcher).
+    std::mutex scratch_mu;
+    std::vector<std::pair<cudaStream_t, DevBuf*>> qwin_by_stream;
+    DevBuf& qwin_for(cudaStream_t s) {
+        if (s == stream) return qwin;
+        std::lock_guard<std::mutex> lk(scratch_mu);
+        for (auto& e : qwin_by_stream)
+            if (e.first == s) return *e.second;
+        qwin_by_stream.emplace_back(s, new DevBuf);
+        return *qwin_by_stream.back().second;
+    }
+    uint32_t nb() const { return hi - lo; }
+    uint64_t bytes() const { return uint64_t(nb()) * S; }
+    uint64_t byte_lo() const { return lo / 8; }
+    uint64_t nbytes_window() const { return (uint64_t(hi) + 7) / 8 - lo / 8; }
+};
+
+struct xpir_table {
+    int device;
+    uint8_t seed[32];
+    CuckooDev d{};
+    CuckooState h{};
+    CuckooState* dstate = nullptr;
+    uint8_t* data = nullptr;  // payloads of buckets [lo, hi)
+    uint32_t lo = 0, hi = 0;  // a payload shard of the logical table (metadata is whole)
+    cudaStream_t stream = nullptr;
+    DevBuf in_b1, in_b2, in_payload, in_reports, gather;
+    CuckooParScratch par;
+    bool parallel_prefix = true;  // XPIR_CUCKOO_SEQUENTIAL=1 disables (A/B checks)
+    std::mutex mu;
+    uint64_t slots() const { return uint64_t(d.buckets) * d.depth; }
+    uint64_t data_bytes() const { return uint64_t(hi - lo) * d.depth * d.item; }
+    bool sharded() const { return lo != 0 || hi != d.buckets; }
+};
+
+struct xpir_window {
+    int device;
+    uint32_t m, h, w;
+    uint64_t base = 0;
+    uint64_t words;
+    std::deque<unsigned long long*> deltas;
+    cudaStream_t stream = nullptr;
+    DevBuf pos, seqs, scratch, enc;
+    std::mutex mu;
+};
+
+struct xpir_server {
+    int device;
+    xpir_table* table = nullptr;
+    xpir_window* window = nullptr;
+    uint32_t rotate_writes, epoch_ring;
+    uint64_t writes = 0, latest_epoch = 0;
+    struct Sealed {
+        uint64_t epoch;
+        uint32_t since_batch;  // table batch id the image is synchronised with
+        xpir_store* st;
+    };
+    std::deque<Sealed> ring;  // oldest first
+    std::mutex mu;
+};
+

@@ -1,0 +1,337 @@
+// C-ABI (include/xpir.h): the blocked cuckoo table — cuckoo::Table (cuckoo.hpp:37-84, cuckoo.cpp).
+#include "capi_internal.cuh"
+
+// ===========================================================================
+// cuckoo table
+// ===========================================================================
+
+static const uint32_t DRAW_CAP = 1u << 16;
+
+static void table_free_all(xpir_table* t) {
+    cudaFree(t->d.used);
+    cudaFree(t->d.beta1);
+    cudaFree(t->d.beta2);
+    cudaFree(t->d.stamp);
+    cudaFree(t->d.origin);
+    cudaFree(t->d.touched_mark);
+    cudaFree(t->d.touched);
+    cudaFree(t->d.mod_batch);
+    cudaFree(t->d.chain_pre);
+    cudaFree(t->d.fifo);
+    cudaFree(t->d.draws);
+    cudaFree(t->dstate);
+    cudaFree(t->data);
+    t->in_b1.release();
+    t->in_b2.release();
+    t->in_payload.release();
+    t->in_reports.release();
+    t->gather.release();
+    t->par.release();
+    if (t->stream) cudaStreamDestroy(t->stream);
+}
+
+extern "C" {
+
+int xpir_table_create(int device, uint32_t buckets, uint32_t depth, uint64_t capacity,
+                      uint64_t item_size, const uint8_t seed[32], xpir_table** out) {
+    return xpir_table_create_shard(device, buckets, depth, capacity, item_size, seed, 0, buckets, out);
+}
+
+int xpir_table_create_shard(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
+                            const uint8_t seed[32], uint32_t lo, uint32_t hi, xpir_table** out) {
+    if (!out || !seed) return fail(XPIR_EINVAL, "table_create: null argument");
+    if (buckets == 0 || depth == 0 || item_size == 0)  // cuckoo.cpp:15-16
+        return fail(XPIR_EINVAL, "cuckoo: table dimensions must be positive");
+    if (capacity == 0 || capacity > uint64_t(buckets) * depth)  // cuckoo.cpp:17-18
+        return fail(XPIR_EINVAL, "cuckoo: capacity must be in [1, buckets*depth]");
+    if (uint64_t(buckets) * depth >= (uint64_t(1) << 32))
+        return fail(XPIR_EINVAL, "cuckoo: more than 2^32 slots");
+    if (lo >= hi || hi > buckets) return fail(XPIR_EINVAL, "table_create: bad shard bucket range");
+    int ndev = 0;
+    XCK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(XPIR_EINVAL, "table_create: bad device");
+    DeviceGuard g(device);
+    auto* t = new xpir_table;
+    t->device = device;
+    std::memcpy(t->seed, seed, 32);
+    t->d.buckets = buckets;
+    t->d.depth = depth;
+    t->d.capacity = capacity;
+    t->d.item = item_size;
+    const uint64_t slots = t->slots();
+    uint64_t fc = 1;
+    while (fc < 2 * slots + 1024) fc <<= 1;
+    t->d.fifo_cap = fc;
+    t->d.draw_cap = DRAW_CAP;
+    cudaError_t e = cudaSuccess;
+    auto M = [&](void** p, size_t n) {
+        if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(n, 16));
+        if (e == cudaSuccess) e = cudaMemset(*p, 0, std::max<size_t>(n, 16));
+    };
+    M(reinterpret_cast<void**>(&t->d.used), slots);
+    M(reinterpret_cast<void**>(&t->d.beta1), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.beta2), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.stamp), 8 * slots);
+    M(reinterpret_cast<void**>(&t->d.origin), 8 * slots);
+    M(reinterpret_cast<void**>(&t->d.touched_mark), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.touched), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.mod_batch), 4 * slots);
+    M(reinterpret_cast<void**>(&t->d.chain_pre), 8 * 3 * 512);
+    M(reinterpret_cast<void**>(&t->d.fifo), 8 * fc);
+    M(reinterpret_cast<void**>(&t->d.draws), 8 * uint64_t(DRAW_CAP));
+    M(reinterpret_cast<void**>(&t->dstate), sizeof(CuckooState));
+    t->lo = lo;
+    t->hi = hi;
+    M(reinterpret_cast<void**>(&t->data), uint64_t(hi - lo) * depth * item_size);
+    if (e == cudaSuccess) e = cudaMemset(t->d.fifo, 0xff, 8 * fc);  // -1: no entry
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        table_free_all(t);
+        delete t;
+        return fail(e == cudaErrorMemoryAllocation ? XPIR_ENOMEM : XPIR_ECUDA,
+                    std::string("table_create: ") + cudaGetErrorString(e));
+    }
+    t->h = CuckooState{};
+    if (const char* ev = std::getenv("XPIR_CUCKOO_SEQUENTIAL")) t->parallel_prefix = ev[0] != '1';
+    *out = t;
+    return XPIR_OK;
+}
+
+int xpir_table_destroy(xpir_table* t) {
+    if (!t) return XPIR_OK;
+    DeviceGuard g(t->device);
+    cudaStreamSynchronize(t->stream);
+    table_free_all(t);
+    delete t;
+    return XPIR_OK;
+}
+
+int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2,
+                                const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
+                                void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+    if (n == 0) return XPIR_OK;
+    if (!d_b1 || !d_b2 || !d_payload) return fail(XPIR_EINVAL, "table_insert: null buffer");
+    if (t->sharded())
+        return fail(XPIR_EINVAL, "table_insert: payload shard: use insert_walk + apply_gather (all shards) + apply_scatter");
+    int rc = xpir_table_insert_walk_dev(t, d_b1, d_b2, n, d_reports, stream);
+    if (rc) return rc;
+    rc = xpir_table_apply_gather_dev(t, nullptr, stream);
+    if (rc) return rc;
+    return xpir_table_apply_scatter_dev(t, d_payload, stream);
+}
+
+int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n,
+                               uint32_t* d_reports, void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    t->h.batch_id += 1;
+    t->h.n_touched = 0;
+    uint64_t i = 0;
+    // K6a: the eviction-free, GC-free prefix of the round is placed in parallel
+    // (exactly what the sequential walk would do); the walk continues from the
+    // first insert that needs an eviction or a FIFO GC.
+    if (t->parallel_prefix && n >= 64 && t->h.live < t->d.capacity) {
+        const uint64_t room = t->d.capacity - t->h.live;
+        uint64_t applied = 0;
+        XCK(cuckoo_parallel_prefix(t->d, t->h, d_b1, d_b2, n < room ? n : room, d_reports, t->par, &applied, s));
+        i = applied;
+    }
+    for (int guard = 0; i < n; ++guard) {
+        if (t->h.rng_block + 1024 > t->h.draw_base + t->h.draw_count || guard == 0) {
+            // (re)fill the draw window starting at the next unconsumed nonce
+            t->h.draw_base = t->h.rng_block;
+            t->h.draw_count = DRAW_CAP;
+            XCK(launch_draws(t->seed, t->h.draw_base, DRAW_CAP, t->d.draws, s));
+            count_launches(1);
+        }
+        XCK(cudaMemcpyAsync(t->dstate, &t->h, sizeof(CuckooState), cudaMemcpyHostToDevice, s));
+        XCK(launch_cuckoo_walk(t->d, t->dstate, d_b1, d_b2, i, n, d_reports, s));
+        count_launches(1);
+        XCK(cudaMemcpyAsync(&t->h, t->dstate, sizeof(CuckooState), cudaMemcpyDeviceToHost, s));
+        XCK(cudaStreamSynchronize(s));
+        if (t->h.status == 2) return fail(XPIR_ESTATE, "table_insert: FIFO ring overflow");
+        if (t->h.resume_at <= i && t->h.status != 1)
+            return fail(XPIR_ESTATE, "table_insert: walk made no progress");
+        i = t->h.resume_at;
+        if (t->h.status == 1) t->h.draw_count = 0;  // force a refill
+    }
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_table_apply_gather_dev(xpir_table* t, const xpir_shard_map* map, void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_apply: null table");
+    ShardMap m{};
+    if (map) {
+        if (map->n > 8) return fail(XPIR_EINVAL, "table_apply: at most 8 shards");
+        m.n = map->n;
+        for (uint32_t k = 0; k <= map->n; ++k) m.lo[k] = map->bucket_lo[k];
+        for (uint32_t k = 0; k < map->n; ++k) m.data[k] = map->data[k];
+        if (m.n && (m.lo[0] != 0 || m.lo[m.n] != t->d.buckets))
+            return fail(XPIR_EINVAL, "table_apply: shard map must cover every bucket");
+    } else if (t->sharded()) {
+        return fail(XPIR_EINVAL, "table_apply: a payload shard needs the shard map");
+    }
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    XCK(t->gather.ensure(uint64_t(t->h.n_touched) * t->d.item));
+    t->d.gather = t->gather.as<uint8_t>();
+    XCK(launch_cuckoo_gather_sharded(t->d, &t->h, t->lo, t->hi, t->data, m, s));
+    count_launches(1);
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_table_apply_scatter_dev(xpir_table* t, const uint8_t* d_payload, void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_apply: null table");
+    if (t->h.n_touched && !d_payload) return fail(XPIR_EINVAL, "table_apply: null payload");
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    XCK(launch_cuckoo_scatter_sharded(t->d, &t->h, t->lo, t->hi, t->data, d_payload, s));
+    count_launches(1);
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+int xpir_table_shard(const xpir_table* t, uint32_t* lo, uint32_t* hi) {
+    if (!t) return fail(XPIR_EINVAL, "table_shard: null table");
+    if (lo) *lo = t->lo;
+    if (hi) *hi = t->hi;
+    return XPIR_OK;
+}
+
+int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b2,
+                            const uint8_t* payload, uint64_t n, uint32_t* reports) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+    if (n == 0) return XPIR_OK;
+    if (!b1 || !b2 || !payload) return fail(XPIR_EINVAL, "table_insert: null buffer");
+    // cuckoo.cpp:57-58 — validated per item in order; items before the bad one
+    // are inserted, exactly as a loop of Table::insert calls would leave them.
+    uint64_t ok = n;
+    for (uint64_t k = 0; k < n; ++k)
+        if (b1[k] >= t->d.buckets || b2[k] >= t->d.buckets) {
+            ok = k;
+            break;
+        }
+    std::lock_guard<std::mutex> lk(t->mu);
+    DeviceGuard g(t->device);
+    cudaStream_t s = t->stream;
+    if (ok > 0) {
+        XCK(t->in_b1.ensure(4 * ok));
+        XCK(t->in_b2.ensure(4 * ok));
+        XCK(t->in_payload.ensure(ok * t->d.item));
+        XCK(t->in_reports.ensure(16 * ok));
+        XCK(cudaMemcpyAsync(t->in_b1.p, b1, 4 * ok, cudaMemcpyHostToDevice, s));
+        XCK(cudaMemcpyAsync(t->in_b2.p, b2, 4 * ok, cudaMemcpyHostToDevice, s));
+        XCK(cudaMemcpyAsync(t->in_payload.p, payload, ok * t->d.item, cudaMemcpyHostToDevice, s));
+        int rc = xpir_table_insert_batch_dev(t, t->in_b1.as<uint32_t>(), t->in_b2.as<uint32_t>(),
+                                             t->in_payload.as<uint8_t>(), ok,
+                                             t->in_reports.as<uint32_t>(), s);
+        if (rc) return rc;
+        if (reports)
+            XCK(cudaMemcpyAsync(reports, t->in_reports.p, 16 * ok, cudaMemcpyDeviceToHost, s));
+        XCK(cudaStreamSynchronize(s));
+    }
+    if (ok < n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
+    return XPIR_OK;
+}
+
+int xpir_table_reserve(xpir_table* t, uint64_t max_batch) {
+    if (!t) return fail(XPIR_EINVAL, "table_reserve: null table");
+    std::lock_guard<std::mutex> lk(t->mu);
+    DeviceGuard g(t->device);
+    const uint64_t n = std::min<uint64_t>(max_batch, t->slots());
+    XCK(t->gather.ensure(n * t->d.item));
+    XCK(t->in_b1.ensure(4 * max_batch));
+    XCK(t->in_b2.ensure(4 * max_batch));
+    XCK(t->in_reports.ensure(16 * max_batch));
+    XCK(cuckoo_reserve(t->par, max_batch, t->d.buckets, t->stream));  // claim-sort scratch
+    XCK(cudaStreamSynchronize(t->stream));
+    return XPIR_OK;
+}
+
+int xpir_table_snapshot(const xpir_table* t, uint8_t* host_out) {
+    if (!t || !host_out) return fail(XPIR_EINVAL, "table_snapshot: null argument");
+    DeviceGuard g(t->device);
+    XCK(cudaStreamSynchronize(t->stream));
+    XCK(cudaMemcpy(host_out, t->data, t->data_bytes(), cudaMemcpyDeviceToHost));
+    return XPIR_OK;
+}
+
+void* xpir_table_device_data(const xpir_table* t) { return t ? t->data : nullptr; }
+
+int xpir_table_seal(const xpir_table* t, xpir_store* st, uint64_t epoch, void* stream) {
+    if (!t || !st) return fail(XPIR_EINVAL, "table_seal: null argument");
+    if (st->N != t->d.buckets || uint64_t(st->S) != uint64_t(t->d.depth) * t->d.item)
+        return fail(XPIR_EINVAL, "table_seal: store geometry differs from the table");
+    if (st->device != t->device) return fail(XPIR_EINVAL, "table_seal: different devices");
+    if (st->lo < t->lo || st->hi > t->hi) return fail(XPIR_EINVAL, "table_seal: store range outside the payload shard");
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    XCK(cudaMemcpyAsync(st->data, t->data + uint64_t(st->lo - t->lo) * st->S, st->bytes(),
+                        cudaMemcpyDeviceToDevice, s));
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    st->epoch = epoch;
+    return XPIR_OK;
+}
+
+int xpir_table_meta(const xpir_table* t, uint8_t* used, uint32_t* b1, uint32_t* b2,
+                    uint64_t* stamp) {
+    if (!t) return fail(XPIR_EINVAL, "table_meta: null table");
+    DeviceGuard g(t->device);
+    XCK(cudaStreamSynchronize(t->stream));
+    const uint64_t n = t->slots();
+    if (used) XCK(cudaMemcpy(used, t->d.used, n, cudaMemcpyDeviceToHost));
+    if (b1) XCK(cudaMemcpy(b1, t->d.beta1, 4 * n, cudaMemcpyDeviceToHost));
+    if (b2) XCK(cudaMemcpy(b2, t->d.beta2, 4 * n, cudaMemcpyDeviceToHost));
+    if (stamp) XCK(cudaMemcpy(stamp, t->d.stamp, 8 * n, cudaMemcpyDeviceToHost));
+    return XPIR_OK;
+}
+
+int xpir_table_counters(const xpir_table* t, uint64_t* writes, uint64_t* live, uint64_t* next_stamp) {
+    if (!t) return fail(XPIR_EINVAL, "table_counters: null table");
+    if (writes) *writes = t->h.writes;
+    if (live) *live = t->h.live;
+    if (next_stamp) *next_stamp = t->h.next_stamp;
+    return XPIR_OK;
+}
+
+int xpir_table_slot_used(const xpir_table* t, uint32_t bucket, uint32_t slot) {
+    if (!t || bucket >= t->d.buckets || slot >= t->d.depth)
+        return fail(XPIR_EINVAL, "slot_used: out of range");
+    DeviceGuard g(t->device);
+    uint8_t u = 0;
+    XCK(cudaStreamSynchronize(t->stream));
+    XCK(cudaMemcpy(&u, t->d.used + uint64_t(bucket) * t->d.depth + slot, 1, cudaMemcpyDeviceToHost));
+    return u ? 1 : 0;
+}
+
+int xpir_table_state_digest(const xpir_table* t, uint8_t out[32]) {
+    if (!t || !out) return fail(XPIR_EINVAL, "state_digest: null argument");
+    if (t->sharded()) return fail(XPIR_EINVAL, "state_digest: needs the whole table (this is a payload shard)");
+    const uint64_t n = t->slots();
+    std::vector<uint8_t> data(n * t->d.item), used(n);
+    std::vector<uint32_t> b1(n), b2(n);
+    std::vector<uint64_t> st(n);
+    int rc = xpir_table_snapshot(t, data.data());
+    if (rc) return rc;
+    rc = xpir_table_meta(t, used.data(), b1.data(), b2.data(), st.data());
+    if (rc) return rc;
+    HostBlake2b h(32);  // cuckoo.cpp:137-149
+    h.update_u64be(t->h.writes);
+    h.update_u64be(t->h.live);
+    h.update_u64be(t->h.next_stamp);
+    h.update(data.data(), data.size());
+    for (uint64_t f = 0; f < n; ++f) {
+        h.update_u64be(used[f] ? 1 : 0);
+        h.update_u64be(uint64_t(b1[f]) << 32 | b2[f]);
+        h.update_u64be(st[f]);
+    }
+    h.final(out);
+    return XPIR_OK;
+}
+
+}  // extern "C"
+
