@@ -52,10 +52,23 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
 
     // acc ^= bucket when the request selects it: one predicate per (request, bucket)
     // shared by the W x 4 predicated XORs (the bucket's 16W bytes in this thread)
-    auto step = [&](const uint4 (&v)[W], const uint32_t (&qw)[RPT], uint32_t bit) {
+    // B <= 4 (HBM-bound): masked XOR from the bit-reversed word (one shift pair per
+    // request x bucket keeps the load stream dense); larger B: predicated XOR.
+    constexpr bool kMask = RPT <= 4;
+    auto step = [&](const uint4 (&v)[W], uint32_t (&qw)[RPT], uint32_t bit) {
 #pragma unroll
-        for (int i = 0; i < RPT; ++i)
-            if (qw[i] & bit) {
+        for (int i = 0; i < RPT; ++i) {
+            if (kMask) {
+                const uint32_t m = uint32_t(int32_t(qw[i]) >> 31);
+                qw[i] <<= 1;
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    acc[i][w].x ^= v[w].x & m;
+                    acc[i][w].y ^= v[w].y & m;
+                    acc[i][w].z ^= v[w].z & m;
+                    acc[i][w].w ^= v[w].w & m;
+                }
+            } else if (qw[i] & bit) {
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                     acc[i][w].x ^= v[w].x;
@@ -64,6 +77,7 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                     acc[i][w].w ^= v[w].w;
                 }
             }
+        }
     };
 
     if (active) {
@@ -82,7 +96,7 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                         if (8 * k < n) w |= uint32_t(__ldg(qp + k)) << (8 * k);
                 }
                 if (n < 32) w &= (1u << n) - 1u;
-                qw[i] = w;  // bucket jc+jj -> bit jj (pir.hpp:25)
+                qw[i] = kMask ? __brev(w) : w;  // bucket jc+jj -> bit jj (pir.hpp:25); bit 31-jj reversed
             }
             if (n == 32) {
 #pragma unroll 8
