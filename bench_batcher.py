@@ -73,6 +73,7 @@ def main():
     ap.add_argument("--max-batch", type=int, default=1024)
     ap.add_argument("--max-wait-us", type=int, default=300)
     ap.add_argument("--pool", type=int, default=1024, help="distinct config-2 shares cycled by the callers")
+    ap.add_argument("--open-rates", default="50000,150000,250000", help="offered rates for the open-loop latency runs")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_batcher.jsonl"))
     args = ap.parse_args()
 
@@ -120,6 +121,25 @@ def main():
                   "max_batch": args.max_batch, "max_wait_us": args.max_wait_us, **common})
     print(json.dumps(lines[-1]), flush=True)
     bt.close()
+
+    # open loop: a fixed offered rate, latency percentiles (serving behaviour)
+    lg.xpl_open_loop.argtypes = [C.c_int, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_void_p,
+                                 C.c_uint32, C.c_double, C.c_double, C.POINTER(C.c_double)]
+    for offered in [float(x) for x in args.open_rates.split(",") if x]:
+        bt2 = xp.Batcher(st, max_batch=args.max_batch, max_wait_us=args.max_wait_us)
+        r6 = (C.c_double * 6)()
+        rc = lg.xpl_open_loop(0, bt2.h, N, S, q.ctypes.data, args.pool, seeds.ctypes.data, T, offered,
+                              min(args.seconds, 3.0), r6)
+        s2 = bt2.stats()
+        bt2.close()
+        if rc:
+            raise RuntimeError(f"open loop rc={rc}")
+        lines.append({"metric": "read-path latency at a fixed offered rate (open loop, batched)", "arm": "batched-open-loop",
+                      "offered_requests_per_s": offered, "achieved_requests_per_s": r6[0], "latency_us_p50": r6[1],
+                      "latency_us_p90": r6[2], "latency_us_p99": r6[3], "latency_us_max": r6[4],
+                      "requests": int(r6[5]), "mean_batch": s2["requests"] / max(s2["batches"], 1),
+                      "max_wait_us": args.max_wait_us, **common})
+        print(json.dumps(lines[-1]), flush=True)
 
     rate = native_drive(1, st.h, min(T, 32), min(args.seconds, 2.0))
     lines.append({"metric": "read-path requests/s (concurrent answer_share scan + mask)", "arm": "unbatched",
