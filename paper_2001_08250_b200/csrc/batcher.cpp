@@ -32,6 +32,7 @@
 
 namespace xpir {
 int set_error(int code, const std::string& msg);  // capi.cu: the thread's xpir_last_error()
+void store_release_stream_scratch(xpir_store* st, cudaStream_t s);  // capi.cu
 }
 
 namespace {
@@ -163,6 +164,10 @@ int bfail(int code, const std::string& m) { return xpir::set_error(code, m); }
 
 void free_bufs(xpir_batcher* b) {
     for (auto& x : b->buf) {
+        if (x.stream) {
+            cudaStreamSynchronize(x.stream);
+            xpir::store_release_stream_scratch(b->st, x.stream);
+        }
         for (uint8_t* p : {x.rows, x.seeds, x.out})
             if (p) cudaFreeHost(p);
         for (uint8_t* p : {x.d_rows, x.d_seeds, x.d_out})

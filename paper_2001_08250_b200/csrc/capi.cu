@@ -23,6 +23,19 @@ int fail(int code, const std::string& msg) {
 const std::string& last_error_message() { return g_err; }
 }  // namespace capi
 int set_error(int code, const std::string& msg) { return capi::fail(code, msg); }
+// Drop the per-stream query scratch of `s` (its owner is destroying the stream;
+// all work on it has completed).
+void store_release_stream_scratch(xpir_store* st, cudaStream_t s) {
+    if (!st) return;
+    std::lock_guard<std::mutex> lk(st->scratch_mu);
+    for (auto it = st->qwin_by_stream.begin(); it != st->qwin_by_stream.end(); ++it)
+        if (it->first == s) {
+            it->second->release();
+            delete it->second;
+            st->qwin_by_stream.erase(it);
+            return;
+        }
+}
 }  // namespace xpir
 
 // ===========================================================================
