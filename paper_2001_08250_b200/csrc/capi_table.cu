@@ -5,7 +5,7 @@
 // cuckoo table
 // ===========================================================================
 
-static const uint32_t DRAW_CAP = 1u << 16;
+static const uint32_t DRAW_CAP = 1u << 18;  // DetRng draws staged per refill (2 MiB)
 
 static void table_free_all(xpir_table* t) {
     cudaFree(t->d.used);

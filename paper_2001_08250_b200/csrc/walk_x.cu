@@ -144,13 +144,19 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
         uint64_t dr_hi = s.rng_block;
         s.status = 0;
         if (use_tm) {  // TMEM part of alt: column c, lane l holds slots X_SM + 64c + 2l (+1)
-            for (uint32_t c = 0; c < 512; ++c) {
-                const uint32_t f = X_SM_SLOTS + c * 64 + 2 * lane;
-                uint32_t v = 0;
-                if (f < slots) v = (d.beta1[f] ^ d.beta2[f]) & 0xffffu;
-                if (f + 1 < slots) v |= ((d.beta1[f + 1] ^ d.beta2[f + 1]) & 0xffffu) << 16;
-                tm_st1(tbase + c, v);
+            for (uint32_t c0 = 0; c0 < 512; c0 += 8) {  // 8 columns per store, loads issued together
+                uint32_t v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t f = X_SM_SLOTS + (c0 + k) * 64 + 2 * lane;
+                    v[k] = 0;
+                    if (f < slots) v[k] = (d.beta1[f] ^ d.beta2[f]) & 0xffffu;
+                    if (f + 1 < slots) v[k] |= ((d.beta1[f + 1] ^ d.beta2[f + 1]) & 0xffffu) << 16;
+                }
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(tbase + c0),
+                             "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
             }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         }
         // alt[] accessor (warp-uniform slot for the TMEM path):
         // returns the old value and stores x (one read-modify-write)
