@@ -439,9 +439,10 @@ class Batcher:
         self.h, self.store = h, store
 
     def close(self):
-        if getattr(self, "h", None):
-            _destroy(lambda: lib().xpir_batcher_destroy(self.h))
-            self.h = None
+        h = getattr(self, "h", None)
+        if h:
+            self.h = None  # new calls fail cleanly; calls already inside finish first
+            _destroy(lambda: lib().xpir_batcher_destroy(h))
 
     __del__ = close
 

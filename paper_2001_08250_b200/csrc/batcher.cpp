@@ -71,6 +71,7 @@ struct xpir_batcher {
     BBuf buf[NBUF];
     std::deque<BBuf*> inflight;  // in submission order
     bool stop = false, completer_stop = false;
+    uint32_t active = 0;  // callers inside xpir_batcher_answer (destroy waits for them)
     std::thread worker, completer;
     uint64_t n_requests = 0, n_batches = 0, max_seen = 0;
 
@@ -245,6 +246,11 @@ int xpir_batcher_destroy(xpir_batcher* b) {
     b->cv_free.notify_all();
     b->worker.join();
     b->completer.join();
+    {
+        // callers of the last batches may still be copying their answers out
+        std::unique_lock<std::mutex> lk(b->mu);
+        b->cv_free.wait(lk, [&] { return b->active == 0; });
+    }
     free_bufs(b);
     delete b;
     return XPIR_OK;
@@ -256,9 +262,22 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
     if (q_bits != b->N) return bfail(XPIR_EINVAL, "answer: query length mismatch");  // pir.cpp:30-31
     const bool masked = mask_seed != nullptr;
     std::unique_lock<std::mutex> lk(b->mu);
+    if (b->stop) return bfail(XPIR_ESTATE, "batcher_answer: batcher is shutting down");
+    b->active += 1;
+    struct Leave {  // the last one out lets a pending destroy proceed
+        xpir_batcher* b;
+        ~Leave() {
+            std::lock_guard<std::mutex> g(b->mu);
+            if (--b->active == 0) b->cv_free.notify_all();
+        }
+    };
     BBuf* buf = nullptr;
     for (;;) {
-        if (b->stop) return bfail(XPIR_ESTATE, "batcher_answer: batcher is shutting down");
+        if (b->stop) {
+            lk.unlock();
+            Leave leave{b};
+            return bfail(XPIR_ESTATE, "batcher_answer: batcher is shutting down");
+        }
         for (auto& x : b->buf)
             if (x.state == BState::Forming && x.masked == masked && x.count < b->max_batch) buf = &x;
         if (!buf)
@@ -277,6 +296,7 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
         if (buf) break;
         b->cv_free.wait(lk);
     }
+    Leave leave{b};  // (constructed after the join loop: the lock above is released below)
     const uint32_t k = buf->count++;
     const uint64_t gen = buf->gen;
     b->n_requests += 1;

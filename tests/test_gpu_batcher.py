@@ -78,3 +78,40 @@ def test_query_length_mismatch_raises(xp, cuda):
     assert bt.answer(q).tobytes() == bytes(32)
     bt.close()
     st.close()
+
+
+def test_close_while_callers_are_active(xp, port, cuda):
+    """Destroying the batcher under load: every in-flight caller gets its correct
+    answer or a clean 'shutting down' error — no crash, no torn answer."""
+    N, S = 2048, 256
+    g = np.random.default_rng(9)
+    db = g.integers(0, 256, N * S, dtype=np.uint8)
+    st = xp.Store(N, S)
+    st.upload(db)
+    bt = xp.Batcher(st, max_batch=16, max_wait_us=200)
+    q = g.integers(0, 256, (64, N // 8), dtype=np.uint8)
+    want = port.answer_batch(db, N, S, q, 64)
+    bad, ok = [], [0]
+
+    def worker(t):
+        for r in range(200):
+            k = (t * 7 + r) % 64
+            try:
+                a = bt.answer(q[k])
+            except xp.XpirError:
+                return
+            if not np.array_equal(a, want[k]):
+                bad.append((t, r))
+            ok[0] += 1
+
+    ts = [threading.Thread(target=worker, args=(t,)) for t in range(32)]
+    for t in ts:
+        t.start()
+    import time
+
+    time.sleep(0.05)
+    bt.close()
+    for t in ts:
+        t.join()
+    assert not bad and ok[0] > 0
+    st.close()
