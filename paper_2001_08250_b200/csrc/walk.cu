@@ -51,11 +51,19 @@ size_t walk_w_smem_bytes(uint64_t slots) {
     return (2 * words) * 4 + W_RING * 8 + 2 * W_CHUNK * 4 + W_HT * 4 + 16;
 }
 
-__global__ void __launch_bounds__(256)
+// G == false: occupancy and touched maps bit-packed in shared memory (tables up to
+// WALKW_MAX_SLOTS). G == true: any table size — occupancy read from the global
+// `used` bytes (one 4/8-byte load per bucket for depth 4/8) and the touched set
+// kept as touched_mark[slot] == batch id, as k_cuckoo_walk_x does; nothing is
+// staged or written back.
+// DEP != 0: the bucket depth as a compile-time constant (the depth-4 tables of
+// every BASELINE config) — no run-time depth dispatch or multiplies per hop.
+template <bool G, uint32_t DEP>
+__global__ void __launch_bounds__(256, 1)
 k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __restrict__ beta1,
                 const uint32_t* __restrict__ beta2, uint64_t i0, uint64_t n, uint32_t* __restrict__ reports) {
     extern __shared__ __align__(16) uint32_t sm[];
-    const uint32_t slots = d.buckets * d.depth;
+    const uint32_t slots = G ? 0u : d.buckets * (DEP ? DEP : d.depth);
     const uint32_t words = (slots + 31) / 32;
     uint64_t* ring = reinterpret_cast<uint64_t*>(sm);  // 8-byte aligned first
     uint32_t* used_bits = sm + 2 * W_RING;
@@ -66,7 +74,7 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
 
     CuckooState s = *gst;
     // stage the occupancy map and the touched map of this round
-    for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
+    for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {  // (G: words == 0)
         uint32_t v = 0;
         for (uint32_t b = 0; b < 32; ++b) {
             const uint32_t f = w * 32 + b;
@@ -77,7 +85,7 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
     }
     for (uint32_t k = threadIdx.x; k < W_HT; k += blockDim.x) htag[k] = FULL;
     __syncthreads();
-    for (uint32_t k = threadIdx.x; k < s.n_touched; k += blockDim.x) {
+    for (uint32_t k = threadIdx.x; k < (G ? 0u : s.n_touched); k += blockDim.x) {
         const uint32_t f = d.touched[k];
         atomicOr(&touch_bits[f >> 5], 1u << (f & 31));
     }
@@ -85,7 +93,7 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
 
     if (threadIdx.x < 32) {
         const uint32_t lane = threadIdx.x;
-        const uint32_t depth = d.depth;
+        const uint32_t depth = DEP ? DEP : d.depth;
         const uint32_t dmask = depth >= 32 ? FULL : (1u << depth) - 1u;  // depth <= 32 (launcher)
         const uint64_t fmask = d.fifo_cap - 1;
         const uint64_t gend = s.draw_base + s.draw_count;  // end of the global draw window
@@ -93,6 +101,18 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
         s.status = 0;
 
         auto free_mask = [&](uint32_t b) -> uint32_t {  // bit s set: slot s of bucket b is free
+            if constexpr (G) {
+                const uint8_t* u = d.used + size_t(b) * depth;
+                if (depth == 4 || depth == 8) {  // 0/1 bytes -> one bit per slot
+                    uint64_t w = depth == 4 ? uint64_t(*reinterpret_cast<const uint32_t*>(u))
+                                            : *reinterpret_cast<const uint64_t*>(u);
+                    w = (w | (w >> 7) | (w >> 14) | (w >> 21) | (w >> 28) | (w >> 35) | (w >> 42) | (w >> 49));
+                    return uint32_t(~w) & dmask;  // bit k of byte 0 = used[k] (bytes are 0/1)
+                }
+                uint32_t m = 0;
+                for (uint32_t k = 0; k < depth; ++k) m |= u[k] ? 0u : (1u << k);
+                return m;
+            }
             const uint32_t f0 = b * depth, w0 = f0 >> 5, sh = f0 & 31;
             uint64_t bits = used_bits[w0];
             if (sh + depth > 32) bits |= uint64_t(used_bits[w0 + 1]) << 32;
@@ -106,16 +126,21 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
             __syncwarp();
         };
         // ---- the sequential path (warp-redundant) ------------------------------
-        auto is_touched = [&](uint32_t f) -> bool { return (touch_bits[f >> 5] >> (f & 31)) & 1u; };
+        auto is_touched = [&](uint32_t f) -> bool {
+            if constexpr (G) return d.touched_mark[f] == s.batch_id;
+            return (touch_bits[f >> 5] >> (f & 31)) & 1u;
+        };
         auto touch = [&](uint32_t f, int64_t org) {
             if (!is_touched(f)) {
-                touch_bits[f >> 5] |= 1u << (f & 31);
+                if constexpr (G) d.touched_mark[f] = s.batch_id;
+                else touch_bits[f >> 5] |= 1u << (f & 31);
                 d.touched[s.n_touched++] = f;
             }
             d.origin[f] = org;
         };
         auto place = [&](uint32_t f, uint32_t b1, uint32_t b2, uint64_t stamp, int64_t org) {  // :37-46
-            used_bits[f >> 5] |= 1u << (f & 31);
+            if constexpr (G) d.used[f] = 1;
+            else used_bits[f >> 5] |= 1u << (f & 31);
             d.beta1[f] = b1;
             d.beta2[f] = b2;
             d.stamp[f] = stamp;
@@ -124,7 +149,8 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
             s.live++;
         };
         auto clear = [&](uint32_t f) {  // :48-54
-            used_bits[f >> 5] &= ~(1u << (f & 31));
+            if constexpr (G) d.used[f] = 0;
+            else used_bits[f >> 5] &= ~(1u << (f & 31));
             d.fifo[d.stamp[f] & fmask] = -1;
             d.beta1[f] = 0;
             d.beta2[f] = 0;
@@ -150,11 +176,16 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 }
             }
             uint32_t stored = 0, dropped = 0, gc = 0, disp = 0;
+            // both buckets' occupancy in one round trip, together with the FIFO head
+            // reads below (re-read when the GC frees a slot)
+            uint32_t m1 = free_mask(b1), m2 = free_mask(b2);
             s.writes++;  // :62
             if (s.live == d.capacity) {  // :64-69 FIFO GC of the oldest entry
                 while (d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
                 clear(uint32_t(d.fifo[s.fifo_head & fmask]));
                 gc = 1;
+                m1 = free_mask(b1);
+                m2 = free_mask(b2);
             }
             const uint64_t stamp = s.next_stamp++;  // :71
             // stamps of dead entries at the head never matter again: skip them
@@ -165,8 +196,7 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 s.status = 2;
                 return false;
             }
-            const uint32_t m1 = free_mask(b1);  // :73-84
-            const uint32_t m2 = m1 ? 0u : free_mask(b2);
+            if (m1) m2 = 0;  // :73-84 (bucket 2 only when bucket 1 is full)
             if (m1 | m2) {
                 const uint32_t b = m1 ? b1 : b2;
                 place(b * depth + uint32_t(__ffs(int(m1 ? m1 : m2)) - 1), b1, b2, stamp, int64_t(i));
@@ -177,7 +207,23 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 uint64_t cst = stamp;
                 int64_t corg = int64_t(i);
                 bool carry_incoming = true, incoming_stored = false, done = false;
+                // power-of-two depth: the victim slot is the next staged draw, so its
+                // metadata is loaded together with the bucket's occupancy (unused when
+                // the bucket has room) — one dependent round trip per hop
+                const bool spec = (depth & (depth - 1)) == 0;
                 for (uint32_t hops = 0;; ++hops) {
+                    uint32_t vs = 0, v1 = 0, v2 = 0, vtm = 0;
+                    uint64_t vst = 0;
+                    int64_t vo = 0;
+                    if (spec) {
+                        vs = uint32_t(ring[s.rng_block & (W_RING - 1)]) & (depth - 1);
+                        const uint32_t vf = be * depth + vs;
+                        v1 = d.beta1[vf];
+                        v2 = d.beta2[vf];
+                        vst = d.stamp[vf];
+                        vo = d.origin[vf];
+                        if constexpr (G) vtm = d.touched_mark[vf];
+                    }
                     const uint32_t fm = free_mask(be);
                     if (fm) {
                         place(be * depth + uint32_t(__ffs(int(fm)) - 1), c1, c2, cst, corg);
@@ -188,19 +234,34 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                         break;
                     }
                     if (hops == XPIR_MAX_DISPLACEMENTS_DEV) break;
-                    const uint32_t vs = uint32_t(uniform(depth));
+                    if (spec) {
+                        s.rng_block++;  // == uniform(depth) for a power-of-two bound
+                    } else {
+                        vs = uint32_t(uniform(depth));
+                        const uint32_t vf = be * depth + vs;
+                        v1 = d.beta1[vf];
+                        v2 = d.beta2[vf];
+                        vst = d.stamp[vf];
+                        vo = d.origin[vf];
+                        if constexpr (G) vtm = d.touched_mark[vf];
+                    }
                     const uint32_t vf = be * depth + vs;
-                    const uint32_t v1 = d.beta1[vf], v2 = d.beta2[vf];
-                    const uint64_t vst = d.stamp[vf];
-                    const int64_t vo = d.origin[vf];
-                    const int64_t vorg = is_touched(vf) ? vo : -int64_t(vf) - 2;
+                    bool vt;
+                    if constexpr (G) vt = vtm == s.batch_id;
+                    else vt = is_touched(vf);
+                    const int64_t vorg = vt ? vo : -int64_t(vf) - 2;
                     // clear(vf) then place(vf, carry) (:110-113): occupancy and live unchanged
                     d.fifo[vst & fmask] = -1;
                     d.beta1[vf] = c1;
                     d.beta2[vf] = c2;
                     d.stamp[vf] = cst;
                     d.fifo[cst & fmask] = int64_t(vf);
-                    touch(vf, corg);
+                    if (!vt) {  // touch(vf, corg)
+                        if constexpr (G) d.touched_mark[vf] = s.batch_id;
+                        else touch_bits[vf >> 5] |= 1u << (vf & 31);
+                        d.touched[s.n_touched++] = vf;
+                    }
+                    d.origin[vf] = corg;
                     if (carry_incoming) incoming_stored = true;
                     c1 = v1;
                     c2 = v2;
@@ -255,14 +316,18 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                     const uint64_t i = c + lane;
                     f = pb * depth + uint32_t(__ffs(int(pm)) - 1);
                     const uint64_t stamp = s.next_stamp + lane;
-                    atomicOr(&used_bits[f >> 5], 1u << (f & 31));
+                    if constexpr (G) d.used[f] = 1;
+                    else atomicOr(&used_bits[f >> 5], 1u << (f & 31));
                     d.beta1[f] = b1;
                     d.beta2[f] = b2;
                     d.stamp[f] = stamp;
                     d.fifo[stamp & fmask] = int64_t(f);
                     d.origin[f] = int64_t(i);
                     newt = !is_touched(f);
-                    if (newt) atomicOr(&touch_bits[f >> 5], 1u << (f & 31));
+                    if (newt) {
+                        if constexpr (G) d.touched_mark[f] = s.batch_id;
+                        else atomicOr(&touch_bits[f >> 5], 1u << (f & 31));
+                    }
                     if (reports) reinterpret_cast<uint4*>(reports)[i] = make_uint4(1, 0, 0, 0);
                 }
                 const uint32_t nm = __ballot_sync(FULL, newt);
@@ -289,7 +354,7 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
         if (lane == 0) *gst = s;
     }
     __syncthreads();
-    // occupancy map back to the global byte array
+    // occupancy map back to the global byte array (G: words == 0)
     for (uint32_t w = threadIdx.x; w < words; w += blockDim.x) {
         const uint32_t v = used_bits[w];
         const uint32_t f0 = w * 32;
@@ -299,15 +364,20 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
 
 cudaError_t launch_cuckoo_walk_w(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
                                  uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s) {
-    const size_t smem = walk_w_smem_bytes(uint64_t(d.buckets) * d.depth);
-    cudaError_t e = cudaFuncSetAttribute(k_cuckoo_walk_w, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const uint64_t slots = uint64_t(d.buckets) * d.depth;
+    const bool g = slots > WALKW_MAX_SLOTS;
+    const size_t smem = walk_w_smem_bytes(g ? 0 : slots);
+    auto k = d.depth == 4 ? (g ? k_cuckoo_walk_w<true, 4> : k_cuckoo_walk_w<false, 4>)
+                          : (g ? k_cuckoo_walk_w<true, 0> : k_cuckoo_walk_w<false, 0>);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    k_cuckoo_walk_w<<<1, 256, smem, s>>>(d, st, beta1, beta2, i0, n, reports);
+    k<<<1, 256, smem, s>>>(d, st, beta1, beta2, i0, n, reports);
     return cudaGetLastError();
 }
 
 bool walk_w_supported(const CuckooDev& d) {
-    return uint64_t(d.buckets) * d.depth <= WALKW_MAX_SLOTS && d.depth <= 32;
+    // the global-map variant takes any size; slot ids stay 32-bit
+    return uint64_t(d.buckets) * d.depth < (uint64_t(1) << 32) && d.depth <= 32;
 }
 
 }  // namespace xpir

@@ -188,10 +188,14 @@ def test_parallel_prefix_matches_sequential(xp, port, cuda, nb, depth, cap, n, s
     (33000, 3, 1.0, 0.95, 0.0, "x"),    # depth 3: uniform(depth) with rejection, TMEM part
     (16384, 8, 0.9, 1.3, 0.01, "x"),    # 131,072 slots at capacity: FIFO GC on every insert past it
     (20000, 4, 1.0, 0.96, 0.0, "w"),    # the warp walk with global victim metadata (A/B)
+    (140000, 4, 1.0, 0.95, 0.01, "g"),  # 560,000 slots: beyond the on-chip maps, global-map warp walk
+    (70000, 8, 0.95, 1.1, 0.0, "g"),    # depth 8 (one 8-byte occupancy load), GC past capacity
+    (190000, 3, 1.0, 0.94, 0.0, "g"),   # depth 3: per-byte occupancy, rejection draws
 ])
 def test_walk_kernels_large_tables(xp, port, cuda, nb, depth, cap_frac, load, same_frac, walk):
     """The warp-cooperative walks on tables whose alt index spills into TMEM
-    (k_cuckoo_walk_x) or that run the global-metadata walk (k_cuckoo_walk_w), at
+    (k_cuckoo_walk_x) or that run the global-metadata walk (k_cuckoo_walk_w, with
+    its occupancy/touched maps in global memory past 512 Ki slots), at
     high load with long eviction chains, beta1 == beta2 items, non-power-of-two
     depth and GC: reports, table bytes, metadata and state digest equal the
     oracle's sequential cuckoo::Table::insert (cuckoo.cpp:56-126)."""
