@@ -69,6 +69,23 @@ def test_scan_matches_oracle(xp, port, cuda, kernel, N, S, B):
         assert xp.last_scan_kernel() == 2
 
 
+@pytest.mark.parametrize("S", [96, 512])
+def test_direct_every_small_batch(xp, port, cuda, S):
+    """The direct kernel's request tiling (tiles of 1/2/4/6/8 requests, partial
+    last tiles) for every B = 1..17, ragged bucket count."""
+    N = 1001
+    g = np.random.default_rng(S)
+    db = rand(g, N * S)
+    st = xp.Store(N, S)
+    st.upload(db)
+    xp.set_scan_opts(1)
+    for B in range(1, 18):
+        q = rand(g, B, (N + 7) // 8)
+        q[:, -1] &= 0x01
+        assert np.array_equal(st.answer_batch(q), port.answer_batch(db, N, S, q, B)), B
+        assert xp.last_scan_kernel() == 1
+
+
 def test_dirty_trailing_bits_are_ignored(xp, port, cuda):
     # pir::answer only reads bits j < N (pir.cpp:33-34)
     N, S, B = 1001, 256, 200
