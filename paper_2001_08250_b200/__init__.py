@@ -190,6 +190,15 @@ def _destroy(fn) -> None:
         pass
 
 
+def _quiet_del(self) -> None:
+    """__del__ of every handle class: close(), but never raise from a finalizer
+    (at interpreter shutdown even this module's globals may be gone)."""
+    try:
+        self.close()
+    except Exception:  # noqa: BLE001
+        pass
+
+
 def _check(rc: int) -> int:
     if rc >= 0:
         return rc
@@ -286,7 +295,7 @@ class DeviceBuffer:
             _destroy(lambda: lib().xpir_dev_free(self.device, self.ptr))
             self.ptr = None
 
-    __del__ = close
+    __del__ = _quiet_del
 
 
 def ipc_handle(d_ptr, device: int = 0) -> bytes:
@@ -327,7 +336,7 @@ class Store:
             _destroy(lambda: lib().xpir_store_destroy(self.h))
             self.h = None
 
-    __del__ = close
+    __del__ = _quiet_del
 
     @property
     def shard_bytes(self) -> int:
@@ -444,7 +453,7 @@ class Batcher:
             self.h = None  # new calls fail cleanly; calls already inside finish first
             _destroy(lambda: lib().xpir_batcher_destroy(h))
 
-    __del__ = close
+    __del__ = _quiet_del
 
     def answer(self, q, mask_seed: bytes | None = None, q_bits: int | None = None) -> np.ndarray:
         """pir::answer(snapshot, q), or mask_answer(answer(..), mask_seed) (pir.cpp:29-39, 65-69)."""
@@ -582,7 +591,7 @@ class Table:
             _destroy(lambda: lib().xpir_table_destroy(self.h))
             self.h = None
 
-    __del__ = close
+    __del__ = _quiet_del
 
     def insert_batch(self, beta1, beta2, payload) -> np.ndarray:
         """Table::insert for each item in order; returns n x 4 InsertReport rows."""
@@ -675,7 +684,7 @@ class Window:
             _destroy(lambda: lib().xpir_window_destroy(self.h))
             self.h = None
 
-    __del__ = close
+    __del__ = _quiet_del
 
     def absorb(self, positions) -> None:
         p = np.ascontiguousarray(positions, np.uint32).reshape(-1)
@@ -768,7 +777,7 @@ class _BorrowedStore(Store):
     def close(self):
         self.h = None
 
-    __del__ = close
+    __del__ = _quiet_del
 
 
 _BARRIER_FN = C.CFUNCTYPE(None, C.c_void_p)
@@ -809,7 +818,7 @@ class Server:
             _destroy(lambda: lib().xpir_server_destroy(self.h))
             self.h = None
 
-    __del__ = close
+    __del__ = _quiet_del
 
     def apply_round(self, beta1, beta2, payload, interest, seal_after: bool = False, smap=None, barrier=None):
         """ServerCore::apply_write for each write (+ seal). On a shard rank pass the
