@@ -45,12 +45,14 @@ constexpr uint32_t X_NEED = 640;         // draws staged before a sequential ins
 constexpr uint32_t X_CHUNK = 256;        // staged inserts (beta pairs)
 constexpr uint32_t X_HT = 256;           // placement-bucket hash of the batch path
 constexpr uint32_t X_CHAIN = 512;        // >= MAX_DISPLACEMENTS + 1
+constexpr uint32_t X_HS = 1000;          // long-chain slot -> last-visit hash (>= 2 x distinct slots)
+constexpr uint32_t X_EMPTY = 0xffffffffu;
 constexpr uint32_t FULLM = 0xffffffffu;
 constexpr uint16_t NONE16 = 0xffff;
 
 struct XLayout {
     uint32_t alt_sm, words;
-    size_t o_ring, o_alt, o_used, o_sb1, o_sb2, o_ht, o_chain, o_prev, o_src, o_pre, o_taddr, total;
+    size_t o_ring, o_alt, o_used, o_sb1, o_sb2, o_ht, o_chain, o_hash, o_src, o_pre, o_taddr, total;
     __host__ __device__ explicit XLayout(uint32_t slots) {
         alt_sm = slots < X_SM_SLOTS ? slots : X_SM_SLOTS;
         words = (slots + 31) / 32;
@@ -62,8 +64,8 @@ struct XLayout {
         o_sb2 = a16(o_sb1 + X_CHUNK * 4);
         o_ht = a16(o_sb2 + X_CHUNK * 4);
         o_chain = a16(o_ht + X_HT * 4);
-        o_prev = a16(o_chain + X_CHAIN * 4);
-        o_src = a16(o_prev + X_CHAIN * 2);
+        o_hash = a16(o_chain + X_CHAIN * 4);  // u32 entries: slot << 9 | last visit index
+        o_src = a16(o_hash + X_HS * 4);
         o_pre = a16(o_src + (X_CHAIN + 16) * 2);  // 32 x {u64 stamp, u64 origin, u32 b1, b2, mark, pad}
         o_taddr = a16(o_pre + 32 * 32);
         total = o_taddr + 16;
@@ -107,7 +109,7 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
     uint32_t* sb2 = reinterpret_cast<uint32_t*>(smx + L.o_sb2);
     uint32_t* htag = reinterpret_cast<uint32_t*>(smx + L.o_ht);
     uint32_t* chain = reinterpret_cast<uint32_t*>(smx + L.o_chain);
-    uint16_t* prevk = reinterpret_cast<uint16_t*>(smx + L.o_prev);
+    uint32_t* hsh = reinterpret_cast<uint32_t*>(smx + L.o_hash);
     uint16_t* srck = reinterpret_cast<uint16_t*>(smx + L.o_src);
     const uint32_t smem_base = static_cast<uint32_t>(__cvta_generic_to_shared(smx));
     const bool use_tm = slots > X_SM_SLOTS;
@@ -291,36 +293,90 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 __syncwarp();
             } else {
             // ---- resolve a long chain through global scratch ----------------
+            // Chunks of 32 hops in order, O(h) overall: within a chunk revisits are
+            // found with __match_any_sync, across chunks through a shared-memory hash
+            // (slot -> last visit so far); srck[j] = the item placed at step j
+            // (NONE16 = the incoming one, q = the pre-chain content of chain[q]).
             uint64_t* pre = d.chain_pre;  // [3 * X_CHAIN]: (b1 | b2 << 32), stamp, origin
-            for (uint32_t k = lane; k < h; k += 32) {
-                const uint32_t v = chain[k];
-                pre[3 * k] = uint64_t(d.beta1[v]) | uint64_t(d.beta2[v]) << 32;
-                pre[3 * k + 1] = d.stamp[v];
-                const int64_t o = d.origin[v];
-                pre[3 * k + 2] = uint64_t(d.touched_mark[v] == s.batch_id ? o : -int64_t(v) - 2);
-                uint16_t p = NONE16;
-                for (int32_t q = int32_t(k) - 1; q >= 0; --q)
-                    if (chain[q] == v) {
-                        p = uint16_t(q);
-                        break;
+            auto hslot = [](uint32_t v) { return (v * 2654435761u) % X_HS; };
+            for (uint32_t k = lane; k < X_HS; k += 32) hsh[k] = X_EMPTY;
+            if (lane == 0) srck[0] = NONE16;
+            __syncwarp();
+            for (uint32_t base = 0; base < h; base += 32) {
+                const uint32_t k = base + lane;
+                const bool valid = k < h;
+                const uint32_t v = valid ? chain[k] : (0x80000000u | lane);
+                if (valid) {
+                    pre[3 * k] = uint64_t(d.beta1[v]) | uint64_t(d.beta2[v]) << 32;
+                    pre[3 * k + 1] = d.stamp[v];
+                    const int64_t o = d.origin[v];
+                    pre[3 * k + 2] = uint64_t(d.touched_mark[v] == s.batch_id ? o : -int64_t(v) - 2);
+                }
+                const uint32_t mm = __match_any_sync(FULLM, v);
+                const uint32_t below = mm & ((1u << lane) - 1u);
+                const uint32_t above = mm & ~((2u << lane) - 1u);
+                // last earlier visit: in this chunk, else from the hash (earlier chunks)
+                int prev = below ? int(base) + 31 - __clz(int(below)) : -1;
+                uint32_t hpos = hslot(v), hfound = X_EMPTY;
+                if (valid && !below) {
+                    for (;;) {
+                        const uint32_t e = hsh[hpos];
+                        if (e == X_EMPTY) break;
+                        if ((e >> 9) == v) {
+                            hfound = hpos;
+                            prev = int(e & 511u);
+                            break;
+                        }
+                        hpos = hpos + 1 == X_HS ? 0 : hpos + 1;
                     }
-                prevk[k] = p;
+                }
+                // f(k) = item carried out of hop k = srck[k + 1]:
+                // prev < 0 -> k; else srck[prev] (known when prev <= base, else f(prev - 1) in this chunk)
+                int cur = int(k), res = -3;  // -3 pending
+                bool pend = valid;
+                while (__any_sync(FULLM, pend)) {
+                    const int p = __shfl_sync(FULLM, prev, (cur - int(base)) & 31);
+                    if (pend) {
+                        if (p < 0) {
+                            res = cur;
+                            pend = false;
+                        } else if (p <= int(base)) {
+                            res = srck[p] == NONE16 ? -1 : int(srck[p]);
+                            pend = false;
+                        } else {
+                            cur = p - 1;
+                        }
+                    }
+                }
+                if (valid) srck[k + 1] = res < 0 ? NONE16 : uint16_t(res);
+                // record the last visit of each slot of this chunk
+                if (valid && above == 0) {
+                    const uint32_t ent = v << 9 | k;
+                    if (hfound != X_EMPTY) {
+                        hsh[hfound] = ent;
+                    } else {
+                        uint32_t q = hslot(v);
+                        for (;;) {
+                            const uint32_t old = atomicCAS(&hsh[q], X_EMPTY, ent);
+                            if (old == X_EMPTY) break;
+                            if ((old >> 9) == v) {  // seen in an earlier chunk and earlier in this one
+                                hsh[q] = ent;
+                                break;
+                            }
+                            q = q + 1 == X_HS ? 0 : q + 1;
+                        }
+                    }
+                }
+                __syncwarp();
             }
-            __syncwarp();
-            // src[k]: the item placed at step k (NONE16 = the incoming one, j = pre-content of chain[j])
-            if (lane == 0) {
-                srck[0] = NONE16;
-                for (uint32_t k = 0; k < h; ++k) srck[k + 1] = prevk[k] != NONE16 ? srck[prevk[k]] : uint16_t(k);
-            }
-            __syncwarp();
             for (uint32_t k = lane; k <= h; k += 32) {
                 const uint16_t src = srck[k];
                 uint32_t slot;
                 if (k < h) {
                     slot = chain[k];
-                    bool last = true;
-                    for (uint32_t q = k + 1; q < h && last; ++q) last = chain[q] != slot;
-                    if (!last) continue;
+                    uint32_t q = hslot(slot), e;
+                    while ((e = hsh[q]) >> 9 != slot) q = q + 1 == X_HS ? 0 : q + 1;
+                    if ((e & 511u) != k) continue;  // not the last visit of this slot
                 } else {
                     slot = final_slot;
                 }
