@@ -50,9 +50,18 @@ constexpr uint32_t X_EMPTY = 0xffffffffu;
 constexpr uint32_t FULLM = 0xffffffffu;
 constexpr uint16_t NONE16 = 0xffff;
 
+// A finished chain handed from the walking warp to the resolving warp: its slots
+// (chains of <= 32 hops; longer ones stay in the shared chain[] log), final slot
+// (FULLM = dropped) and the incoming item.
+struct XRec {
+    uint32_t v[32];
+    uint32_t h, final_slot, b1, b2;
+    uint64_t stamp, i;
+};
+
 struct XLayout {
     uint32_t alt_sm, words;
-    size_t o_ring, o_alt, o_used, o_sb1, o_sb2, o_ht, o_chain, o_hash, o_src, o_pre, o_taddr, total;
+    size_t o_ring, o_alt, o_used, o_sb1, o_sb2, o_ht, o_chain, o_hash, o_src, o_q, o_qf, o_taddr, total;
     __host__ __device__ explicit XLayout(uint32_t slots) {
         alt_sm = slots < X_SM_SLOTS ? slots : X_SM_SLOTS;
         words = (slots + 31) / 32;
@@ -66,8 +75,9 @@ struct XLayout {
         o_chain = a16(o_ht + X_HT * 4);
         o_hash = a16(o_chain + X_CHAIN * 4);  // u32 entries: slot << 9 | last visit index
         o_src = a16(o_hash + X_HS * 4);
-        o_pre = a16(o_src + (X_CHAIN + 16) * 2);  // 32 x {u64 stamp, u64 origin, u32 b1, b2, mark, pad}
-        o_taddr = a16(o_pre + 32 * 32);
+        o_q = a16(o_src + (X_CHAIN + 16) * 2);  // 2 hand-off records (XRec)
+        o_qf = a16(o_q + 2 * sizeof(XRec));    // flags: full[0], full[1], chain[] busy, done
+        o_taddr = a16(o_qf + 16);
         total = o_taddr + 16;
     }
 };
@@ -132,16 +142,223 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
     }
     for (uint32_t f = threadIdx.x; f < L.alt_sm; f += blockDim.x) alt[f] = uint16_t(d.beta1[f] ^ d.beta2[f]);
     for (uint32_t k = threadIdx.x; k < X_HT; k += blockDim.x) htag[k] = FULLM;
+    if (threadIdx.x < 4) reinterpret_cast<volatile uint32_t*>(smx + L.o_qf)[threadIdx.x] = 0;
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tbase = use_tm ? *reinterpret_cast<const uint32_t*>(smx + L.o_taddr) : 0u;
 
     CuckooState s = *gst;
+    const uint32_t depth = d.depth;
+    const uint64_t fmask = d.fifo_cap - 1;
+    XRec* recs = reinterpret_cast<XRec*>(smx + L.o_q);
+    volatile uint32_t* qflag = reinterpret_cast<volatile uint32_t*>(smx + L.o_qf);
+    auto touch_store = [&](uint32_t f, int64_t org) {  // lane-local store of one slot's origin + mark
+        d.origin[f] = org;
+        d.touched_mark[f] = s.batch_id;
+    };
+    // ---- resolve a finished chain: who ends where (see the header comment); warp 1 ----
+    auto resolve_chain = [&](const XRec& r) {
+        const uint32_t h = r.h, final_slot = r.final_slot, b1 = r.b1, b2 = r.b2;
+        const uint64_t stamp = r.stamp, i = r.i;
+        if (h <= 32) {
+            // ---- resolve a short chain in registers -------------------------
+            // lane k holds chain[k] and its pre-chain content; revisits by match_any
+            const uint32_t my_v = lane < h ? r.v[lane] : (0x80000000u | lane);
+            uint64_t my_st = 0;
+            int64_t my_org = 0;
+            uint32_t my_b1 = 0, my_b2 = 0, my_mark = 0;
+            if (lane < h) {
+                my_st = d.stamp[my_v];
+                my_org = d.origin[my_v];
+                my_b1 = d.beta1[my_v];
+                my_b2 = d.beta2[my_v];
+                my_mark = d.touched_mark[my_v];
+            }
+            const int64_t my_pre_org = my_mark == s.batch_id ? my_org : -int64_t(my_v) - 2;
+            const uint32_t mm = __match_any_sync(FULLM, my_v);
+            const uint32_t below = mm & ((1u << lane) - 1u);
+            const uint32_t above = mm & ~((2u << lane) - 1u);
+            const int prev = below ? 31 - __clz(int(below)) : -1;  // last earlier visit
+            // f(k) = the item carried out of hop k: the pre-content of chain[k] (= k),
+            // or the item placed at its previous visit p (INC if p == 0, else f(p - 1))
+            int cur = int(lane), res = -2;  // -2 pending, -1 incoming, j >= 0 pre(chain[j])
+            bool pend = lane < h;
+            if (!pend) res = int(lane);
+            while (__any_sync(FULLM, pend)) {
+                const int p = __shfl_sync(FULLM, prev, cur & 31);
+                if (pend) {
+                    if (p < 0) {
+                        res = cur;
+                        pend = false;
+                    } else if (p == 0) {
+                        res = -1;
+                        pend = false;
+                    } else {
+                        cur = p - 1;
+                    }
+                }
+            }
+            // step k places item src(k) = (k == 0 ? incoming : f(k - 1)) at chain[k];
+            // step h places f(h - 1) at the final slot (or drops it)
+            const int srck_l = __shfl_up_sync(FULLM, res, 1);
+            const int src_here = lane == 0 ? -1 : srck_l;
+            const int src_final = h == 0 ? -1 : __shfl_sync(FULLM, res, (h - 1) & 31);
+            auto content = [&](int src, uint32_t& c1, uint32_t& c2, uint64_t& cst, int64_t& corg) {
+                const int sl = src < 0 ? 0 : src;
+                const uint32_t x1 = __shfl_sync(FULLM, my_b1, sl), x2 = __shfl_sync(FULLM, my_b2, sl);
+                const uint64_t xs = __shfl_sync(FULLM, my_st, sl);
+                const int64_t xo = __shfl_sync(FULLM, my_pre_org, sl);
+                if (src < 0) {
+                    c1 = b1;
+                    c2 = b2;
+                    cst = stamp;
+                    corg = int64_t(i);
+                } else {
+                    c1 = x1;
+                    c2 = x2;
+                    cst = xs;
+                    corg = xo;
+                }
+            };
+            uint32_t c1, c2;
+            uint64_t cst;
+            int64_t corg;
+            content(src_here, c1, c2, cst, corg);
+            if (lane < h && above == 0) {  // last visit of chain[lane]: its final content
+                d.beta1[my_v] = c1;
+                d.beta2[my_v] = c2;
+                d.stamp[my_v] = cst;
+                d.fifo[cst & fmask] = int64_t(my_v);
+                touch_store(my_v, corg);
+            }
+            content(src_final, c1, c2, cst, corg);
+            if (lane == 0) {
+                if (final_slot == FULLM) {
+                    d.fifo[cst & fmask] = -1;  // the dropped item leaves the FIFO
+                } else {
+                    d.beta1[final_slot] = c1;
+                    d.beta2[final_slot] = c2;
+                    d.stamp[final_slot] = cst;
+                    d.fifo[cst & fmask] = int64_t(final_slot);
+                    touch_store(final_slot, corg);
+                }
+            }
+            __syncwarp();
+        } else {
+        // ---- resolve a long chain through global scratch ----------------
+        // Chunks of 32 hops in order, O(h) overall: within a chunk revisits are
+        // found with __match_any_sync, across chunks through a shared-memory hash
+        // (slot -> last visit so far); srck[j] = the item placed at step j
+        // (NONE16 = the incoming one, q = the pre-chain content of chain[q]).
+        uint64_t* pre = d.chain_pre;  // [3 * X_CHAIN]: (b1 | b2 << 32), stamp, origin
+        auto hslot = [](uint32_t v) { return (v * 2654435761u) % X_HS; };
+        for (uint32_t k = lane; k < X_HS; k += 32) hsh[k] = X_EMPTY;
+        if (lane == 0) srck[0] = NONE16;
+        __syncwarp();
+        for (uint32_t base = 0; base < h; base += 32) {
+            const uint32_t k = base + lane;
+            const bool valid = k < h;
+            const uint32_t v = valid ? chain[k] : (0x80000000u | lane);
+            if (valid) {
+                pre[3 * k] = uint64_t(d.beta1[v]) | uint64_t(d.beta2[v]) << 32;
+                pre[3 * k + 1] = d.stamp[v];
+                const int64_t o = d.origin[v];
+                pre[3 * k + 2] = uint64_t(d.touched_mark[v] == s.batch_id ? o : -int64_t(v) - 2);
+            }
+            const uint32_t mm = __match_any_sync(FULLM, v);
+            const uint32_t below = mm & ((1u << lane) - 1u);
+            const uint32_t above = mm & ~((2u << lane) - 1u);
+            // last earlier visit: in this chunk, else from the hash (earlier chunks)
+            int prev = below ? int(base) + 31 - __clz(int(below)) : -1;
+            uint32_t hpos = hslot(v), hfound = X_EMPTY;
+            if (valid && !below) {
+                for (;;) {
+                    const uint32_t e = hsh[hpos];
+                    if (e == X_EMPTY) break;
+                    if ((e >> 9) == v) {
+                        hfound = hpos;
+                        prev = int(e & 511u);
+                        break;
+                    }
+                    hpos = hpos + 1 == X_HS ? 0 : hpos + 1;
+                }
+            }
+            // f(k) = item carried out of hop k = srck[k + 1]:
+            // prev < 0 -> k; else srck[prev] (known when prev <= base, else f(prev - 1) in this chunk)
+            int cur = int(k), res = -3;  // -3 pending
+            bool pend = valid;
+            while (__any_sync(FULLM, pend)) {
+                const int p = __shfl_sync(FULLM, prev, (cur - int(base)) & 31);
+                if (pend) {
+                    if (p < 0) {
+                        res = cur;
+                        pend = false;
+                    } else if (p <= int(base)) {
+                        res = srck[p] == NONE16 ? -1 : int(srck[p]);
+                        pend = false;
+                    } else {
+                        cur = p - 1;
+                    }
+                }
+            }
+            if (valid) srck[k + 1] = res < 0 ? NONE16 : uint16_t(res);
+            // record the last visit of each slot of this chunk
+            if (valid && above == 0) {
+                const uint32_t ent = v << 9 | k;
+                if (hfound != X_EMPTY) {
+                    hsh[hfound] = ent;
+                } else {
+                    uint32_t q = hslot(v);
+                    for (;;) {
+                        const uint32_t old = atomicCAS(&hsh[q], X_EMPTY, ent);
+                        if (old == X_EMPTY) break;
+                        if ((old >> 9) == v) {  // seen in an earlier chunk and earlier in this one
+                            hsh[q] = ent;
+                            break;
+                        }
+                        q = q + 1 == X_HS ? 0 : q + 1;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+        for (uint32_t k = lane; k <= h; k += 32) {
+            const uint16_t src = srck[k];
+            uint32_t slot;
+            if (k < h) {
+                slot = chain[k];
+                uint32_t q = hslot(slot), e;
+                while ((e = hsh[q]) >> 9 != slot) q = q + 1 == X_HS ? 0 : q + 1;
+                if ((e & 511u) != k) continue;  // not the last visit of this slot
+            } else {
+                slot = final_slot;
+            }
+            uint32_t c1 = b1, c2 = b2;
+            uint64_t cst = stamp;
+            int64_t corg = int64_t(i);
+            if (src != NONE16) {
+                const uint64_t bb = pre[3 * src];
+                c1 = uint32_t(bb);
+                c2 = uint32_t(bb >> 32);
+                cst = pre[3 * src + 1];
+                corg = int64_t(pre[3 * src + 2]);
+            }
+            if (slot == FULLM) {  // the dropped item leaves the FIFO
+                d.fifo[cst & fmask] = -1;
+                continue;
+            }
+            d.beta1[slot] = c1;
+            d.beta2[slot] = c2;
+            d.stamp[slot] = cst;
+            d.fifo[cst & fmask] = int64_t(slot);
+            touch_store(slot, corg);
+        }
+        __syncwarp();
+        }
+            };
     if (warp == 0) {
-        const uint32_t depth = d.depth;
         const uint32_t dmask = depth >= 32 ? FULLM : (1u << depth) - 1u;
         const bool dpow2 = (depth & (depth - 1)) == 0;
-        const uint64_t fmask = d.fifo_cap - 1;
         const uint64_t gend = s.draw_base + s.draw_count;
         uint64_t dr_hi = s.rng_block;
         s.status = 0;
@@ -197,222 +414,21 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 if (tail == 0 || v <= ~uint64_t(0) - tail) return v % bound;
             }
         };
-        auto touch_store = [&](uint32_t f, int64_t org) {  // lane-local store of one slot's origin + mark
-            d.origin[f] = org;
-            d.touched_mark[f] = s.batch_id;
+        // hand-off to warp 1: record slots alternate; flags are written after a fence
+        uint32_t wslot = 0;
+        auto wait_zero = [&](uint32_t k) {
+            while (qflag[k] != 0) __nanosleep(20);
+            __syncwarp();
+            __threadfence_block();
         };
-
-        // ---- resolve a finished chain: who ends where (see the header comment) ----
-        bool pend_chain = false;
-        uint32_t p_h = 0, p_final = FULLM, p_b1 = 0, p_b2 = 0;
-        uint64_t p_stamp = 0, p_i = 0;
-        auto resolve_chain = [&]() {
-            const uint32_t h = p_h, final_slot = p_final, b1 = p_b1, b2 = p_b2;
-            const uint64_t stamp = p_stamp, i = p_i;
-            const uint32_t my_v = lane < h && lane < 32 ? chain[lane] : (0x80000000u | lane);
-            asm volatile("cp.async.wait_all;\n" ::: "memory");
-            __syncwarp();
-            if (h <= 32) {
-                // ---- resolve a short chain in registers -------------------------
-                // lane k holds chain[k] and its pre-chain content; revisits by match_any
-                const uint8_t* mine = smx + L.o_pre + lane * 32;
-                const uint64_t my_st = *reinterpret_cast<const uint64_t*>(mine);
-                const int64_t my_org = *reinterpret_cast<const int64_t*>(mine + 8);
-                const uint32_t my_b1 = *reinterpret_cast<const uint32_t*>(mine + 16);
-                const uint32_t my_b2 = *reinterpret_cast<const uint32_t*>(mine + 20);
-                const uint32_t my_mark = *reinterpret_cast<const uint32_t*>(mine + 24);
-                const int64_t my_pre_org = my_mark == s.batch_id ? my_org : -int64_t(my_v) - 2;
-                const uint32_t mm = __match_any_sync(FULLM, my_v);
-                const uint32_t below = mm & ((1u << lane) - 1u);
-                const uint32_t above = mm & ~((2u << lane) - 1u);
-                const int prev = below ? 31 - __clz(int(below)) : -1;  // last earlier visit
-                // f(k) = the item carried out of hop k: the pre-content of chain[k] (= k),
-                // or the item placed at its previous visit p (INC if p == 0, else f(p - 1))
-                int cur = int(lane), res = -2;  // -2 pending, -1 incoming, j >= 0 pre(chain[j])
-                bool pend = lane < h;
-                if (!pend) res = int(lane);
-                while (__any_sync(FULLM, pend)) {
-                    const int p = __shfl_sync(FULLM, prev, cur & 31);
-                    if (pend) {
-                        if (p < 0) {
-                            res = cur;
-                            pend = false;
-                        } else if (p == 0) {
-                            res = -1;
-                            pend = false;
-                        } else {
-                            cur = p - 1;
-                        }
-                    }
-                }
-                // step k places item src(k) = (k == 0 ? incoming : f(k - 1)) at chain[k];
-                // step h places f(h - 1) at the final slot (or drops it)
-                const int srck_l = __shfl_up_sync(FULLM, res, 1);
-                const int src_here = lane == 0 ? -1 : srck_l;
-                const int src_final = h == 0 ? -1 : __shfl_sync(FULLM, res, (h - 1) & 31);
-                auto content = [&](int src, uint32_t& c1, uint32_t& c2, uint64_t& cst, int64_t& corg) {
-                    const int sl = src < 0 ? 0 : src;
-                    const uint32_t x1 = __shfl_sync(FULLM, my_b1, sl), x2 = __shfl_sync(FULLM, my_b2, sl);
-                    const uint64_t xs = __shfl_sync(FULLM, my_st, sl);
-                    const int64_t xo = __shfl_sync(FULLM, my_pre_org, sl);
-                    if (src < 0) {
-                        c1 = b1;
-                        c2 = b2;
-                        cst = stamp;
-                        corg = int64_t(i);
-                    } else {
-                        c1 = x1;
-                        c2 = x2;
-                        cst = xs;
-                        corg = xo;
-                    }
-                };
-                uint32_t c1, c2;
-                uint64_t cst;
-                int64_t corg;
-                content(src_here, c1, c2, cst, corg);
-                if (lane < h && above == 0) {  // last visit of chain[lane]: its final content
-                    d.beta1[my_v] = c1;
-                    d.beta2[my_v] = c2;
-                    d.stamp[my_v] = cst;
-                    d.fifo[cst & fmask] = int64_t(my_v);
-                    touch_store(my_v, corg);
-                }
-                content(src_final, c1, c2, cst, corg);
-                if (lane == 0) {
-                    if (final_slot == FULLM) {
-                        d.fifo[cst & fmask] = -1;  // the dropped item leaves the FIFO
-                    } else {
-                        d.beta1[final_slot] = c1;
-                        d.beta2[final_slot] = c2;
-                        d.stamp[final_slot] = cst;
-                        d.fifo[cst & fmask] = int64_t(final_slot);
-                        touch_store(final_slot, corg);
-                    }
-                }
-                __syncwarp();
-            } else {
-            // ---- resolve a long chain through global scratch ----------------
-            // Chunks of 32 hops in order, O(h) overall: within a chunk revisits are
-            // found with __match_any_sync, across chunks through a shared-memory hash
-            // (slot -> last visit so far); srck[j] = the item placed at step j
-            // (NONE16 = the incoming one, q = the pre-chain content of chain[q]).
-            uint64_t* pre = d.chain_pre;  // [3 * X_CHAIN]: (b1 | b2 << 32), stamp, origin
-            auto hslot = [](uint32_t v) { return (v * 2654435761u) % X_HS; };
-            for (uint32_t k = lane; k < X_HS; k += 32) hsh[k] = X_EMPTY;
-            if (lane == 0) srck[0] = NONE16;
-            __syncwarp();
-            for (uint32_t base = 0; base < h; base += 32) {
-                const uint32_t k = base + lane;
-                const bool valid = k < h;
-                const uint32_t v = valid ? chain[k] : (0x80000000u | lane);
-                if (valid) {
-                    pre[3 * k] = uint64_t(d.beta1[v]) | uint64_t(d.beta2[v]) << 32;
-                    pre[3 * k + 1] = d.stamp[v];
-                    const int64_t o = d.origin[v];
-                    pre[3 * k + 2] = uint64_t(d.touched_mark[v] == s.batch_id ? o : -int64_t(v) - 2);
-                }
-                const uint32_t mm = __match_any_sync(FULLM, v);
-                const uint32_t below = mm & ((1u << lane) - 1u);
-                const uint32_t above = mm & ~((2u << lane) - 1u);
-                // last earlier visit: in this chunk, else from the hash (earlier chunks)
-                int prev = below ? int(base) + 31 - __clz(int(below)) : -1;
-                uint32_t hpos = hslot(v), hfound = X_EMPTY;
-                if (valid && !below) {
-                    for (;;) {
-                        const uint32_t e = hsh[hpos];
-                        if (e == X_EMPTY) break;
-                        if ((e >> 9) == v) {
-                            hfound = hpos;
-                            prev = int(e & 511u);
-                            break;
-                        }
-                        hpos = hpos + 1 == X_HS ? 0 : hpos + 1;
-                    }
-                }
-                // f(k) = item carried out of hop k = srck[k + 1]:
-                // prev < 0 -> k; else srck[prev] (known when prev <= base, else f(prev - 1) in this chunk)
-                int cur = int(k), res = -3;  // -3 pending
-                bool pend = valid;
-                while (__any_sync(FULLM, pend)) {
-                    const int p = __shfl_sync(FULLM, prev, (cur - int(base)) & 31);
-                    if (pend) {
-                        if (p < 0) {
-                            res = cur;
-                            pend = false;
-                        } else if (p <= int(base)) {
-                            res = srck[p] == NONE16 ? -1 : int(srck[p]);
-                            pend = false;
-                        } else {
-                            cur = p - 1;
-                        }
-                    }
-                }
-                if (valid) srck[k + 1] = res < 0 ? NONE16 : uint16_t(res);
-                // record the last visit of each slot of this chunk
-                if (valid && above == 0) {
-                    const uint32_t ent = v << 9 | k;
-                    if (hfound != X_EMPTY) {
-                        hsh[hfound] = ent;
-                    } else {
-                        uint32_t q = hslot(v);
-                        for (;;) {
-                            const uint32_t old = atomicCAS(&hsh[q], X_EMPTY, ent);
-                            if (old == X_EMPTY) break;
-                            if ((old >> 9) == v) {  // seen in an earlier chunk and earlier in this one
-                                hsh[q] = ent;
-                                break;
-                            }
-                            q = q + 1 == X_HS ? 0 : q + 1;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-            for (uint32_t k = lane; k <= h; k += 32) {
-                const uint16_t src = srck[k];
-                uint32_t slot;
-                if (k < h) {
-                    slot = chain[k];
-                    uint32_t q = hslot(slot), e;
-                    while ((e = hsh[q]) >> 9 != slot) q = q + 1 == X_HS ? 0 : q + 1;
-                    if ((e & 511u) != k) continue;  // not the last visit of this slot
-                } else {
-                    slot = final_slot;
-                }
-                uint32_t c1 = b1, c2 = b2;
-                uint64_t cst = stamp;
-                int64_t corg = int64_t(i);
-                if (src != NONE16) {
-                    const uint64_t bb = pre[3 * src];
-                    c1 = uint32_t(bb);
-                    c2 = uint32_t(bb >> 32);
-                    cst = pre[3 * src + 1];
-                    corg = int64_t(pre[3 * src + 2]);
-                }
-                if (slot == FULLM) {  // the dropped item leaves the FIFO
-                    d.fifo[cst & fmask] = -1;
-                    continue;
-                }
-                d.beta1[slot] = c1;
-                d.beta2[slot] = c2;
-                d.stamp[slot] = cst;
-                d.fifo[cst & fmask] = int64_t(slot);
-                touch_store(slot, corg);
-            }
-            __syncwarp();
-            }
-                };
-        auto resolve_pending = [&]() {
-            if (pend_chain) {
-                resolve_chain();
-                pend_chain = false;
-            }
+        auto drain = [&]() {  // every handed-off chain resolved (its metadata written)
+            wait_zero(0);
+            wait_zero(1);
+            wait_zero(2);
         };
 
         // the sequential path (warp-redundant: every lane runs it with the same values)
         auto insert_one = [&](uint64_t i, uint32_t b1, uint32_t b2) -> bool {
-            resolve_pending();  // the previous chain's metadata before this insert reads any
             if (dr_hi - s.rng_block < X_NEED) {
                 refill();
                 if (dr_hi - s.rng_block < X_NEED) {
@@ -423,6 +439,7 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
             uint32_t dropped = 0, gc = 0, disp = 0;
             s.writes++;                     // :62
             if (s.live == d.capacity) {     // :64-69 FIFO GC of the oldest entry
+                drain();                    // it reads and clears metadata a pending chain writes
                 while (d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
                 const uint32_t f = uint32_t(d.fifo[s.fifo_head & fmask]);
                 used_bits[f >> 5] &= ~(1u << (f & 31));  // clear() (:48-54)
@@ -438,8 +455,10 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 __syncwarp();
             }
             const uint64_t stamp = s.next_stamp++;  // :71
-            if (stamp - s.fifo_head >= d.fifo_cap)  // dead entries at the head never matter again
+            if (stamp - s.fifo_head >= d.fifo_cap) {  // dead entries at the head never matter again
+                drain();
                 while (s.fifo_head < stamp && d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
+            }
             if (stamp - s.fifo_head >= d.fifo_cap) {
                 s.writes--;
                 s.next_stamp--;
@@ -466,10 +485,7 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 uint32_t be = uniform(2) == 0 ? b1 : b2;
                 uint32_t calt = b1 ^ b2;  // alternate-bucket key of the carried item
                 uint32_t h = 0, final_slot = FULLM;
-                // lane k < 32 prefetches the pre-chain content of chain[k] into shared
-                // memory while the walk goes on (nothing is written to the global
-                // metadata during the walk); cp.async keeps the registers free
-                const uint32_t pre_sm = smem_base + uint32_t(L.o_pre) + lane * 32;
+                uint32_t myv = 0;  // lane k < 32 logs chain[k]; longer chains go to chain[]
                 for (;; ++h) {
                     const uint64_t dnext = ring[s.rng_block & (X_RING - 1)];  // issued before the test
                     const uint32_t fm = free_mask(be);
@@ -489,13 +505,14 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                         vs = uint32_t(uniform(depth));
                     }
                     const uint32_t vf = be * depth + vs;
-                    chain[h] = vf;
-                    if (h < 32 && lane == h) {
-                        cp_async_ca<8>(pre_sm, d.stamp + vf);
-                        cp_async_ca<8>(pre_sm + 8, d.origin + vf);
-                        cp_async_ca<4>(pre_sm + 16, d.beta1 + vf);
-                        cp_async_ca<4>(pre_sm + 20, d.beta2 + vf);
-                        cp_async_ca<4>(pre_sm + 24, d.touched_mark + vf);
+                    if (h < 32) {
+                        if (lane == h) myv = vf;
+                    } else {
+                        if (h == 32) {  // chain[] is free once warp 1 is done with the last long chain
+                            wait_zero(2);
+                            chain[lane] = myv;
+                        }
+                        chain[h] = vf;
                     }
                     const uint32_t va = alt_swap(vf, calt);  // the victim's key; the carry takes the slot
                     calt = va;
@@ -503,16 +520,25 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 }
                 disp = final_slot == FULLM ? XPIR_MAX_DISPLACEMENTS_DEV : h;
                 dropped = final_slot == FULLM ? 1u : 0u;
+                // hand the chain to warp 1, which writes its metadata while this warp goes
+                // on (the walk itself reads only on-chip state)
+                wait_zero(wslot);
+                XRec& r = recs[wslot];
+                r.v[lane] = myv;
+                if (lane == 0) {
+                    r.h = h;
+                    r.final_slot = final_slot;
+                    r.b1 = b1;
+                    r.b2 = b2;
+                    r.stamp = stamp;
+                    r.i = i;
+                    if (h > 32) qflag[2] = 1;
+                }
                 __syncwarp();
-                // the chain's metadata is resolved later (before the next chain or at the
-                // end of the launch), so its prefetches have long landed by then
-                pend_chain = true;
-                p_h = h;
-                p_final = final_slot;
-                p_b1 = b1;
-                p_b2 = b2;
-                p_stamp = stamp;
-                p_i = i;
+                __threadfence_block();
+                if (lane == 0) qflag[wslot] = 1;
+                __syncwarp();
+                wslot ^= 1;
             }
             if (reports && lane == 0) reinterpret_cast<uint4*>(reports)[i] = make_uint4(1, dropped, gc, disp);
             return true;
@@ -586,10 +612,38 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 }
             }
         }
-        resolve_pending();
+        drain();
+        if (lane == 0) qflag[3] = 1;  // done: warp 1 exits
         s.resume_at = c;
         if (lane == 0) *gst = s;
         __threadfence_block();
+    } else if (warp == 1) {
+        // the resolver: chains in hand-off order
+        uint32_t rslot = 0;
+        for (;;) {
+            uint32_t full;
+            while ((full = qflag[rslot]) == 0) {
+                if (qflag[3]) {
+                    full = qflag[rslot];
+                    break;
+                }
+                __nanosleep(32);
+            }
+            __syncwarp();
+            if (full == 0) break;
+            __threadfence_block();
+            const XRec& r = recs[rslot];
+            const bool lng = r.h > 32;
+            resolve_chain(r);
+            __syncwarp();
+            __threadfence_block();
+            if (lane == 0) {
+                if (lng) qflag[2] = 0;
+                qflag[rslot] = 0;
+            }
+            __syncwarp();
+            rslot ^= 1;
+        }
     }
     __syncthreads();
     // occupancy back to the byte map; touched list rebuilt from the marks
