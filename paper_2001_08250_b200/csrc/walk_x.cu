@@ -106,11 +106,13 @@ bool walk_x_supported(const CuckooDev& d) {
            XLayout(uint32_t(slots)).total <= 232448;
 }
 
+// DEP != 0: compile-time bucket depth (4 at every BASELINE config).
+template <uint32_t DEP>
 __global__ void __launch_bounds__(256, 1)
 k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __restrict__ beta1,
                 const uint32_t* __restrict__ beta2, uint64_t i0, uint64_t n, uint32_t* __restrict__ reports) {
     extern __shared__ __align__(16) uint8_t smx[];
-    const uint32_t slots = d.buckets * d.depth;
+    const uint32_t slots = d.buckets * (DEP ? DEP : d.depth);
     const XLayout L(slots);
     uint64_t* ring = reinterpret_cast<uint64_t*>(smx + L.o_ring);
     uint16_t* alt = reinterpret_cast<uint16_t*>(smx + L.o_alt);
@@ -148,7 +150,7 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
     const uint32_t tbase = use_tm ? *reinterpret_cast<const uint32_t*>(smx + L.o_taddr) : 0u;
 
     CuckooState s = *gst;
-    const uint32_t depth = d.depth;
+    const uint32_t depth = DEP ? DEP : d.depth;
     const uint64_t fmask = d.fifo_cap - 1;
     XRec* recs = reinterpret_cast<XRec*>(smx + L.o_q);
     volatile uint32_t* qflag = reinterpret_cast<volatile uint32_t*>(smx + L.o_qf);
@@ -691,9 +693,10 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
 cudaError_t launch_cuckoo_walk_x(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
                                  uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s) {
     const XLayout L(uint32_t(uint64_t(d.buckets) * d.depth));
-    cudaError_t e = cudaFuncSetAttribute(k_cuckoo_walk_x, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
+    auto k = d.depth == 4 ? k_cuckoo_walk_x<4> : k_cuckoo_walk_x<0>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.total));
     if (e != cudaSuccess) return e;
-    k_cuckoo_walk_x<<<1, 256, L.total, s>>>(d, st, beta1, beta2, i0, n, reports);
+    k<<<1, 256, L.total, s>>>(d, st, beta1, beta2, i0, n, reports);
     return cudaGetLastError();
 }
 
