@@ -490,6 +490,11 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 uint32_t myv = 0;  // lane k < 32 logs chain[k]; longer chains go to chain[]
                 for (;; ++h) {
                     const uint64_t dnext = ring[s.rng_block & (X_RING - 1)];  // issued before the test
+                    // power-of-two depth: the victim slot is known before the occupancy
+                    // test, so its shared-memory alt entry is read alongside it
+                    const uint32_t vf_spec = be * depth + (uint32_t(dnext) & (depth - 1));
+                    const bool spec = dpow2 && vf_spec < X_SM_SLOTS;
+                    const uint32_t va_spec = spec ? alt[vf_spec] : 0u;
                     const uint32_t fm = free_mask(be);
                     if (fm) {
                         final_slot = be * depth + uint32_t(__ffs(int(fm)) - 1);
@@ -516,7 +521,13 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                         }
                         chain[h] = vf;
                     }
-                    const uint32_t va = alt_swap(vf, calt);  // the victim's key; the carry takes the slot
+                    uint32_t va;  // the victim's key; the carry takes the slot
+                    if (spec) {
+                        alt[vf] = uint16_t(calt);
+                        va = va_spec;
+                    } else {
+                        va = alt_swap(vf, calt);
+                    }
                     calt = va;
                     be ^= va;  // :118 (beta1 ^ beta2 ^ be is the victim's other bucket)
                 }
