@@ -170,8 +170,8 @@ int xpir_probe_tmem(int device, int variant, double* bytes_per_clk_sm);
 /* the GPU"): concurrent single-request callers — server::answer_share       */
 /* (server.cpp:115-135) from node.cpp's session/link threads — are coalesced  */
 /* into one scan. A batch is sealed when it holds max_batch requests or       */
-/* max_wait_us after its first request; two pinned batches alternate (one     */
-/* forming while the other is scanned). Callers pack their own query and      */
+/* max_wait_us after its first request; three pinned batches rotate (one    */
+/* forming, one scanning, one completing). Callers pack their own query and */
 /* unpack their own answer. Thread-safe; the store must outlive the batcher.  */
 /* ------------------------------------------------------------------------ */
 typedef struct xpir_batcher xpir_batcher;
