@@ -144,7 +144,8 @@ typedef struct {
                           4 = M4RM register accumulators, 5 = M4RM half-TMEM accumulators,
                           6 = warp-private nibble tables, 7 = M4RM nibble tables,
                           8 = M4RM quad-interleaved 32-byte-column tables with full-TMEM
-                              accumulators (auto for B >= 2048, S % 32 == 0) */
+                              accumulators (auto for B >= 2048, S % 32 == 0),
+                          9 = M4RM 6-bucket tables (64 rows per 6 buckets) */
     int ctas_per_sm;   /* 0 = auto */
     int reserved[6];
 } xpir_scan_opts;

@@ -302,6 +302,11 @@ static uint32_t g_nib_min_batch = 0xffffffffu;
 static uint32_t g_k4_min_batch = 24;   // nibble-table M4RM (kernel 7) from here
 static uint32_t g_m4_min_batch = 257;  // byte-table M4RM (kernels 2/5) from here
 static uint32_t g_q_min_batch = 2048;  // quad-table full-TMEM M4RM (kernel 8) from here
+// 6-bucket-table M4RM (kernel 9) for B in [129, 256]: 6-15% faster than the
+// nibble tables there (1 GiB store, S = 1024/4096: B = 256 1.96 vs 2.30 ms);
+// past 256 its request tiles split and the byte tables win
+static uint32_t g_k6_min_batch = 129;
+static uint32_t g_k6_max_batch = 256;
 
 static int choose_kernel(const xpir_store* st, uint32_t B) {
     int k;
@@ -320,9 +325,11 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
             const double c5 = m4_ok ? double((uint64_t(B) + 2047) / 2048 * 2048) / 3.0 : 1e300;
             return m4rm_q_cost(B, nullptr) < c5 ? 8 : 2;
         }
-        k = !m4_ok ? 1 : B >= g_m4_min_batch ? 2 : B >= g_k4_min_batch ? 7 : B >= g_nib_min_batch ? 6 : 1;
+        k = !m4_ok ? 1
+            : (B >= g_k6_min_batch && B <= g_k6_max_batch) ? 9
+            : B >= g_m4_min_batch ? 2 : B >= g_k4_min_batch ? 7 : B >= g_nib_min_batch ? 6 : 1;
     }
-    if ((k == 2 || k == 6 || k == 7) && !m4_ok) k = 1;
+    if ((k == 2 || k == 6 || k == 7 || k == 9) && !m4_ok) k = 1;
     if (k == 8 && !q_ok) k = 1;
     return k;
 }
@@ -343,6 +350,14 @@ static int run_m4(xpir_store* st, const uint8_t* qT, uint64_t qstride, uint32_t 
         timing_end(s, ev);
         count_launches(1);
         g_last_kernel = 8;
+        return XPIR_OK;
+    }
+    if (kernel == 9) {  // 6-bucket tables
+        timing_begin(s, &ev);
+        XCK(launch_scan_m4rm6(a, num_sms(st->device)));
+        timing_end(s, ev);
+        count_launches(1);
+        g_last_kernel = 9;
         return XPIR_OK;
     }
     if (kernel == 7) {  // nibble tables
@@ -400,7 +415,7 @@ static int scan_rows(xpir_store* st, const uint8_t* rows, uint64_t stride, uint3
     if (B == 0) return XPIR_OK;
     const int k = choose_kernel(st, B);
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
-    if (k != 2 && k != 7 && k != 8) return run_rows(st, k, rows + blo, stride, B, d_out, s);
+    if (k != 2 && k != 7 && k != 8 && k != 9) return run_rows(st, k, rows + blo, stride, B, d_out, s);
     const uint64_t qs = m4rm_qstride(B);
     DevBuf& qw = st->qwin_for(s);
     XCK(qw.ensure(m4rm_qrows(nbw) * qs));
@@ -436,7 +451,7 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
     // K2: expand only this shard's window of every request's selection vector,
     // straight into the layout the chosen scan kernel reads.
-    if (k == 2 || k == 7 || k == 8) {
+    if (k == 2 || k == 7 || k == 8 || k == 9) {
         const uint64_t qs = m4rm_qstride(B);
         DevBuf& qw = st->qwin_for(s);
         XCK(qw.ensure(m4rm_qrows(nbw) * qs));
@@ -481,7 +496,7 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
     count_launches(1);
     const int k = choose_kernel(st, B);
     int rc;
-    if (k == 2 || k == 7 || k == 8) {
+    if (k == 2 || k == 7 || k == 8 || k == 9) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
         XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s, k == 8));
@@ -549,7 +564,7 @@ int xpir_answer_batch_mixed(xpir_store* st, uint32_t B, const uint8_t* is_seed, 
     count_launches(1);
     const int k = choose_kernel(st, B);
     int rc;
-    if (k == 2 || k == 7 || k == 8) {
+    if (k == 2 || k == 7 || k == 8 || k == 9) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
         XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s, k == 8));

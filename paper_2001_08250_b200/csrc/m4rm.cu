@@ -318,7 +318,11 @@ cudaError_t launch_scan_m4rm(const M4Args& a, int ctas_per_sm, int num_sms, int 
 }
 
 uint64_t m4rm_qstride(uint32_t B) { return (uint64_t(B) + 15) & ~uint64_t(15); }
-uint64_t m4rm_qrows(uint64_t n_groups) { return (n_groups + 15) & ~uint64_t(15); }
+// rows of the group-major query layout: a multiple of 48 covers the 16-byte
+// chunks of the nibble kernel, the 12-byte chunks of the 6-bucket kernel and
+// the 4-byte sets of the quad kernel (rows past the vector are never selected:
+// they map to zero-filled buckets)
+uint64_t m4rm_qrows(uint64_t n_groups) { return (n_groups + 47) / 48 * 48; }
 
 cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
                             uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4) {

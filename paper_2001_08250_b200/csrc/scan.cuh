@@ -56,6 +56,7 @@ cudaError_t launch_scan_m4rm_q(const M4Args& a, int num_sms);
 int m4rm_q_tile(uint32_t B);
 double m4rm_q_cost(uint32_t B, int* tile);  // vs the half-TMEM kernel: ceil(B/2048)*2048/3.0
 cudaError_t launch_scan_m4rm4(const M4Args& a, int num_sms);  // nibble tables (m4rm4.cu)
+cudaError_t launch_scan_m4rm6(const M4Args& a, int num_sms);  // 6-bucket tables (m4rm6.cu)
 uint64_t m4rm_qstride(uint32_t B);
 uint64_t m4rm_qrows(uint64_t n_groups);  // rows to allocate (staging reads 16-row chunks)
 // set4 = true: the set-interleaved layout of k_scan_m4rm_q (kernel 8)

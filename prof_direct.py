@@ -15,12 +15,12 @@ for S in (4096, 512):
     st = xp.Store(N, S)
     st.fill_keystream(bytes(32), 0)
     cs = torch.cuda.current_stream()
-    for B in (4, 8, 12, 16, 24, 32, 48, 64):
+    for B in (4, 8, 12, 16, 24, 32, 48, 64, 96, 128, 192, 256, 384, 512):
         q = torch.randint(0, 256, (B, N // 8), dtype=torch.uint8, device='cuda')
         out = torch.empty((B, S), dtype=torch.uint8, device='cuda')
         ref = None
         row = [S, B]
-        for k in (0, 1, 6, 7):
+        for k in (0, 1, 6, 7, 9):
             xp.set_scan_opts(k)
             ts = []
             for r in range(5):

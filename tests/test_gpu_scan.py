@@ -50,7 +50,7 @@ def test_full_retrieval_every_target(xp, port, cuda):
             assert np.array_equal(np.bitwise_xor.reduce(ans, axis=0), db.reshape(N, S)[beta])
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6, 7])
+@pytest.mark.parametrize("kernel", [1, 2, 6, 7, 9])
 @pytest.mark.parametrize("N,S,B", [
     (8, 128, 1), (9, 128, 3), (1000, 256, 97), (1024, 4096, 64), (777, 512, 130),
     (4096, 128, 1), (2048, 1024, 513), (4000, 2048, 1025), (256, 32768, 40), (12345, 128, 300),
@@ -86,6 +86,28 @@ def test_direct_every_small_batch(xp, port, cuda, S):
         assert xp.last_scan_kernel() == 1
 
 
+@pytest.mark.parametrize("N,S,B", [(1, 128, 5), (97, 128, 64), (96, 256, 129), (191, 128, 256), (4099, 384, 300),
+                                   (20000, 128, 257), (777, 1024, 1000)])
+def test_six_bucket_tables_match_oracle(xp, port, cuda, N, S, B):
+    """Kernel 9: 24-bit query units split into four 6-bucket groups; bucket counts
+    ending mid-group, mid-unit and mid-chunk (96), 1/2/4-request lane tiles and
+    partial request tiles."""
+    g = np.random.default_rng(N * 3 + S + B)
+    db = rand(g, N * S)
+    q = rand(g, B, (N + 7) // 8)
+    if N % 8:
+        q[:, -1] &= (1 << (N % 8)) - 1
+    xp.set_scan_opts(9)
+    st = xp.Store(N, S)
+    st.upload(db)
+    got = st.answer_batch(q)
+    assert xp.last_scan_kernel() == 9
+    assert np.array_equal(got, port.answer_batch(db, N, S, q, B))
+    if S % 128 == 0 and 129 <= B <= 256:  # the automatic choice in its batch range
+        xp.set_scan_opts(0)
+        assert np.array_equal(st.answer_batch(q), got) and xp.last_scan_kernel() == 9
+
+
 def test_dirty_trailing_bits_are_ignored(xp, port, cuda):
     # pir::answer only reads bits j < N (pir.cpp:33-34)
     N, S, B = 1001, 256, 200
@@ -95,7 +117,7 @@ def test_dirty_trailing_bits_are_ignored(xp, port, cuda):
     q[:, -1] |= 0xFE
     st = xp.Store(N, S)
     st.upload(db)
-    for k in (1, 2, 6, 7):
+    for k in (1, 2, 6, 7, 9):
         xp.set_scan_opts(k)
         assert np.array_equal(st.answer_batch(q), port.answer_batch(db, N, S, q, B))
 
