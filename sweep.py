@@ -26,13 +26,36 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
+def summarize(path: str) -> None:
+    """The tables of profiles/r01_config5_sweep_summary.txt from a sweep jsonl."""
+    rows = [json.loads(l) for l in open(path)][1:]
+    shapes = sorted({(r["slot"], r["depth"]) for r in rows})
+    bs = sorted({r["B"] for r in rows})
+    at = {(r["slot"], r["depth"], r["B"]): r for r in rows}
+    print("# config 5: 1 GiB DetRng(5) store, slot x depth shapes, B explicit DetRng(55) vectors; sweep.py (current dispatch)")
+    print("# fraction of the HBM-or-ALU roofline max(T_hbm, T_alu)/T (T_alu = dense select-XOR LOP3s / measured LOP3 rate)")
+    print("shape    " + "".join(f"{b:>7d}" for b in bs))
+    for sl, dp in shapes:
+        print(f"{sl:4d}x{dp:<3d}" + "".join(f"{at[(sl, dp, b)]['roofline_frac']:7.2f}" for b in bs))
+    print("# requests/s (thousands)")
+    for sl, dp in shapes:
+        print(f"{sl:4d}x{dp:<3d}" + "".join(f"{at[(sl, dp, b)]['requests_per_s'] / 1e3:7.1f}" for b in bs))
+    ks = [at[(shapes[-1][0], shapes[-1][1], b)]["kernel"] for b in bs]
+    print("# kernel used (1 direct, 7 m4rm nibble tables, 9 m4rm 6-bucket tables, 2 m4rm byte tables/registers, "
+          "5 byte tables/half TMEM, 8 quad tables/full TMEM): " + str(ks))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--max-batch", type=int, default=16384)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_config5_sweep.jsonl"))
     ap.add_argument("--slots", default="256,512,1024,2048,4096")
     ap.add_argument("--depths", default="2,4,8")
+    ap.add_argument("--summary", default=None, help="print the fraction / req/s / kernel tables of a sweep jsonl")
     args = ap.parse_args()
+    if args.summary:
+        summarize(args.summary)
+        return
 
     import torch
 
