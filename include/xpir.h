@@ -351,6 +351,10 @@ int xpir_server_apply_round_sharded(xpir_server* sv, const uint32_t* beta1, cons
                                     uint64_t n, int seal_after, const xpir_shard_map* map,
                                     void (*barrier)(void*), void* barrier_ctx, uint32_t* reports,
                                     uint64_t* sealed_epoch);
+/* Server start-up: size the per-round scratch for rounds of up to max_batch
+ * writes and allocate every sealed image of the ring up front, so a round never
+ * allocates device memory. */
+int xpir_server_reserve(xpir_server* sv, uint64_t max_batch);
 int xpir_server_seal(xpir_server* sv, uint64_t* epoch);            /* seal_epoch, server.cpp:75-81 */
 /* snapshot_at (server.cpp:83-87); epoch 0 = latest. The store stays owned by the
  * server and valid until its epoch leaves the ring. */

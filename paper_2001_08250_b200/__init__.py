@@ -137,6 +137,7 @@ _SIGS = {
     "xpir_server_destroy": ([_vp], C.c_int),
     "xpir_server_apply_round": ([_vp, _u32p, _u32p, _u8p, _u32p, C.c_uint32, C.c_uint64, C.c_int, _u32p, _u64p],
                                 C.c_int),
+    "xpir_server_reserve": ([_vp, C.c_uint64], C.c_int),
     "xpir_server_seal": ([_vp, _u64p], C.c_int),
     "xpir_server_snapshot": ([_vp, C.c_uint64, C.POINTER(_vp)], C.c_int),
     "xpir_server_info": ([_vp, _u64p, _u64p, _u64p, C.POINTER(_vp), C.POINTER(_vp)], C.c_int),
@@ -841,6 +842,11 @@ class Server:
                 pos.shape[1] if n else 0, n, 1 if seal_after else 0, C.cast(C.pointer(smap), _vp),
                 C.cast(cb, _vp), None, _p(rep, _u32p), C.byref(ep)))
         return rep[:n], ep.value
+
+    def reserve(self, max_batch: int) -> None:
+        """Server start-up: per-round scratch for rounds of up to max_batch writes and
+        every sealed image of the ring allocated now (no allocation inside a round)."""
+        _check(lib().xpir_server_reserve(self.h, max_batch))
 
     def seal(self) -> int:
         ep = C.c_uint64()

@@ -68,12 +68,15 @@ inline int num_sms(int dev) {
 struct DevBuf {
     void* p = nullptr;
     size_t cap = 0;
+    // grows geometrically (x1.5): a buffer sized by a per-round count that creeps
+    // up (e.g. touched slots) is reallocated O(log) times, not every round —
+    // cudaFree/cudaMalloc inside a round can stall for milliseconds or more
     cudaError_t ensure(size_t n) {
         if (n <= cap) return cudaSuccess;
         if (p) cudaFree(p);
         p = nullptr;
+        size_t want = std::max({n, size_t(256), cap + cap / 2});
         cap = 0;
-        size_t want = std::max(n, size_t(256));
         cudaError_t e = cudaMalloc(&p, want);
         if (e == cudaSuccess) cap = want;
         return e;
@@ -208,7 +211,8 @@ struct xpir_server {
         uint32_t since_batch;  // table batch id the image is synchronised with
         xpir_store* st;
     };
-    std::deque<Sealed> ring;  // oldest first
+    std::deque<Sealed> ring;           // oldest first
+    std::vector<xpir_store*> spare;    // pre-allocated images (xpir_server_reserve)
     std::mutex mu;
 };
 

@@ -18,8 +18,14 @@ static int server_seal(xpir_server* sv, uint64_t* epoch_out) {  // server.cpp:75
                                     t->stream));
         count_launches(1);
     } else {
-        int rc = xpir_store_create(sv->device, t->d.buckets, uint32_t(t->d.depth * t->d.item), t->lo, t->hi, &e.st);
-        if (rc) return rc;
+        if (!sv->spare.empty()) {
+            e.st = sv->spare.back();
+            sv->spare.pop_back();
+        } else {
+            int rc = xpir_store_create(sv->device, t->d.buckets, uint32_t(t->d.depth * t->d.item), t->lo, t->hi,
+                                       &e.st);
+            if (rc) return rc;
+        }
         XCK(cudaMemcpyAsync(e.st->data, t->data, e.st->bytes(), cudaMemcpyDeviceToDevice, t->stream));
     }
     XCK(cudaStreamSynchronize(t->stream));
@@ -67,6 +73,7 @@ int xpir_server_create_shard(int device, uint32_t buckets, uint32_t depth, uint6
 int xpir_server_destroy(xpir_server* sv) {
     if (!sv) return XPIR_OK;
     for (auto& e : sv->ring) xpir_store_destroy(e.st);
+    for (auto* st : sv->spare) xpir_store_destroy(st);
     xpir_table_destroy(sv->table);
     xpir_window_destroy(sv->window);
     delete sv;
@@ -152,6 +159,21 @@ int xpir_server_apply_round_sharded(xpir_server* sv, const uint32_t* beta1, cons
     }
     if (ok < n) return fail(XPIR_EINVAL, "write targets a bucket outside the table");
     if (seal_after) return server_seal(sv, sealed_epoch);
+    return XPIR_OK;
+}
+
+int xpir_server_reserve(xpir_server* sv, uint64_t max_batch) {
+    if (!sv) return fail(XPIR_EINVAL, "server_reserve: null server");
+    std::lock_guard<std::mutex> lk(sv->mu);
+    int rc = xpir_table_reserve(sv->table, max_batch);
+    if (rc) return rc;
+    xpir_table* t = sv->table;
+    while (sv->ring.size() + sv->spare.size() < sv->epoch_ring) {
+        xpir_store* st = nullptr;
+        rc = xpir_store_create(sv->device, t->d.buckets, uint32_t(t->d.depth * t->d.item), t->lo, t->hi, &st);
+        if (rc) return rc;
+        sv->spare.push_back(st);
+    }
     return XPIR_OK;
 }
 

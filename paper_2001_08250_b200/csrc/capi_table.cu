@@ -242,7 +242,9 @@ int xpir_table_reserve(xpir_table* t, uint64_t max_batch) {
     if (!t) return fail(XPIR_EINVAL, "table_reserve: null table");
     std::lock_guard<std::mutex> lk(t->mu);
     DeviceGuard g(t->device);
-    const uint64_t n = std::min<uint64_t>(max_batch, t->slots());
+    // a round touches its new items' slots plus the slots of the items its
+    // eviction chains move: sized for twice the batch (capped at the table)
+    const uint64_t n = std::min<uint64_t>(2 * max_batch + 1024, t->slots());
     XCK(t->gather.ensure(n * t->d.item));
     XCK(t->in_b1.ensure(4 * max_batch));
     XCK(t->in_b2.ensure(4 * max_batch));

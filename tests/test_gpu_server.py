@@ -16,6 +16,8 @@ def test_server_rounds_and_epoch_ring(xp, port, cuda, nb, depth, item, ring, R):
     seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
     cap = nb * depth * 3 // 4
     sv = xp.Server(nb, depth, cap, item, seed, m, h, W, R, ring)
+    if ring != 2:  # start-up reservation: pre-allocated ring images are used in order
+        sv.reserve(3 * cap // 4)
     T = port.table(nb, depth, cap, item, seed)
     PW = port.window(m, h, W)
     PW.rotate()  # server.cpp:40
