@@ -310,6 +310,16 @@ int xpir_window_encode_delta(xpir_window* win, uint64_t i, uint8_t* out, uint64_
  * be NULL (size query). */
 int xpir_encode_delta_dev(int device, const uint64_t* d_words, uint32_t m_bits, uint8_t* d_out, uint64_t cap,
                           uint64_t* len, void* stream);
+/* The write's interest field (wire.cpp:154-169, INTEREST_FIELD_LEN = 64 bytes):
+ * notify::encode_positions (notify.cpp:182-196) of n writes x h positions into
+ * cap-byte fields (d_ok[i] = 0 where the reference throws: the encoding is longer
+ * than cap — at m = 2^20, h = 23 about a fifth are), and notify::decode_positions
+ * (notify.cpp:198-214): d_count[i] = count, positions in d_pos[i*cap ...], or
+ * 0xffffffff for std::nullopt. h <= 128, cap <= 4096. */
+int xpir_encode_positions_dev(int device, const uint32_t* d_pos, uint32_t h, uint64_t n, uint32_t cap,
+                              uint8_t* d_fields, uint8_t* d_ok, void* stream);
+int xpir_decode_positions_dev(int device, const uint8_t* d_fields, uint32_t cap, uint64_t n, uint32_t* d_pos,
+                              uint32_t* d_count, void* stream);
 /* notify::decode_delta (notify.cpp:151-170), decoded on device. XPIR_EINVAL is the
  * reference's std::nullopt (malformed input). words == NULL: header only
  * (*m_bits); else words receives ceil(m/64) words (EINVAL if words_cap is short). */

@@ -104,6 +104,10 @@ class Port:
         L.xo_encode_delta.restype = C.c_uint64
         L.xo_decode_delta.argtypes = [_u8p, C.c_uint64, _u32p, _u64p, C.c_uint64]
         L.xo_decode_delta.restype = C.c_int
+        L.xo_encode_positions.argtypes = [_u32p, C.c_uint32, _u8p, C.c_uint64]
+        L.xo_encode_positions.restype = C.c_uint64
+        L.xo_decode_positions.argtypes = [_u8p, C.c_uint64, _u32p, C.c_uint32, _u32p]
+        L.xo_decode_positions.restype = C.c_int
 
     # primitives
     def chacha20(self, key: bytes, nonce: bytes, n: int, block0: int = 0) -> bytes:
@@ -185,6 +189,23 @@ class Port:
         w = np.zeros((m.value + 63) // 64, np.uint64)
         self.lib.xo_decode_delta(_p(b), len(buf), C.byref(m), _p(w, _u64p), len(w))
         return m.value, w
+
+    # write interest field (notify.cpp:182-214, wire.cpp:154-169)
+    def encode_positions(self, positions, cap: int = 64):
+        """The cap-byte field, or None where the reference throws (too long)."""
+        p = np.ascontiguousarray(positions, np.uint32)
+        out = np.zeros(max(cap, 1), np.uint8)
+        n = self.lib.xo_encode_positions(_p(p, _u32p), len(p), _p(out), cap)
+        return None if n > cap else out[:cap].tobytes()
+
+    def decode_positions(self, buf: bytes):
+        """Positions, or None (the reference's nullopt)."""
+        b = _u8(buf) if len(buf) else np.zeros(1, np.uint8)
+        out = np.zeros(max(8 * len(buf), 1), np.uint32)
+        cnt = C.c_uint32()
+        if not self.lib.xo_decode_positions(_p(b), len(buf), _p(out, _u32p), len(out), C.byref(cnt)):
+            return None
+        return out[:cnt.value].copy()
 
 
 class PortRng:
@@ -362,6 +383,10 @@ class Ref:
         L.ref_encode_delta.restype = C.c_int64
         L.ref_decode_delta.argtypes = [_u8p, C.c_uint64, _u32p, _u64p, C.c_uint64]
         L.ref_decode_delta.restype = C.c_int
+        L.ref_encode_positions.argtypes = [_u32p, C.c_uint64, _u8p, C.c_uint64]
+        L.ref_encode_positions.restype = C.c_int64
+        L.ref_decode_positions.argtypes = [_u8p, C.c_uint64, _u32p, C.c_uint32, _u32p]
+        L.ref_decode_positions.restype = C.c_int
         L.ref_window_digest_n.argtypes = [C.c_void_p, C.c_uint64, _u8p]
 
     def _chk(self, rc):
@@ -440,6 +465,20 @@ class Ref:
         w = np.zeros((m.value + 63) // 64, np.uint64)
         self.lib.ref_decode_delta(_p(b), len(buf), C.byref(m), _p(w, _u64p), len(w))
         return m.value, w
+
+    def encode_positions(self, positions, cap: int = 64):
+        p = np.ascontiguousarray(positions, np.uint32)
+        out = np.zeros(max(cap, 1), np.uint8)
+        n = self.lib.ref_encode_positions(_p(p, _u32p) if len(p) else None, len(p), _p(out), cap)
+        return None if n < 0 else out[:cap].tobytes()
+
+    def decode_positions(self, buf: bytes):
+        b = _u8(buf) if len(buf) else np.zeros(1, np.uint8)
+        out = np.zeros(max(8 * len(buf), 1), np.uint32)
+        cnt = C.c_uint32()
+        if not self.lib.ref_decode_positions(_p(b), len(buf), _p(out, _u32p), len(out), C.byref(cnt)):
+            return None
+        return out[:cnt.value].copy()
 
 
 class RefRng:

@@ -300,6 +300,25 @@ int ref_decode_delta(const uint8_t* buf, uint64_t len, uint32_t* m, uint64_t* wo
     if (words && d->words.size() <= words_cap) std::memcpy(words, d->words.data(), d->words.size() * 8);
     return 1;
 }
+// notify::encode_positions: encoded length, or -1 when the reference throws
+// (the field capacity is exceeded); out receives the cap-byte field
+int64_t ref_encode_positions(const uint32_t* positions, uint64_t n, uint8_t* out, uint64_t cap) {
+    try {
+        bytes enc = notify::encode_positions(std::span<const uint32_t>(positions, n), cap);
+        std::memcpy(out, enc.data(), enc.size());
+        return int64_t(enc.size());
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+// notify::decode_positions: 1 ok (count, positions when they fit), 0 nullopt
+int ref_decode_positions(const uint8_t* buf, uint64_t len, uint32_t* out, uint32_t max_out, uint32_t* count) {
+    auto p = notify::decode_positions(byte_view(buf, len));
+    if (!p) return 0;
+    *count = uint32_t(p->size());
+    for (size_t i = 0; i < p->size() && i < max_out; ++i) out[i] = (*p)[i];
+    return 1;
+}
 void ref_window_digest_n(void* w, uint64_t count, uint8_t* out32) {
     auto d = static_cast<notify::Window*>(w)->digest(count);
     std::memcpy(out32, d.data(), 32);

@@ -628,6 +628,47 @@ uint64_t xo_encode_delta(uint32_t m_bits, const uint64_t* words, uint8_t* out, u
     return need;
 }
 
+/* notify::encode_positions (notify.cpp:182-196): varint(count) || varint(first) ||
+ * varint(gaps) of the sorted positions, zero-padded to cap bytes. Returns the
+ * encoded length; > cap means the reference throws (out is then left zeroed). */
+uint64_t xo_encode_positions(const uint32_t* positions, uint32_t n, uint8_t* out, uint64_t cap) {
+    uint32_t s[256];
+    if (n > 256) return ~0ull;
+    memcpy(s, positions, (size_t)n * 4);
+    for (uint32_t i = 1; i < n; ++i) { /* insertion sort (std::sort order) */
+        const uint32_t v = s[i];
+        uint32_t j = i;
+        while (j > 0 && s[j - 1] > v) {
+            s[j] = s[j - 1];
+            --j;
+        }
+        s[j] = v;
+    }
+    uint64_t need = xo_put_varint(NULL, 0, 0, n);
+    for (uint32_t i = 0; i < n; ++i) need = xo_put_varint(NULL, need, 0, i == 0 ? s[i] : s[i] - s[i - 1]);
+    if (out) memset(out, 0, cap);
+    if (!out || need > cap) return need;
+    uint64_t at = xo_put_varint(out, 0, cap, n);
+    for (uint32_t i = 0; i < n; ++i) at = xo_put_varint(out, at, cap, i == 0 ? s[i] : s[i] - s[i - 1]);
+    return need;
+}
+
+/* notify::decode_positions (notify.cpp:198-214): 1 ok (*count positions written
+ * when they fit in max_out), 0 = std::nullopt. */
+int xo_decode_positions(const uint8_t* buf, uint64_t len, uint32_t* out, uint32_t max_out, uint32_t* count_out) {
+    uint64_t at = 0, count = 0, pos = 0;
+    if (!xo_get_varint(buf, len, &at, &count) || count > len * 8) return 0;
+    for (uint64_t i = 0; i < count; ++i) {
+        uint64_t gap;
+        if (!xo_get_varint(buf, len, &at, &gap)) return 0;
+        pos = i == 0 ? gap : pos + gap; /* uint64 arithmetic, wrapping as the reference's */
+        if (pos > 0xffffffffull) return 0;
+        if (out && i < max_out) out[i] = (uint32_t)pos;
+    }
+    *count_out = (uint32_t)count;
+    return 1;
+}
+
 int xo_decode_delta(const uint8_t* buf, uint64_t len, uint32_t* m_bits, uint64_t* words,
                     uint64_t words_cap) { /* :151-170 */
     uint64_t at = 0, m = 0, count = 0;

@@ -108,6 +108,8 @@ const uint64_t* xo_window_delta(const xo_window* w, uint64_t i);
 uint64_t xo_encode_delta(uint32_t m_bits, const uint64_t* words, uint8_t* out, uint64_t cap);
 /* notify::decode_delta (notify.cpp:151-170): 1 ok, 0 nullopt; words (ceil(m/64), zeroed here) when cap suffices */
 int xo_decode_delta(const uint8_t* buf, uint64_t len, uint32_t* m_bits, uint64_t* words, uint64_t words_cap);
+uint64_t xo_encode_positions(const uint32_t* positions, uint32_t n, uint8_t* out, uint64_t cap);
+int xo_decode_positions(const uint8_t* buf, uint64_t len, uint32_t* out, uint32_t max_out, uint32_t* count_out);
 
 #ifdef __cplusplus
 }

@@ -157,6 +157,8 @@ _SIGS = {
     "xpir_window_encode_delta": ([_vp, C.c_uint64, _u8p, C.c_uint64, _u64p], C.c_int),
     "xpir_encode_delta_dev": ([C.c_int, _vp, C.c_uint32, _vp, C.c_uint64, _u64p, _vp], C.c_int),
     "xpir_decode_delta": ([C.c_int, _u8p, C.c_uint64, _u32p, _u64p, C.c_uint64], C.c_int),
+    "xpir_encode_positions_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint64, C.c_uint32, _vp, _vp, _vp], C.c_int),
+    "xpir_decode_positions_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint64, _vp, _vp, _vp], C.c_int),
     "xpir_server_freeze": ([_vp, _u64p, _u64p, _u8p, _u64p], C.c_int),
     "xpir_batcher_create": ([_vp, C.c_uint32, C.c_uint32, C.POINTER(_vp)], C.c_int),
     "xpir_batcher_destroy": ([_vp], C.c_int),
@@ -764,6 +766,20 @@ def encode_delta_dev(d_words, m_bits: int, d_out=None, cap: int = 0, device: int
     n = C.c_uint64()
     _check(lib().xpir_encode_delta_dev(device, _ptr(d_words), m_bits, _ptr(d_out), cap, C.byref(n), _stream(stream)))
     return n.value
+
+
+def encode_positions_dev(d_pos, h: int, n: int, d_fields, d_ok, cap: int = 64, device: int = 0, stream=None) -> None:
+    """notify::encode_positions (notify.cpp:182-196) of n writes x h positions into
+    cap-byte interest fields (wire.cpp:154); d_ok[i] = 0 where the reference throws."""
+    _check(lib().xpir_encode_positions_dev(device, _ptr(d_pos), h, n, cap, _ptr(d_fields), _ptr(d_ok),
+                                           _stream(stream)))
+
+
+def decode_positions_dev(d_fields, n: int, d_pos, d_count, cap: int = 64, device: int = 0, stream=None) -> None:
+    """notify::decode_positions (notify.cpp:198-214) of n cap-byte fields: d_count[i]
+    = count (positions in d_pos[i, :count]) or 0xffffffff (std::nullopt)."""
+    _check(lib().xpir_decode_positions_dev(device, _ptr(d_fields), cap, n, _ptr(d_pos), _ptr(d_count),
+                                           _stream(stream)))
 
 
 # ---------------------------------------------------------------------------

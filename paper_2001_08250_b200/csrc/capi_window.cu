@@ -232,6 +232,32 @@ int xpir_encode_delta_dev(int device, const uint64_t* d_words, uint32_t m_bits, 
     return XPIR_OK;
 }
 
+// notify::encode_positions (notify.cpp:182-196) for n writes of h positions each
+// into cap-byte fields; d_ok[i] = 0 where the reference throws (too long).
+int xpir_encode_positions_dev(int device, const uint32_t* d_pos, uint32_t h, uint64_t n, uint32_t cap,
+                              uint8_t* d_fields, uint8_t* d_ok, void* stream) {
+    if (n && (!d_fields || !d_ok || (h && !d_pos))) return fail(XPIR_EINVAL, "encode_positions: null buffer");
+    if (h > 128 || cap == 0 || cap > 4096) return fail(XPIR_EINVAL, "encode_positions: h <= 128, 1 <= cap <= 4096");
+    DeviceGuard g(device);
+    XCK(launch_encode_positions(d_pos, h, n, cap, d_fields, d_ok, static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    if (!stream) XCK(cudaStreamSynchronize(nullptr));
+    return XPIR_OK;
+}
+
+// notify::decode_positions (notify.cpp:198-214) of n cap-byte fields: d_count[i] =
+// the count (positions in d_pos[i*cap ..]) or 0xffffffff for std::nullopt.
+int xpir_decode_positions_dev(int device, const uint8_t* d_fields, uint32_t cap, uint64_t n, uint32_t* d_pos,
+                              uint32_t* d_count, void* stream) {
+    if (n && (!d_fields || !d_pos || !d_count)) return fail(XPIR_EINVAL, "decode_positions: null buffer");
+    if (cap == 0 || cap > 4096) return fail(XPIR_EINVAL, "decode_positions: 1 <= cap <= 4096");
+    DeviceGuard g(device);
+    XCK(launch_decode_positions(d_fields, cap, n, d_pos, d_count, static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    if (!stream) XCK(cudaStreamSynchronize(nullptr));
+    return XPIR_OK;
+}
+
 // notify::decode_delta (notify.cpp:131-170). EINVAL = the reference's nullopt.
 // words == NULL: header only (*m_bits). Otherwise words must hold ceil(m/64).
 int xpir_decode_delta(int device, const uint8_t* buf, uint64_t len, uint32_t* m_bits, uint64_t* words,

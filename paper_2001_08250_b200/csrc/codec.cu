@@ -274,4 +274,74 @@ cudaError_t launch_decode_delta(const uint8_t* buf, uint64_t len, uint64_t* word
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// The write's interest field (wire.cpp:154-169): notify::encode_positions /
+// decode_positions (notify.cpp:182-214), one thread per write. A field is
+// varint(count) || varint(first) || varint(gaps) of the sorted positions,
+// zero-padded to `cap` bytes (INTEREST_FIELD_LEN = 64 on the wire).
+
+constexpr uint32_t POS_MAX_H = 128;
+
+__global__ void k_encode_positions(const uint32_t* __restrict__ pos, uint32_t h, uint64_t n, uint32_t cap,
+                                   uint8_t* __restrict__ out, uint8_t* __restrict__ ok) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t s[POS_MAX_H];
+    for (uint32_t k = 0; k < h; ++k) {  // insertion sort (std::sort order, duplicates kept)
+        const uint32_t v = pos[i * h + k];
+        uint32_t j = k;
+        while (j > 0 && s[j - 1] > v) {
+            s[j] = s[j - 1];
+            --j;
+        }
+        s[j] = v;
+    }
+    uint64_t need = vlen(h);
+    for (uint32_t k = 0; k < h; ++k) need += vlen(k == 0 ? s[k] : s[k] - s[k - 1]);
+    uint8_t* f = out + i * cap;
+    uint32_t at = 0;
+    if (need <= cap) {  // otherwise the reference throws: the field stays zero, ok = 0
+        at = vput(f, h);
+        for (uint32_t k = 0; k < h; ++k) at += vput(f + at, k == 0 ? s[k] : s[k] - s[k - 1]);
+    }
+    for (uint32_t k = at; k < cap; ++k) f[k] = 0;
+    ok[i] = need <= cap ? 1 : 0;
+}
+
+__global__ void k_decode_positions(const uint8_t* __restrict__ fields, uint32_t cap, uint64_t n,
+                                   uint32_t* __restrict__ pos, uint32_t* __restrict__ count) {
+    const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t* f = fields + i * cap;
+    uint32_t* o = pos + i * cap;
+    uint64_t at = 0, c = 0, p = 0;
+    uint32_t res = 0xffffffffu;  // std::nullopt
+    if (vget(f, cap, at, c) && c <= uint64_t(cap) * 8) {
+        uint64_t k = 0;
+        for (; k < c; ++k) {
+            uint64_t gap;
+            if (!vget(f, cap, at, gap)) break;
+            p = k == 0 ? gap : p + gap;  // uint64 arithmetic, wrapping as the reference's
+            if (p > 0xffffffffull) break;
+            if (k < cap) o[k] = uint32_t(p);  // a parsed varint takes >= 1 byte: k < cap
+        }
+        if (k == c) res = uint32_t(c);
+    }
+    count[i] = res;
+}
+
+cudaError_t launch_encode_positions(const uint32_t* pos, uint32_t h, uint64_t n, uint32_t cap, uint8_t* out,
+                                    uint8_t* ok, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_encode_positions<<<uint32_t((n + 127) / 128), 128, 0, s>>>(pos, h, n, cap, out, ok);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode_positions(const uint8_t* fields, uint32_t cap, uint64_t n, uint32_t* pos, uint32_t* count,
+                                    cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_decode_positions<<<uint32_t((n + 127) / 128), 128, 0, s>>>(fields, cap, n, pos, count);
+    return cudaGetLastError();
+}
+
 }  // namespace xpir

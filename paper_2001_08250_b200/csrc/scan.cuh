@@ -103,6 +103,10 @@ size_t decode_delta_scratch_bytes(uint64_t len);
 cudaError_t launch_encode_delta(const uint64_t* words, uint64_t nwords, uint32_t m_bits, uint8_t* out, uint64_t cap,
                                 unsigned long long* len_out, void* scratch, size_t scratch_bytes, cudaStream_t s);
 // hdr: 5 x u64 of device memory; hdr[0] = 0 ok / 1 malformed / 2 words_cap too small, hdr[1] = m
+cudaError_t launch_encode_positions(const uint32_t* pos, uint32_t h, uint64_t n, uint32_t cap, uint8_t* out,
+                                    uint8_t* ok, cudaStream_t s);
+cudaError_t launch_decode_positions(const uint8_t* fields, uint32_t cap, uint64_t n, uint32_t* pos, uint32_t* count,
+                                    cudaStream_t s);
 cudaError_t launch_decode_delta(const uint8_t* buf, uint64_t len, uint64_t* words, uint64_t words_cap,
                                 unsigned long long* hdr, void* scratch, size_t scratch_bytes, cudaStream_t s);
 

@@ -245,3 +245,29 @@ def test_codec_port_vs_reference(port, ref):
             for cut in (0, 1, len(enc) // 2, len(enc) - 1):
                 bad = enc[:cut]
                 assert (port.decode_delta(bad) is None) == (ref.decode_delta(bad) is None)
+
+
+def test_interest_field_codec_pinned_to_reference(port):
+    """notify::encode_positions / decode_positions (notify.cpp:182-214): the C
+    restatement equals the compiled reference on random position sets (including
+    fields too long for the 64-byte wire field, where the reference throws) and
+    on random / malformed fields (std::nullopt)."""
+    import oracle
+
+    if not oracle.ref_available():
+        pytest.skip("reference not built")
+    R = oracle.Ref()
+    g = np.random.default_rng(5)
+    for t in range(4000):
+        m = int(g.choice([1 << 10, 1 << 16, 1 << 20, (1 << 32) - 1]))
+        pos = g.integers(0, m, int(g.integers(0, 40))).astype(np.uint32)
+        cap = int(g.choice([16, 64, 100]))
+        assert port.encode_positions(pos, cap) == R.encode_positions(pos, cap)
+        buf = g.integers(0, 256, int(g.integers(0, 70)), dtype=np.uint8)
+        if t % 3 == 0:
+            buf &= 0x7F
+        a, b = port.decode_positions(buf.tobytes()), R.decode_positions(buf.tobytes())
+        assert (a is None) == (b is None) and (a is None or np.array_equal(a, b))
+    # config 3's m = 2^20, h = 23 overflows the 64-byte field for about a fifth of the writes
+    big = sum(R.encode_positions(g.integers(0, 1 << 20, 23).astype(np.uint32), 64) is None for _ in range(200))
+    assert 10 < big < 100
