@@ -1,6 +1,6 @@
 """bench_codec.py — interest-window codecs on the
 config-3 interest delta (2^20 bits after 32,000 writes x 23 positions):
-notify::encode_delta / decode_delta (notify.cpp:131-170) on device vs the
+notify::encode_delta / decode_delta (notify.cpp:139-180) on device vs the
 unmodified reference on one host core (oracle/_ref).
 
     python bench_codec.py [--out profiles/r01_codec.jsonl]

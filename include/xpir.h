@@ -298,11 +298,11 @@ int xpir_window_absorb_interest_dev(xpir_window* win, const uint8_t id[16], cons
 int xpir_window_rotate(xpir_window* win);
 int xpir_window_info(const xpir_window* win, uint64_t* size, uint64_t* base);
 int xpir_window_delta(const xpir_window* win, uint64_t i, uint64_t* out_words);
-/* Window::digest (notify.cpp:87-107). */
+/* Window::digest (notify.cpp:90-107). */
 int xpir_window_digest(const xpir_window* win, uint8_t out[32]);
-/* Window::digest(count) over the oldest `count` deltas (notify.cpp:91-107). */
+/* Window::digest(count) over the oldest `count` deltas (notify.cpp:92-107). */
 int xpir_window_digest_n(const xpir_window* win, uint64_t count, uint8_t out[32]);
-/* notify::encode_delta (notify.cpp:131-149) of delta i (0 = oldest), encoded on
+/* notify::encode_delta (notify.cpp:139-157) of delta i (0 = oldest), encoded on
  * device: varint(m) || varint(ones) || varint(first position) || varint(gaps).
  * out == NULL: *len = size only. EINVAL when cap < *len. */
 int xpir_window_encode_delta(xpir_window* win, uint64_t i, uint8_t* out, uint64_t cap, uint64_t* len);
@@ -320,7 +320,7 @@ int xpir_encode_positions_dev(int device, const uint32_t* d_pos, uint32_t h, uin
                               uint8_t* d_fields, uint8_t* d_ok, void* stream);
 int xpir_decode_positions_dev(int device, const uint8_t* d_fields, uint32_t cap, uint64_t n, uint32_t* d_pos,
                               uint32_t* d_count, void* stream);
-/* notify::decode_delta (notify.cpp:151-170), decoded on device. XPIR_EINVAL is the
+/* notify::decode_delta (notify.cpp:159-180), decoded on device. XPIR_EINVAL is the
  * reference's std::nullopt (malformed input). words == NULL: header only
  * (*m_bits); else words receives ceil(m/64) words (EINVAL if words_cap is short). */
 int xpir_decode_delta(int device, const uint8_t* buf, uint64_t len, uint32_t* m_bits, uint64_t* words,

@@ -172,7 +172,7 @@ class Port:
     def window(self, m, h, w) -> "PortWindow":
         return PortWindow(self, m, h, w)
 
-    # interest-delta codecs (notify.cpp:131-170)
+    # interest-delta codecs (notify.cpp:139-180)
     def encode_delta(self, m: int, words: np.ndarray) -> bytes:
         w = np.ascontiguousarray(words, np.uint64)
         n = self.lib.xo_encode_delta(m, _p(w, _u64p), None, 0)

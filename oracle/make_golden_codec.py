@@ -1,6 +1,6 @@
 """Writes tests/golden/codec.json from the UNMODIFIED reference build
 (oracle/_ref/libxpir_ref.so): notify::encode_delta / decode_delta
-(notify.cpp:131-170) vectors — the reference's own test_notify.cpp cases
+(notify.cpp:139-180) vectors — the reference's own test_notify.cpp cases
 (DetRng(11) densities on m = 4097, an empty 2^23-bit delta, the {3, 9} delta and
 its trailing/truncated corruptions), random deltas at several widths, the
 config-3 interest delta, and a set of malformed inputs with their verdicts.
@@ -60,7 +60,7 @@ def main():
     enc = R.encode_delta(recipes.C3["m"], w)
     cases.append({"name": "config3_delta", "m": recipes.C3["m"], "words_sha256": hashlib.sha256(w.tobytes()).hexdigest(),
                   "enc_len": len(enc), "enc_sha256": hashlib.sha256(enc).hexdigest()})
-    # malformed inputs (test_notify.cpp:141-153 and the decode rules of notify.cpp:151-170)
+    # malformed inputs (test_notify.cpp:141-153 and the decode rules of notify.cpp:159-180)
     ok39 = R.encode_delta(64, words_of(64, [3, 9]))
     bad = {
         "empty": b"", "trailing": ok39 + b"\x00", "truncated": ok39[:-1], "m_only": b"\x40",

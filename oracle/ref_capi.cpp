@@ -284,7 +284,7 @@ void ref_window_delta_words(void* w, uint64_t i, uint64_t* out) {
     std::memcpy(out, d.words.data(), d.words.size() * 8);
 }
 
-// notify::encode_delta / decode_delta (notify.cpp:131-170), Window::digest(count)
+// notify::encode_delta / decode_delta (notify.cpp:139-180), Window::digest(count)
 int64_t ref_encode_delta(uint32_t m, const uint64_t* words, uint8_t* out, uint64_t cap) {
     notify::DeltaFilter d = notify::DeltaFilter::empty(m);
     std::memcpy(d.words.data(), words, d.words.size() * 8);

@@ -566,7 +566,7 @@ uint64_t xo_window_size(const xo_window* x) { return x->n; }
 uint64_t xo_window_base(const xo_window* x) { return x->base; }
 const uint64_t* xo_window_delta(const xo_window* x, uint64_t i) { return x->deltas[i]; }
 
-/* ---- interest-delta codecs (notify.cpp:110-170) ---------------------------- */
+/* ---- interest-delta codecs (notify.cpp:119-180) ---------------------------- */
 static uint64_t xo_put_varint(uint8_t* out, uint64_t at, uint64_t cap, uint64_t v) { /* :110-116 */
     while (v >= 0x80) {
         if (out && at < cap) out[at] = (uint8_t)(v | 0x80);

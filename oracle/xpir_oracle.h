@@ -104,9 +104,9 @@ void xo_window_digest_n(const xo_window* w, uint64_t count, uint8_t out[32]); /*
 uint64_t xo_window_size(const xo_window* w);
 uint64_t xo_window_base(const xo_window* w);
 const uint64_t* xo_window_delta(const xo_window* w, uint64_t i);
-/* notify::encode_delta (notify.cpp:131-149): returns the encoded size; writes when cap suffices */
+/* notify::encode_delta (notify.cpp:139-157): returns the encoded size; writes when cap suffices */
 uint64_t xo_encode_delta(uint32_t m_bits, const uint64_t* words, uint8_t* out, uint64_t cap);
-/* notify::decode_delta (notify.cpp:151-170): 1 ok, 0 nullopt; words (ceil(m/64), zeroed here) when cap suffices */
+/* notify::decode_delta (notify.cpp:159-180): 1 ok, 0 nullopt; words (ceil(m/64), zeroed here) when cap suffices */
 int xo_decode_delta(const uint8_t* buf, uint64_t len, uint32_t* m_bits, uint64_t* words, uint64_t words_cap);
 uint64_t xo_encode_positions(const uint32_t* positions, uint32_t n, uint8_t* out, uint64_t cap);
 int xo_decode_positions(const uint8_t* buf, uint64_t len, uint32_t* out, uint32_t max_out, uint32_t* count_out);

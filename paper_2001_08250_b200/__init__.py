@@ -723,7 +723,7 @@ class Window:
         return out
 
     def digest(self, count: int | None = None) -> bytes:
-        """Window::digest() / digest(count) (notify.cpp:89-107)."""
+        """Window::digest() / digest(count) (notify.cpp:90-107)."""
         out = np.empty(32, np.uint8)
         if count is None:
             _check(lib().xpir_window_digest(self.h, _p(out)))
@@ -732,7 +732,7 @@ class Window:
         return out.tobytes()
 
     def encode_delta(self, i: int) -> bytes:
-        """notify::encode_delta(delta(i)) (notify.cpp:131-149), encoded on device."""
+        """notify::encode_delta(delta(i)) (notify.cpp:139-157), encoded on device."""
         return _window_encode(self.h, i)
 
 
@@ -745,7 +745,7 @@ def _window_encode(h, i: int) -> bytes:
 
 
 def decode_delta(buf: bytes, device: int = 0):
-    """notify::decode_delta (notify.cpp:151-170) on device: (m_bits, words) or None
+    """notify::decode_delta (notify.cpp:159-180) on device: (m_bits, words) or None
     for malformed input (the reference's std::nullopt)."""
     b = _u8(buf) if len(buf) else np.zeros(1, np.uint8)
     m = C.c_uint32()

@@ -1,4 +1,4 @@
-// C-ABI (include/xpir.h): the interest window and its codecs — notify::Window (notify.cpp:54-170).
+// C-ABI (include/xpir.h): the interest window and its codecs — notify::Window (notify.cpp:54-180).
 #include "capi_internal.cuh"
 
 // ===========================================================================
@@ -157,7 +157,7 @@ int xpir_window_delta(const xpir_window* win, uint64_t i, uint64_t* out) {
     return XPIR_OK;
 }
 
-int xpir_window_digest(const xpir_window* win, uint8_t out[32]) {  // notify.cpp:87-107
+int xpir_window_digest(const xpir_window* win, uint8_t out[32]) {  // notify.cpp:90-107
     if (!win) return fail(XPIR_EINVAL, "window_digest: null argument");
     return xpir_window_digest_n(win, win->deltas.size(), out);
 }
@@ -183,7 +183,7 @@ int xpir_window_digest_n(const xpir_window* win, uint64_t count, uint8_t out[32]
     return XPIR_OK;
 }
 
-// notify::encode_delta (notify.cpp:131-149) of delta i (0 = oldest) on device.
+// notify::encode_delta (notify.cpp:139-157) of delta i (0 = oldest) on device.
 // out == NULL: size query. Otherwise out must hold *len bytes (EINVAL if cap is short).
 int xpir_window_encode_delta(xpir_window* win, uint64_t i, uint8_t* out, uint64_t cap, uint64_t* len) {
     if (!win || !len) return fail(XPIR_EINVAL, "window_encode_delta: null argument");
@@ -258,7 +258,7 @@ int xpir_decode_positions_dev(int device, const uint8_t* d_fields, uint32_t cap,
     return XPIR_OK;
 }
 
-// notify::decode_delta (notify.cpp:131-170). EINVAL = the reference's nullopt.
+// notify::decode_delta (notify.cpp:139-180). EINVAL = the reference's nullopt.
 // words == NULL: header only (*m_bits). Otherwise words must hold ceil(m/64).
 int xpir_decode_delta(int device, const uint8_t* buf, uint64_t len, uint32_t* m_bits, uint64_t* words,
                       uint64_t words_cap) {

@@ -1,5 +1,5 @@
 // Interest-window codecs on device: notify::encode_delta
-// and notify::decode_delta (notify.cpp:118-170), the wire form of a served or
+// and notify::decode_delta (notify.cpp:127-180), the wire form of a served or
 // frozen interest delta (ServerCore::make_freeze, server.cpp:45-56).
 //
 // encode: varint(m_bits) || varint(ones) || varint(first set position) ||
@@ -36,7 +36,7 @@ __device__ __forceinline__ uint32_t vlen(uint64_t v) {
     }
     return n;
 }
-__device__ __forceinline__ uint32_t vput(uint8_t* p, uint64_t v) {  // put_varint, notify.cpp:110-116
+__device__ __forceinline__ uint32_t vput(uint8_t* p, uint64_t v) {  // put_varint, notify.cpp:119-125
     uint32_t n = 0;
     while (v >= 0x80) {
         p[n++] = uint8_t(v) | 0x80;
@@ -45,7 +45,7 @@ __device__ __forceinline__ uint32_t vput(uint8_t* p, uint64_t v) {  // put_varin
     p[n++] = uint8_t(v);
     return n;
 }
-// get_varint (notify.cpp:118-129) over bytes [at, len): value, or false
+// get_varint (notify.cpp:127-137) over bytes [at, len): value, or false
 __device__ __forceinline__ bool vget(const uint8_t* buf, uint64_t len, uint64_t& at, uint64_t& out) {
     uint64_t v = 0;
     int shift = 0;
@@ -164,7 +164,7 @@ __global__ void k_dec_b(const uint8_t* __restrict__ buf, uint64_t len, unsigned 
     for (uint64_t j = b0; j < b1; ++j) {
         if (buf[j] & 0x80) continue;
         uint64_t a = start, v = 0;
-        if (j - start + 1 > 10 || !vget(buf, j + 1, a, v)) atomicExch(&hdr[0], 1ull);  // > 10 bytes (notify.cpp:122)
+        if (j - start + 1 > 10 || !vget(buf, j + 1, a, v)) atomicExch(&hdr[0], 1ull);  // > 10 bytes (notify.cpp:130)
         s += v;
         start = j + 1;
     }
@@ -179,7 +179,7 @@ __global__ void k_dec_c(const uint8_t* __restrict__ buf, uint64_t len, unsigned 
     if (t >= nch) return;
     if (hdr[4]) return;
     const uint64_t m = hdr[1], count = hdr[2], at = hdr[3];
-    if (t == nch - 1) {  // exactly `count` varints, nothing after the last one (notify.cpp:140-150)
+    if (t == nch - 1) {  // exactly `count` varints, nothing after the last one (notify.cpp:166-178)
         const unsigned long long tot = ends_ex[t] + nends[t];
         if (tot != count || (len > at && (buf[len - 1] & 0x80))) atomicExch(&hdr[0], 1ull);
     }

@@ -1,5 +1,5 @@
 """GPU parity of the interest-window codecs on device:
-notify::encode_delta / decode_delta (notify.cpp:131-170) and
+notify::encode_delta / decode_delta (notify.cpp:139-180) and
 ServerCore::make_freeze (server.cpp:45-56), against the golden vectors written
 from the unmodified reference (tests/golden/codec.json) and the oracle.
 Byte-exact: every encoding, verdict and decoded word."""

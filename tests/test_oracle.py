@@ -204,7 +204,7 @@ def test_port_vs_reference_cuckoo(port, ref):
         assert A.state_digest() == B.state_digest()
 
 
-# --- interest-delta codecs (notify.cpp:131-170), pinned by tests/golden/codec.json --------
+# --- interest-delta codecs (notify.cpp:139-180), pinned by tests/golden/codec.json --------
 def _codec_words(c):
     if c.get("words_zero"):
         return np.zeros((c["m"] + 63) // 64, np.uint64)
