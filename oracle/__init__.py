@@ -383,6 +383,10 @@ class Ref:
         L.ref_encode_delta.restype = C.c_int64
         L.ref_decode_delta.argtypes = [_u8p, C.c_uint64, _u32p, _u64p, C.c_uint64]
         L.ref_decode_delta.restype = C.c_int
+        L.ref_encode_positions_batch.argtypes = [_u32p, C.c_uint32, C.c_uint64, C.c_uint64, _u8p, _u8p]
+        L.ref_encode_positions_batch.restype = None
+        L.ref_decode_positions_batch.argtypes = [_u8p, C.c_uint64, C.c_uint64, _u32p, _u32p]
+        L.ref_decode_positions_batch.restype = None
         L.ref_encode_positions.argtypes = [_u32p, C.c_uint64, _u8p, C.c_uint64]
         L.ref_encode_positions.restype = C.c_int64
         L.ref_decode_positions.argtypes = [_u8p, C.c_uint64, _u32p, C.c_uint32, _u32p]
@@ -471,6 +475,23 @@ class Ref:
         out = np.zeros(max(cap, 1), np.uint8)
         n = self.lib.ref_encode_positions(_p(p, _u32p) if len(p) else None, len(p), _p(out), cap)
         return None if n < 0 else out[:cap].tobytes()
+
+    def encode_positions_batch(self, pos: np.ndarray, cap: int = 64):
+        """(fields n x cap, ok n) for n writes x h positions (reference loop in C++)."""
+        p = np.ascontiguousarray(pos, np.uint32)
+        n, h = p.shape
+        out = np.zeros((n, cap), np.uint8)
+        ok = np.zeros(n, np.uint8)
+        self.lib.ref_encode_positions_batch(_p(p, _u32p), h, n, cap, _p(out), _p(ok))
+        return out, ok
+
+    def decode_positions_batch(self, fields: np.ndarray):
+        f = np.ascontiguousarray(fields, np.uint8)
+        n, cap = f.shape
+        pos = np.zeros((n, cap), np.uint32)
+        cnt = np.zeros(n, np.uint32)
+        self.lib.ref_decode_positions_batch(_p(f), cap, n, _p(pos, _u32p), _p(cnt, _u32p))
+        return pos, cnt
 
     def decode_positions(self, buf: bytes):
         b = _u8(buf) if len(buf) else np.zeros(1, np.uint8)

@@ -311,6 +311,24 @@ int64_t ref_encode_positions(const uint32_t* positions, uint64_t n, uint8_t* out
         return -1;
     }
 }
+// the same for n writes of h positions (a server decoding / a client encoding a
+// round's writes), timed by bench_codec.py: ok[i] = 0 where the reference throws
+void ref_encode_positions_batch(const uint32_t* positions, uint32_t h, uint64_t n, uint64_t cap, uint8_t* out,
+                                uint8_t* ok) {
+    for (uint64_t i = 0; i < n; ++i) ok[i] = ref_encode_positions(positions + i * h, h, out + i * cap, cap) >= 0;
+}
+// count[i] = number of positions (written to pos[i*cap ..]) or 0xffffffff for nullopt
+void ref_decode_positions_batch(const uint8_t* fields, uint64_t cap, uint64_t n, uint32_t* pos, uint32_t* count) {
+    for (uint64_t i = 0; i < n; ++i) {
+        auto p = notify::decode_positions(byte_view(fields + i * cap, cap));
+        if (!p) {
+            count[i] = 0xffffffffu;
+            continue;
+        }
+        count[i] = uint32_t(p->size());
+        for (size_t k = 0; k < p->size() && k < cap; ++k) pos[i * cap + k] = (*p)[k];
+    }
+}
 // notify::decode_positions: 1 ok (count, positions when they fit), 0 nullopt
 int ref_decode_positions(const uint8_t* buf, uint64_t len, uint32_t* out, uint32_t max_out, uint32_t* count) {
     auto p = notify::decode_positions(byte_view(buf, len));
