@@ -115,8 +115,8 @@ uint64_t xpir_query_window_bytes(const xpir_store* st);
  * buffer out_ptrs[k] (a local or CUDA-IPC-mapped peer pointer) holds all B rows
  * at the same offsets. Each owner must have initialised its rows (zero or mask
  * pad, xpir_init_rows_dev) before any rank launches; after every rank's scan
- * completes the owner's rows are final. Needs S % 128 == 0 and B >= 2048
- * (the half-TMEM M4RM kernel); 1..8 ranks. pir::reconstruct semantics. */
+ * completes the owner's rows are final. Needs S % 32 == 0 and B >= 2048
+ * (runs the quad-table M4RM kernel 8); 1..8 ranks. pir::reconstruct semantics. */
 int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, uint32_t batch,
                                       uint8_t* const* out_ptrs, const uint32_t* row_bounds, uint32_t n_ranks,
                                       void* stream);
