@@ -87,3 +87,16 @@ def test_positions_round_trip(xp, cuda):
     assert ok.all()
     assert (cnt == h).all()
     assert np.array_equal(out[:, :h], np.sort(pos, axis=1))
+
+
+def test_argument_checks(xp, cuda):
+    import torch
+
+    d_pos = torch.zeros((4, 129), dtype=torch.int32, device="cuda")
+    d_f = torch.empty((4, 64), dtype=torch.uint8, device="cuda")
+    d_ok = torch.empty(4, dtype=torch.uint8, device="cuda")
+    with pytest.raises(xp.InvalidArgument):
+        xp.encode_positions_dev(d_pos, 129, 4, d_f, d_ok)  # h <= 128
+    with pytest.raises(xp.InvalidArgument):
+        xp.decode_positions_dev(d_f, 4, d_pos, d_ok, cap=0)
+    xp.encode_positions_dev(d_pos, 0, 0, None, None)  # n = 0: nothing to do
