@@ -307,6 +307,17 @@ static uint32_t g_q_min_batch = 2048;  // quad-table full-TMEM M4RM (kernel 8) f
 // past 256 its request tiles split and the byte tables win
 static uint32_t g_k6_min_batch = 129;
 static uint32_t g_k6_max_batch = 256;
+// XPIR_K9_RANGE="min,max" overrides that range (A/B runs; "1,0" disables kernel 9)
+static const bool g_k6_env = [] {
+    if (const char* e = std::getenv("XPIR_K9_RANGE")) {
+        unsigned a = 0, b = 0;
+        if (std::sscanf(e, "%u,%u", &a, &b) == 2) {
+            g_k6_min_batch = a;
+            g_k6_max_batch = b;
+        }
+    }
+    return true;
+}();
 
 static int choose_kernel(const xpir_store* st, uint32_t B) {
     int k;
