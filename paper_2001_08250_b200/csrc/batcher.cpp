@@ -49,7 +49,8 @@ struct BBuf {
     cudaEvent_t done_ev = nullptr;
     BState state = BState::Idle;
     bool masked = false;
-    uint32_t count = 0, filled = 0;
+    uint32_t count = 0;
+    std::atomic<uint32_t> filled{0};  // callers done packing (no lock: the worker polls it after sealing)
     uint64_t gen = 0;
     std::chrono::steady_clock::time_point first;
     int rc = 0;
@@ -70,8 +71,9 @@ struct xpir_batcher {
     std::condition_variable cv_free;  // callers: a staging batch became idle
     BBuf buf[NBUF];
     std::deque<BBuf*> inflight;  // in submission order
-    bool stop = false, completer_stop = false;
-    uint32_t active = 0;  // callers inside xpir_batcher_answer (destroy waits for them)
+    std::atomic<bool> stop{false};
+    bool completer_stop = false;
+    std::atomic<uint32_t> active{0};  // callers inside xpir_batcher_answer (destroy waits for them)
     std::thread worker, completer;
     uint64_t n_requests = 0, n_batches = 0, max_seen = 0;
 
@@ -94,18 +96,21 @@ struct xpir_batcher {
             cv_work.wait(lk, [&] {
                 for (auto& x : buf)
                     if (x.state == BState::Forming) return true;
-                return stop;
+                return stop.load();
             });
             for (auto& x : buf)  // the oldest forming batch first
                 if (x.state == BState::Forming && (!b || x.gen < b->gen)) b = &x;
             if (!b) break;  // stop, nothing pending
             const auto deadline = b->first + std::chrono::microseconds(max_wait_us);
-            cv_work.wait_until(lk, deadline, [&] { return stop || b->count >= max_batch; });
+            cv_work.wait_until(lk, deadline, [&] { return stop.load() || b->count >= max_batch; });
             b->state = BState::Sealed;  // no more joins
-            cv_work.wait(lk, [&] { return b->filled == b->count; });
-            b->state = BState::InFlight;
             const uint32_t B = b->count;
             const bool masked = b->masked;
+            lk.unlock();
+            // the joined callers are copying their rows in (a few microseconds)
+            while (b->filled.load(std::memory_order_acquire) != B) std::this_thread::yield();
+            lk.lock();
+            b->state = BState::InFlight;
             lk.unlock();
             // queue H2D, scan, D2H on the batch's stream; do not wait
             int rc = XPIR_OK;
@@ -249,7 +254,7 @@ int xpir_batcher_destroy(xpir_batcher* b) {
     {
         // callers of the last batches may still be copying their answers out
         std::unique_lock<std::mutex> lk(b->mu);
-        b->cv_free.wait(lk, [&] { return b->active == 0; });
+        b->cv_free.wait(lk, [&] { return b->active.load() == 0; });
     }
     free_bufs(b);
     delete b;
@@ -263,12 +268,16 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
     const bool masked = mask_seed != nullptr;
     std::unique_lock<std::mutex> lk(b->mu);
     if (b->stop) return bfail(XPIR_ESTATE, "batcher_answer: batcher is shutting down");
-    b->active += 1;
+    b->active.fetch_add(1);
     struct Leave {  // the last one out lets a pending destroy proceed
         xpir_batcher* b;
         ~Leave() {
-            std::lock_guard<std::mutex> g(b->mu);
-            if (--b->active == 0) b->cv_free.notify_all();
+            // seq_cst pair with destroy (store stop, then read active): either it
+            // sees this decrement or this sees stop and wakes it
+            if (b->active.fetch_sub(1) == 1 && b->stop.load()) {
+                std::lock_guard<std::mutex> g(b->mu);
+                b->cv_free.notify_all();
+            }
         }
     };
     BBuf* buf = nullptr;
@@ -288,7 +297,8 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
                     for (auto& y : b->buf) g = y.gen > g ? y.gen : g;
                     x.state = BState::Forming;
                     x.masked = masked;
-                    x.count = x.filled = 0;
+                    x.count = 0;
+                    x.filled.store(0, std::memory_order_relaxed);
                     x.gen = g + 1;
                     x.first = std::chrono::steady_clock::now();
                     break;
@@ -304,10 +314,7 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
     lk.unlock();
     std::memcpy(buf->rows + size_t(k) * b->nb, q, b->nb);
     if (masked) std::memcpy(buf->seeds + size_t(k) * 32, mask_seed, 32);
-    lk.lock();
-    buf->filled += 1;
-    if (buf->filled == buf->count && buf->state == BState::Sealed) b->cv_work.notify_one();
-    lk.unlock();
+    buf->filled.fetch_add(1, std::memory_order_release);
     for (uint64_t d = buf->done_gen.load(std::memory_order_acquire); d != gen;
          d = buf->done_gen.load(std::memory_order_acquire))
         buf->done_gen.wait(d, std::memory_order_acquire);
