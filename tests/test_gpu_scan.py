@@ -213,11 +213,14 @@ def test_config2_three_server_round(xp, port, golden, cuda):
     assert np.array_equal(outs[0] ^ outs[1] ^ outs[2], db.reshape(32768, 4096)[betas])
 
 
-def test_virtual_shards_xor_reduce(xp, port, cuda):
-    """Bucket-range shards on one GPU + the K4 XOR reduce == the unsharded scan."""
+@pytest.mark.parametrize("kernel,B", [(0, 333), (9, 200), (7, 100), (8, 2100), (1, 17)])
+def test_virtual_shards_xor_reduce(xp, port, cuda, kernel, B):
+    """Bucket-range shards on one GPU + the K4 XOR reduce == the unsharded scan,
+    for each scan kernel (shard windows start mid-chunk of every table layout)."""
     torch = cuda
-    N, S, B = 8192, 512, 333
-    g = np.random.default_rng(21)
+    N, S = 8192, 512
+    xp.set_scan_opts(kernel)
+    g = np.random.default_rng(21 + B)
     db, q = rand(g, N * S), rand(g, B, N // 8)
     want = port.answer_batch(db, N, S, q, B)
     dq = torch.from_numpy(q).cuda()
