@@ -40,6 +40,26 @@ BATCH = 8192
 STORE_SEED = 3  # DetRng(3), SURVEY.md §8(d) config 4
 METRIC = "PIR requests/sec (batched XOR-PIR scan, 4 GiB store, 8192 seeded requests)"
 UNIT = "requests/s"
+SAMPLED = os.path.join(ROOT, "tests", "golden", "sampled.json")
+
+
+def workload_config(batch: int) -> dict:
+    """The `config` object both arms print (identical, so the driver can match them)."""
+    return {"workload": "config4: 4 GiB store (1,048,576 buckets x 4 x 1,024 B), 8192 seeded requests, "
+                        "bucket-range sharded",
+            "store_bytes": N_BUCKETS * BUCKET_BYTES, "batch": batch, "buckets": N_BUCKETS,
+            "bucket_bytes": BUCKET_BYTES, "l2": "inputs larger than L2 (4 GiB store streamed every step)"}
+
+
+def sampled_golden():
+    """>= 64 reference rows of the bench's exact batch (oracle/make_golden_sampled.py
+    over the unmodified reference's pir::answer_batch), or None when the run is
+    not the config-4 workload."""
+    if N_BUCKETS != 1 << 20 or not os.path.exists(SAMPLED):
+        return None
+    with open(SAMPLED) as f:
+        g = json.load(f)["config4"]
+    return g if g["B"] == BATCH else None
 
 
 def env_int(name, default):
@@ -173,10 +193,9 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * BATCH / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (DetRng / ChaCha20 recipe of SURVEY.md §8(d))",
-        "config": {"workload": "config4: 4 GiB store (1,048,576 buckets x 4096 B), 8192 seeded requests",
-                   "store_bytes": N_BUCKETS * BUCKET_BYTES, "batch": BATCH,
-                   "parallelism": f"host threads={ref.threads}", "l2": "store larger than L2",
-                   "step": f"a bounded sample of {B} requests per step; ms_per_step scaled to the 8192 batch"},
+        "config": workload_config(BATCH),
+        "parallelism": f"host threads={ref.threads}",
+        "step": f"a bounded sample of {B} requests per step; ms_per_step scaled to the 8192 batch",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.threads, "kind": ref.kind,
                          "sample": ref.describe(B, secs)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -247,6 +266,12 @@ def main():
         t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared_gpu else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+    def sum_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared_gpu else "cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
     B = args.batch
     xp.set_scan_opts(args.kernel)
     key = xp.blake2b(STORE_SEED.to_bytes(8, "little"), 32)  # DetRng(3) key (rng.cpp:18-23)
@@ -269,9 +294,11 @@ def main():
     out = torch.empty((B, BUCKET_BYTES), dtype=torch.uint8, device="cuda")
     torch.cuda.synchronize()
 
+    own = {"rows": out, "r0": 0}
+
     def step():
         if sh is not None:
-            sh.step(seeds, stream=stream)
+            own["rows"], own["r0"] = sh.step(seeds, stream=stream), sh.r0
         else:
             store.answer_batch_seeded_dev(seeds, B, out, stream=stream)
 
@@ -301,6 +328,21 @@ def main():
     ms = max_over_ranks(e0.elapsed_time(e1))
     ms_per_step = ms / args.steps
     value = B / (ms_per_step * 1e-3)
+
+    # parity of the last timed step's output: every reference-sampled row this rank owns
+    parity = "unchecked (not the config-4 workload)"
+    gold = sampled_golden() if B == BATCH else None
+    if gold is not None:
+        import hashlib
+
+        torch.cuda.synchronize()
+        rows, r0 = own["rows"], own["r0"]
+        mine = [(i, r) for i, r in enumerate(gold["rows"]) if r0 <= r < r0 + rows.shape[0]]
+        bad = sum(hashlib.sha256(rows[r - r0].cpu().numpy().tobytes()).hexdigest() != gold["out_rows_sha256"][i]
+                  for i, r in mine)
+        bad, checked = int(sum_over_ranks(float(bad))), int(sum_over_ranks(float(len(mine))))
+        parity = ("ok" if bad == 0 else "MISMATCH") + \
+            f" ({checked} reference rows of the timed batch, tests/golden/sampled.json; {bad} differ)"
 
     if args.quick:
         if rank == 0:
@@ -404,13 +446,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (DetRng(3) store, DetRng(3) seeds -> ChaCha20 query vectors, SURVEY.md §8(d))",
-            "config": {"workload": "config4: 4 GiB store (1,048,576 buckets x 4 x 1,024 B), 8192 seeded "
-                                   "requests, bucket-range sharded",
-                       "store_bytes": N_BUCKETS * BUCKET_BYTES, "batch": B, "buckets": N_BUCKETS,
-                       "bucket_bytes": BUCKET_BYTES, "parallelism": f"bucket-range shards x{world}",
-                       "reduce": ("none" if sh is None else
-                                  "fused peer-atomic epilogue" if sh.fused else "IPC xor reduce-scatter"),
-                       "l2": "inputs larger than L2 (4 GiB store streamed every step)"},
+            "config": workload_config(B),
+            "parallelism": f"bucket-range shards x{world}",
+            "reduce": ("none" if sh is None else
+                       "fused peer epilogue (tile fix-up)" if sh.fused else "IPC xor reduce-scatter"),
+            "parity": parity,
             "effective_scan_GBps": B * N_BUCKETS * BUCKET_BYTES / (ms_per_step * 1e-3) / 1e9,
             "gpu_launches": launches,
             "roofline": roof,

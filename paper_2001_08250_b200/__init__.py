@@ -446,17 +446,38 @@ class Batcher:
     requests, sealed ``max_wait_us`` after its first request."""
 
     def __init__(self, store: Store, max_batch: int = 1024, max_wait_us: int = 200):
+        import threading
+
         h = _vp()
         _check(lib().xpir_batcher_create(store.h, max_batch, max_wait_us, C.byref(h)))
         self.h, self.store = h, store
+        # callers inside a C call; close() waits for them before destroying the handle
+        self._cv, self._users = threading.Condition(), 0
 
     def close(self):
-        h = getattr(self, "h", None)
+        cv = getattr(self, "_cv", None)
+        if cv is None:
+            return
+        with cv:
+            h, self.h = getattr(self, "h", None), None  # new calls fail cleanly
+            cv.wait_for(lambda: self._users == 0)
         if h:
-            self.h = None  # new calls fail cleanly; calls already inside finish first
             _destroy(lambda: lib().xpir_batcher_destroy(h))
 
     __del__ = _quiet_del
+
+    def _enter(self):
+        with self._cv:
+            if not self.h:
+                raise XpirError(XPIR_ESTATE, "batcher is closed")
+            self._users += 1
+            return self.h
+
+    def _leave(self):
+        with self._cv:
+            self._users -= 1
+            if self._users == 0:
+                self._cv.notify_all()
 
     def answer(self, q, mask_seed: bytes | None = None, q_bits: int | None = None) -> np.ndarray:
         """pir::answer(snapshot, q), or mask_answer(answer(..), mask_seed) (pir.cpp:29-39, 65-69)."""
@@ -465,7 +486,11 @@ class Batcher:
             raise InvalidArgument(XPIR_EINVAL, "answer: query length mismatch")
         out = np.empty(self.store.S, np.uint8)
         ms = _p(_u8(mask_seed)) if mask_seed is not None else None
-        _check(lib().xpir_batcher_answer(self.h, _p(qa), self.store.N if q_bits is None else q_bits, ms, _p(out)))
+        h = self._enter()
+        try:
+            _check(lib().xpir_batcher_answer(h, _p(qa), self.store.N if q_bits is None else q_bits, ms, _p(out)))
+        finally:
+            self._leave()
         return out
 
     def stats(self) -> dict:

@@ -272,12 +272,11 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
     struct Leave {  // the last one out lets a pending destroy proceed
         xpir_batcher* b;
         ~Leave() {
-            // seq_cst pair with destroy (store stop, then read active): either it
-            // sees this decrement or this sees stop and wakes it
-            if (b->active.fetch_sub(1) == 1 && b->stop.load()) {
-                std::lock_guard<std::mutex> g(b->mu);
-                b->cv_free.notify_all();
-            }
+            // The decrement happens under mu: destroy evaluates its "active == 0"
+            // predicate under mu too, so it cannot free `b` until this caller has
+            // released the lock — the caller's last touch of `b`.
+            std::lock_guard<std::mutex> g(b->mu);
+            if (b->active.fetch_sub(1) == 1 && b->stop.load()) b->cv_free.notify_all();
         }
     };
     BBuf* buf = nullptr;

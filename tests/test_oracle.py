@@ -271,3 +271,21 @@ def test_interest_field_codec_pinned_to_reference(port):
     # config 3's m = 2^20, h = 23 overflows the 64-byte field for about a fifth of the writes
     big = sum(R.encode_positions(g.integers(0, 1 << 20, 23).astype(np.uint32), 64) is None for _ in range(200))
     assert 10 < big < 100
+
+
+def test_sampled_config5_rows_port(port):
+    """The C restatement reproduces the reference rows of tests/golden/sampled.json
+    (written from the unmodified reference) on the S = 32768 shape, B = 16."""
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "sampled.json")) as f:
+        G = json.load(f)["config5_auto"]
+    e = next(s for s in G["shapes"] if s["S"] == 32768)
+    N, S = e["N"], e["S"]
+    db = np.frombuffer(port.detrng(G["store_seed"]).fill(1 << 30), np.uint8)
+    qg = port.detrng(G["query_rng_seed"])
+    b = next(x for x in e["batches"] if x["B"] == 16)
+    q = np.stack([np.frombuffer(qg.fill(N // 8), np.uint8) for _ in range(16)])
+    out = port.answer_batch(db, N, S, q[b["rows"]], len(b["rows"]), threads=8)
+    assert [sha(out[i]) for i in range(len(b["rows"]))] == b["out_rows_sha256"]
