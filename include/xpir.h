@@ -108,18 +108,24 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
                                  const uint8_t* d_mask_seeds, uint8_t* d_out, void* stream);
 uint64_t xpir_query_window_bytes(const xpir_store* st);
 
-/* Sharded scan with the cross-GPU XOR reduction FUSED into the scan kernel's
- * epilogue: every accumulator flush of this shard's partial answers is XORed
- * (64-bit atomics over NVLink) straight into the answer buffer of the rank that
- * owns the row — rank k owns rows [row_bounds[k], row_bounds[k+1]) and its
- * buffer out_ptrs[k] (a local or CUDA-IPC-mapped peer pointer) holds all B rows
- * at the same offsets. Each owner must have initialised its rows (zero or mask
- * pad, xpir_init_rows_dev) before any rank launches; after every rank's scan
- * completes the owner's rows are final. Needs S % 32 == 0 and B >= 2048
+/* Sharded scan with the cross-GPU XOR reduction FUSED into the scan kernel:
+ * rank k owns answer rows [row_bounds[k], row_bounds[k+1]) in its buffer
+ * out_ptrs[k] (a local or CUDA-IPC-mapped peer pointer; every buffer holds all B
+ * rows at the same offsets); this call is rank self_rank. Inside the kernel the
+ * segment partials of each (request tile, 32-byte column tile) accumulate in a
+ * local buffer, and the tile's last segment pushes its finished rows to their
+ * owners with 64-bit system-scope XOR reductions (NVLink) while other tiles are
+ * still scanning: B*S bytes per rank per batch, (G-1)/G of them to peers — the
+ * volume of a reduce-scatter. Each owner must have initialised its rows (zero or
+ * mask pad, xpir_init_rows_dev) before any rank launches; once every rank's scan
+ * has completed the owner's rows are final. Needs S % 32 == 0 and B >= 2048
  * (runs the quad-table M4RM kernel 8); 1..8 ranks. pir::reconstruct semantics. */
 int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, uint32_t batch,
                                       uint8_t* const* out_ptrs, const uint32_t* row_bounds, uint32_t n_ranks,
-                                      void* stream);
+                                      uint32_t self_rank, void* stream);
+/* Debug counters of the fused epilogue on this store: bytes pushed to peer ranks'
+ * rows and to this rank's own rows since the last reset (synchronises the device). */
+int xpir_store_peer_stats(xpir_store* st, uint64_t* remote_bytes, uint64_t* own_bytes, int reset);
 /* d_out rows [r0, r1) of S bytes = mask pad prng_expand(mask_seed_r, S) (or zero). */
 int xpir_init_rows_dev(int device, uint8_t* d_out, uint32_t r0, uint32_t r1, uint32_t S,
                        const uint8_t* d_mask_seeds, void* stream);
@@ -170,14 +176,21 @@ int xpir_probe_tmem(int device, int variant, double* bytes_per_clk_sm);
 /* Read batcher ("Read requests are batched and forwarded to   */
 /* the GPU"): concurrent single-request callers — server::answer_share       */
 /* (server.cpp:115-135) from node.cpp's session/link threads — are coalesced  */
-/* into one scan. A batch is sealed when it holds max_batch requests or       */
-/* max_wait_us after its first request; three pinned batches rotate (one    */
-/* forming, one scanning, one completing). Callers pack their own query and */
-/* unpack their own answer. Thread-safe; the store must outlive the batcher.  */
+/* into one scan. A batch is sealed at once while the device is idle, else  */
+/* when it holds max_batch requests or max_wait_us after its first request; */
+/* three pinned batches rotate (one forming, one scanning, one completing). */
+/* Callers pack their own query and unpack their own answer. Thread-safe;   */
+/* the store must outlive the batcher.                                      */
 /* ------------------------------------------------------------------------ */
 typedef struct xpir_batcher xpir_batcher;
 
 int xpir_batcher_create(xpir_store* st, uint32_t max_batch, uint32_t max_wait_us, xpir_batcher** out);
+/* A batcher with no default store, for snapshots of N buckets x S bytes on
+ * `device`: every request names its store (xpir_batcher_answer_on). Batches are
+ * sealed adaptively: at once while no batch is in flight, else when full or
+ * max_wait_us after their first request, whichever comes first. */
+int xpir_batcher_create_geometry(int device, uint32_t N, uint32_t S, uint32_t max_batch, uint32_t max_wait_us,
+                                 xpir_batcher** out);
 /* Waits for the requests already submitted, then stops the worker. */
 int xpir_batcher_destroy(xpir_batcher* b);
 /* Blocking: out (bucket_size bytes) = pir::answer(snapshot, q) (pir.cpp:29-39), or
@@ -185,6 +198,13 @@ int xpir_batcher_destroy(xpir_batcher* b);
  * (answer_share, server.cpp:122-123). q holds ceil(N/8) bytes; q_bits must be N. */
 int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, const uint8_t* mask_seed,
                         uint8_t* out);
+/* The same against another store of the batcher's geometry (whole snapshot, same
+ * N and bucket size, same device) — e.g. another sealed epoch of a server ring:
+ * requests are batched per (store, masked). The store must stay alive (and, for
+ * a server ring image, pinned: xpir_server_snapshot_acquire) until the call
+ * returns. */
+int xpir_batcher_answer_on(xpir_batcher* b, xpir_store* st, const uint8_t* q, uint32_t q_bits,
+                           const uint8_t* mask_seed, uint8_t* out);
 int xpir_batcher_stats(xpir_batcher* b, uint64_t* requests, uint64_t* batches, uint64_t* max_batch_seen);
 
 /* ------------------------------------------------------------------------ */
@@ -239,6 +259,10 @@ int xpir_table_destroy(xpir_table* t);
  * {stored, dropped, gc_evicted, displacements} (InsertReport, cuckoo.hpp:23-28). */
 int xpir_table_insert_batch(xpir_table* t, const uint32_t* beta1, const uint32_t* beta2,
                             const uint8_t* payload, uint64_t n, uint32_t* reports);
+/* Device-resident inputs. beta1/beta2 are range-checked on the device before
+ * the walk (one small kernel + a 4-byte read back): the items before the first
+ * out-of-range index are inserted, then XPIR_EINVAL (cuckoo.cpp:57-58), exactly
+ * as the host entry point and a loop of Table::insert calls. */
 int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_beta1, const uint32_t* d_beta2,
                                 const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
                                 void* stream);
@@ -258,6 +282,8 @@ typedef struct {
 int xpir_table_create_shard(int device, uint32_t buckets, uint32_t depth, uint64_t capacity, uint64_t item_size,
                             const uint8_t seed[32], uint32_t lo, uint32_t hi, xpir_table** out);
 int xpir_table_shard(const xpir_table* t, uint32_t* lo, uint32_t* hi);
+/* Range-checked like insert_batch_dev: on XPIR_EINVAL the valid prefix has been
+ * walked and the caller still runs apply_gather / apply_scatter for it. */
 int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_beta1, const uint32_t* d_beta2, uint64_t n,
                                uint32_t* d_reports, void* stream);
 int xpir_table_apply_gather_dev(xpir_table* t, const xpir_shard_map* map, void* stream);
@@ -369,6 +395,13 @@ int xpir_server_seal(xpir_server* sv, uint64_t* epoch);            /* seal_epoch
 /* snapshot_at (server.cpp:83-87); epoch 0 = latest. The store stays owned by the
  * server and valid until its epoch leaves the ring. */
 int xpir_server_snapshot(xpir_server* sv, uint64_t epoch, xpir_store** st);
+/* snapshot_at with a reader pin (the reference keeps a retired snapshot alive
+ * through its shared_ptr, server.cpp:83-87): the image is not reused while
+ * pinned — a seal that pushes a pinned epoch off the ring retires it and seals
+ * into another image; the last release returns it to the spare pool.
+ * epoch 0 = latest; *epoch_out (optional) = the epoch pinned. */
+int xpir_server_snapshot_acquire(xpir_server* sv, uint64_t epoch, xpir_store** st, uint64_t* epoch_out);
+int xpir_server_snapshot_release(xpir_server* sv, xpir_store* st);
 /* ServerCore::make_freeze (server.cpp:45-56): base, newest (= window newest - 1),
  * digest over the frozen deltas and their count; their wire bytes are
  * xpir_window_encode_delta(window, k, ...) for k < count. */

@@ -95,8 +95,9 @@ _SIGS = {
     "xpir_answer_batch_dev": ([_vp, _vp, C.c_uint64, C.c_uint32, C.c_uint32, _vp, _vp, _vp], C.c_int),
     "xpir_answer_batch_seeded_dev": ([_vp, _vp, C.c_uint32, _vp, _vp, _vp], C.c_int),
     "xpir_query_window_bytes": ([_vp], C.c_uint64),
-    "xpir_answer_batch_seeded_peer_dev": ([_vp, _vp, C.c_uint32, C.POINTER(_vp), _u32p, C.c_uint32, _vp],
-                                          C.c_int),
+    "xpir_answer_batch_seeded_peer_dev": ([_vp, _vp, C.c_uint32, C.POINTER(_vp), _u32p, C.c_uint32, C.c_uint32,
+                                           _vp], C.c_int),
+    "xpir_store_peer_stats": ([_vp, _u64p, _u64p, C.c_int], C.c_int),
     "xpir_init_rows_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp], C.c_int),
     "xpir_expand_queries_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint64, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
     "xpir_mask_answer": ([_u8p, C.c_uint64, _u8p, _u8p], C.c_int),
@@ -164,6 +165,11 @@ _SIGS = {
     "xpir_batcher_destroy": ([_vp], C.c_int),
     "xpir_batcher_answer": ([_vp, _u8p, C.c_uint32, _u8p, _u8p], C.c_int),
     "xpir_batcher_stats": ([_vp, _u64p, _u64p, _u64p], C.c_int),
+    "xpir_batcher_create_geometry": ([C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(_vp)],
+                                     C.c_int),
+    "xpir_batcher_answer_on": ([_vp, _vp, _u8p, C.c_uint32, _u8p, _u8p], C.c_int),
+    "xpir_server_snapshot_acquire": ([_vp, C.c_uint64, C.POINTER(_vp), _u64p], C.c_int),
+    "xpir_server_snapshot_release": ([_vp, _vp], C.c_int),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
@@ -431,12 +437,19 @@ class Store:
                                                   _stream(stream)))
 
     def answer_batch_seeded_peer_dev(self, d_seeds, B: int, out_ptrs: list[int], row_bounds: list[int],
-                                     stream=None) -> None:
-        """Shard scan whose epilogue XORs each answer row into its owner rank's buffer."""
+                                     self_rank: int, stream=None) -> None:
+        """Shard scan fused with the cross-GPU XOR reduce: each finished answer tile
+        is pushed once into its owner rank's buffer (include/xpir.h)."""
         ptrs = (_vp * len(out_ptrs))(*out_ptrs)
         bounds = np.ascontiguousarray(row_bounds, np.uint32)
         _check(lib().xpir_answer_batch_seeded_peer_dev(self.h, _ptr(d_seeds), B, ptrs, _p(bounds, _u32p),
-                                                       len(out_ptrs), _stream(stream)))
+                                                       len(out_ptrs), self_rank, _stream(stream)))
+
+    def peer_stats(self, reset: bool = False) -> dict:
+        """Bytes the fused epilogue pushed to peer ranks' rows / own rows."""
+        r, o = C.c_uint64(), C.c_uint64()
+        _check(lib().xpir_store_peer_stats(self.h, C.byref(r), C.byref(o), 1 if reset else 0))
+        return {"remote_bytes": r.value, "own_bytes": o.value}
 
 
 class Batcher:
@@ -445,11 +458,20 @@ class Batcher:
     server.cpp:115-135) are coalesced into one scan of up to ``max_batch``
     requests, sealed ``max_wait_us`` after its first request."""
 
-    def __init__(self, store: Store, max_batch: int = 1024, max_wait_us: int = 200):
+    def __init__(self, store: "Store | None", max_batch: int = 1024, max_wait_us: int = 200,
+                 geometry: tuple[int, int] | None = None, device: int = 0):
+        """store: the batcher's default store; or store=None and geometry=(N, S): a
+        batcher for any whole store of that geometry (answer_on)."""
         import threading
 
         h = _vp()
-        _check(lib().xpir_batcher_create(store.h, max_batch, max_wait_us, C.byref(h)))
+        if store is None:
+            N, S = geometry
+            _check(lib().xpir_batcher_create_geometry(device, N, S, max_batch, max_wait_us, C.byref(h)))
+            self.N, self.S = N, S
+        else:
+            _check(lib().xpir_batcher_create(store.h, max_batch, max_wait_us, C.byref(h)))
+            self.N, self.S = store.N, store.S
         self.h, self.store = h, store
         # callers inside a C call; close() waits for them before destroying the handle
         self._cv, self._users = threading.Condition(), 0
@@ -479,16 +501,22 @@ class Batcher:
             if self._users == 0:
                 self._cv.notify_all()
 
-    def answer(self, q, mask_seed: bytes | None = None, q_bits: int | None = None) -> np.ndarray:
-        """pir::answer(snapshot, q), or mask_answer(answer(..), mask_seed) (pir.cpp:29-39, 65-69)."""
+    def answer(self, q, mask_seed: bytes | None = None, q_bits: int | None = None, store: "Store | None" = None
+               ) -> np.ndarray:
+        """pir::answer(snapshot, q), or mask_answer(answer(..), mask_seed) (pir.cpp:29-39, 65-69);
+        against `store` (same geometry) instead of the default store when given."""
         qa = _u8(q).reshape(-1)
-        if qa.size < (self.store.N + 7) // 8:
+        if qa.size < (self.N + 7) // 8:
             raise InvalidArgument(XPIR_EINVAL, "answer: query length mismatch")
-        out = np.empty(self.store.S, np.uint8)
+        out = np.empty(self.S, np.uint8)
         ms = _p(_u8(mask_seed)) if mask_seed is not None else None
+        qb = self.N if q_bits is None else q_bits
         h = self._enter()
         try:
-            _check(lib().xpir_batcher_answer(h, _p(qa), self.store.N if q_bits is None else q_bits, ms, _p(out)))
+            if store is None:
+                _check(lib().xpir_batcher_answer(h, _p(qa), qb, ms, _p(out)))
+            else:
+                _check(lib().xpir_batcher_answer_on(h, store.h, _p(qa), qb, ms, _p(out)))
         finally:
             self._leave()
         return out
@@ -898,6 +926,15 @@ class Server:
         st = _vp()
         _check(lib().xpir_server_snapshot(self.h, epoch, C.byref(st)))
         return _BorrowedStore(st, self.buckets, self.depth * self.item, self.device, self.lo, self.hi)
+
+    def snapshot_acquire(self, epoch: int = 0) -> tuple[Store, int]:
+        """snapshot_at with a reader pin: the image is not reused until released."""
+        st, ep = _vp(), C.c_uint64()
+        _check(lib().xpir_server_snapshot_acquire(self.h, epoch, C.byref(st), C.byref(ep)))
+        return _BorrowedStore(st, self.buckets, self.depth * self.item, self.device, self.lo, self.hi), ep.value
+
+    def snapshot_release(self, store: Store) -> None:
+        _check(lib().xpir_server_snapshot_release(self.h, store.h))
 
     def info(self):
         w, l, o = C.c_uint64(), C.c_uint64(), C.c_uint64()

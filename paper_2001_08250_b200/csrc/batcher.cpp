@@ -48,6 +48,7 @@ struct BBuf {
     cudaStream_t stream = nullptr;
     cudaEvent_t done_ev = nullptr;
     BState state = BState::Idle;
+    xpir_store* st = nullptr;  // the store this batch scans (fixed when it starts forming)
     bool masked = false;
     uint32_t count = 0;
     std::atomic<uint32_t> filled{0};  // callers done packing (no lock: the worker polls it after sealing)
@@ -101,11 +102,15 @@ struct xpir_batcher {
             for (auto& x : buf)  // the oldest forming batch first
                 if (x.state == BState::Forming && (!b || x.gen < b->gen)) b = &x;
             if (!b) break;  // stop, nothing pending
+            // Adaptive sealing: while the device is idle a batch is sealed at once (a lone
+            // caller pays no batching delay); while a batch is in flight it keeps forming
+            // until it is full, max_wait_us have passed, or the device goes idle.
             const auto deadline = b->first + std::chrono::microseconds(max_wait_us);
-            cv_work.wait_until(lk, deadline, [&] { return stop.load() || b->count >= max_batch; });
+            cv_work.wait_until(lk, deadline, [&] { return stop.load() || b->count >= max_batch || inflight.empty(); });
             b->state = BState::Sealed;  // no more joins
             const uint32_t B = b->count;
             const bool masked = b->masked;
+            xpir_store* const bst = b->st;
             lk.unlock();
             // the joined callers are copying their rows in (a few microseconds)
             while (b->filled.load(std::memory_order_acquire) != B) std::this_thread::yield();
@@ -123,7 +128,8 @@ struct xpir_batcher {
                 err = std::string("batcher H2D: ") + cudaGetErrorString(e);
             }
             if (!rc) {
-                rc = xpir_answer_batch_dev(st, b->d_rows, nb, N, B, masked ? b->d_seeds : nullptr, b->d_out, b->stream);
+                rc = xpir_answer_batch_dev(bst, b->d_rows, nb, N, B, masked ? b->d_seeds : nullptr, b->d_out,
+                                           b->stream);
                 if (rc) err = xpir_last_error();
             }
             if (!rc) {
@@ -161,6 +167,7 @@ struct xpir_batcher {
             inflight.pop_front();
             publish(b, e == cudaSuccess ? XPIR_OK : XPIR_ECUDA,
                     e == cudaSuccess ? std::string() : std::string("batcher: ") + cudaGetErrorString(e));
+            if (inflight.empty()) cv_work.notify_one();  // a forming batch may go now
         }
     }
 };
@@ -172,7 +179,7 @@ void free_bufs(xpir_batcher* b) {
     for (auto& x : b->buf) {
         if (x.stream) {
             cudaStreamSynchronize(x.stream);
-            xpir::store_release_stream_scratch(b->st, x.stream);
+            if (b->st) xpir::store_release_stream_scratch(b->st, x.stream);
         }
         for (uint8_t* p : {x.rows, x.seeds, x.out})
             if (p) cudaFreeHost(p);
@@ -186,17 +193,8 @@ void free_bufs(xpir_batcher* b) {
 
 extern "C" {
 
-int xpir_batcher_create(xpir_store* st, uint32_t max_batch, uint32_t max_wait_us, xpir_batcher** out) {
-    if (!st || !out) return bfail(XPIR_EINVAL, "batcher_create: null argument");
-    if (max_batch == 0) return bfail(XPIR_EINVAL, "batcher_create: max_batch must be positive");
-    uint32_t N, S, lo, hi;
-    uint64_t epoch;
-    void* data = nullptr;
-    int rc = xpir_store_info(st, &N, &S, &lo, &hi, &epoch, &data);
-    if (rc) return rc;
-    int dev = 0;
-    cudaPointerAttributes pa{};
-    if (data && cudaPointerGetAttributes(&pa, data) == cudaSuccess) dev = pa.device;
+static int batcher_create(xpir_store* st, int dev, uint32_t N, uint32_t S, uint32_t max_batch,
+                          uint32_t max_wait_us, xpir_batcher** out) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(dev);
@@ -241,6 +239,28 @@ int xpir_batcher_create(xpir_store* st, uint32_t max_batch, uint32_t max_wait_us
     return XPIR_OK;
 }
 
+int xpir_batcher_create(xpir_store* st, uint32_t max_batch, uint32_t max_wait_us, xpir_batcher** out) {
+    if (!st || !out) return bfail(XPIR_EINVAL, "batcher_create: null argument");
+    if (max_batch == 0) return bfail(XPIR_EINVAL, "batcher_create: max_batch must be positive");
+    uint32_t N, S, lo, hi;
+    uint64_t epoch;
+    void* data = nullptr;
+    int rc = xpir_store_info(st, &N, &S, &lo, &hi, &epoch, &data);
+    if (rc) return rc;
+    int dev = 0;
+    cudaPointerAttributes pa{};
+    if (data && cudaPointerGetAttributes(&pa, data) == cudaSuccess) dev = pa.device;
+    return batcher_create(st, dev, N, S, max_batch, max_wait_us, out);
+}
+
+int xpir_batcher_create_geometry(int device, uint32_t N, uint32_t S, uint32_t max_batch, uint32_t max_wait_us,
+                                 xpir_batcher** out) {
+    if (!out) return bfail(XPIR_EINVAL, "batcher_create: null argument");
+    if (max_batch == 0) return bfail(XPIR_EINVAL, "batcher_create: max_batch must be positive");
+    if (N == 0 || S == 0) return bfail(XPIR_EINVAL, "batcher_create: empty geometry");
+    return batcher_create(nullptr, device, N, S, max_batch, max_wait_us, out);
+}
+
 int xpir_batcher_destroy(xpir_batcher* b) {
     if (!b) return XPIR_OK;
     {
@@ -263,8 +283,22 @@ int xpir_batcher_destroy(xpir_batcher* b) {
 
 int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, const uint8_t* mask_seed,
                         uint8_t* out) {
-    if (!b || !q || !out) return bfail(XPIR_EINVAL, "batcher_answer: null argument");
+    if (!b) return bfail(XPIR_EINVAL, "batcher_answer: null argument");
+    if (!b->st) return bfail(XPIR_EINVAL, "batcher_answer: batcher created by geometry: use xpir_batcher_answer_on");
+    return xpir_batcher_answer_on(b, b->st, q, q_bits, mask_seed, out);
+}
+
+int xpir_batcher_answer_on(xpir_batcher* b, xpir_store* st, const uint8_t* q, uint32_t q_bits,
+                           const uint8_t* mask_seed, uint8_t* out) {
+    if (!b || !st || !q || !out) return bfail(XPIR_EINVAL, "batcher_answer: null argument");
     if (q_bits != b->N) return bfail(XPIR_EINVAL, "answer: query length mismatch");  // pir.cpp:30-31
+    if (st != b->st) {  // another snapshot of the same geometry (e.g. another sealed epoch)
+        uint32_t N = 0, S = 0, lo = 0, hi = 0;
+        int rc = xpir_store_info(st, &N, &S, &lo, &hi, nullptr, nullptr);
+        if (rc) return rc;
+        if (N != b->N || S != b->S || lo != 0 || hi != N)
+            return bfail(XPIR_EINVAL, "batcher_answer: store geometry differs from the batcher's");
+    }
     const bool masked = mask_seed != nullptr;
     std::unique_lock<std::mutex> lk(b->mu);
     if (b->stop) return bfail(XPIR_ESTATE, "batcher_answer: batcher is shutting down");
@@ -287,7 +321,7 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
             return bfail(XPIR_ESTATE, "batcher_answer: batcher is shutting down");
         }
         for (auto& x : b->buf)
-            if (x.state == BState::Forming && x.masked == masked && x.count < b->max_batch) buf = &x;
+            if (x.state == BState::Forming && x.masked == masked && x.st == st && x.count < b->max_batch) buf = &x;
         if (!buf)
             for (auto& x : b->buf)
                 if (x.state == BState::Idle) {
@@ -295,6 +329,7 @@ int xpir_batcher_answer(xpir_batcher* b, const uint8_t* q, uint32_t q_bits, cons
                     uint64_t g = 0;
                     for (auto& y : b->buf) g = y.gen > g ? y.gen : g;
                     x.state = BState::Forming;
+                    x.st = st;
                     x.masked = masked;
                     x.count = 0;
                     x.filled.store(0, std::memory_order_relaxed);

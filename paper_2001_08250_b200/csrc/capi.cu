@@ -78,6 +78,36 @@ void timing_end(cudaStream_t s, cudaEvent_t a) {
     std::lock_guard<std::mutex> lk(g_tmu);
     g_events.emplace_back(a, b);
 }
+
+// Per-thread, per-device scratch of the small host-buffer entry points
+// (mask_answer, prng_expand, prf_batch, make_interest_batch, bloom_positions):
+// a grow-only device buffer and a non-blocking stream, so a call is
+// copy-in / kernel / copy-out / stream sync — no cudaMalloc/cudaFree (cudaFree
+// synchronises the whole device, stalling every concurrent scan) and no work on
+// the legacy default stream.
+struct CallScratch {
+    int device = -1;
+    cudaStream_t s = nullptr;
+    DevBuf dev;
+    ~CallScratch() {
+        if (s) cudaStreamDestroy(s);
+        dev.release();
+    }
+};
+CallScratch& call_scratch() {
+    thread_local CallScratch per_dev[16];
+    int d = 0;
+    cudaGetDevice(&d);
+    CallScratch& cs = per_dev[d & 15];
+    if (cs.device != d) {
+        if (cs.s) cudaStreamDestroy(cs.s);
+        cs.dev.release();
+        cs.s = nullptr;
+        cs.device = d;
+        if (cudaStreamCreateWithFlags(&cs.s, cudaStreamNonBlocking) != cudaSuccess) cs.s = nullptr;
+    }
+    return cs;
+}
 }  // namespace
 
 extern "C" {
@@ -225,6 +255,9 @@ int xpir_store_destroy(xpir_store* st) {
     }
     st->qx.release();
     st->idx.release();
+    st->peer_partial.release();
+    st->peer_cnt.release();
+    st->peer_stats.release();
     cudaStreamDestroy(st->stream);
     delete st;
     return XPIR_OK;
@@ -617,9 +650,10 @@ int xpir_answer_batch_seeded(xpir_store* st, const uint8_t* seeds, uint32_t B,
 
 int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, uint32_t B,
                                       uint8_t* const* out_ptrs, const uint32_t* row_bounds, uint32_t n_ranks,
-                                      void* stream) {
+                                      uint32_t self_rank, void* stream) {
     if (!st) return fail(XPIR_EINVAL, "answer_batch_seeded_peer: null store");
     if (n_ranks < 1 || n_ranks > 8) return fail(XPIR_EINVAL, "answer_batch_seeded_peer: 1..8 ranks");
+    if (self_rank >= n_ranks) return fail(XPIR_EINVAL, "answer_batch_seeded_peer: self_rank out of range");
     if (!out_ptrs || !row_bounds || (B && !d_seeds)) return fail(XPIR_EINVAL, "answer_batch_seeded_peer: null");
     if (row_bounds[0] != 0 || row_bounds[n_ranks] != B)
         return fail(XPIR_EINVAL, "answer_batch_seeded_peer: row bounds must cover [0, B)");
@@ -629,22 +663,52 @@ int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, ui
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : st->stream;
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
     const uint64_t qs = m4rm_qstride(B);
+    // fix-up state of the fused epilogue: zero at (re)allocation, kept zero by the kernel
+    const uint64_t tiles = uint64_t(st->S / 32) * ((B + 2047) / 2048);
+    auto zeroed = [&](DevBuf& b, uint64_t n) -> cudaError_t {
+        const size_t cap0 = b.cap;
+        const void* p0 = b.p;
+        cudaError_t e = b.ensure(n);
+        if (e == cudaSuccess && (b.cap != cap0 || b.p != p0)) e = cudaMemsetAsync(b.p, 0, b.cap, s);
+        return e;
+    };
+    XCK(zeroed(st->peer_partial, uint64_t(B) * st->S));
+    XCK(zeroed(st->peer_cnt, 4 * tiles));
+    XCK(zeroed(st->peer_stats, 16));
     DevBuf& qw = st->qwin_for(s);
     XCK(qw.ensure(m4rm_qrows(nbw) * qs));
     XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s, true));  // the fused path always runs kernel 8
     M4Args a{st->data, st->nb(), st->S, qw.as<uint8_t>(), qs, B, out_ptrs[0], s};
     a.peers.n = n_ranks;
+    a.peers.self = self_rank;
     for (uint32_t k = 0; k < n_ranks; ++k) {
         a.peers.ptr[k] = out_ptrs[k];
         a.peers.bound[k] = row_bounds[k];
     }
     a.peers.bound[n_ranks] = row_bounds[n_ranks];
+    a.peers.partial = st->peer_partial.as<uint8_t>();
+    a.peers.tile_cnt = st->peer_cnt.as<uint32_t>();
+    a.peers.stats = st->peer_stats.as<unsigned long long>();
     cudaEvent_t ev;
     timing_begin(s, &ev);
     XCK(launch_scan_m4rm_q(a, num_sms(st->device)));
     timing_end(s, ev);
     count_launches(2);
     g_last_kernel = 8;
+    return XPIR_OK;
+}
+
+int xpir_store_peer_stats(xpir_store* st, uint64_t* remote_bytes, uint64_t* own_bytes, int reset) {
+    if (!st) return fail(XPIR_EINVAL, "store_peer_stats: null store");
+    uint64_t v[2] = {0, 0};
+    if (st->peer_stats.p) {
+        DeviceGuard g(st->device);
+        XCK(cudaDeviceSynchronize());
+        XCK(cudaMemcpy(v, st->peer_stats.p, 16, cudaMemcpyDeviceToHost));
+        if (reset) XCK(cudaMemset(st->peer_stats.p, 0, 16));
+    }
+    if (remote_bytes) *remote_bytes = v[0];
+    if (own_bytes) *own_bytes = v[1];
     return XPIR_OK;
 }
 
@@ -672,16 +736,17 @@ int xpir_mask_answer(const uint8_t* ans, uint64_t len, const uint8_t seed[32], u
     if (!seed || (len && (!ans || !out))) return fail(XPIR_EINVAL, "mask_answer: null buffer");
     if (!len) return XPIR_OK;
     if (len > 0xffffffffull) return fail(XPIR_EINVAL, "mask_answer: answer too long");
-    uint8_t* d = nullptr;
-    XCK(cudaMalloc(&d, len + 32));
-    cudaError_t e = cudaMemcpy(d, ans, len, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(d + len, seed, 32, cudaMemcpyHostToDevice);
+    CallScratch& cs = call_scratch();
+    if (!cs.s) return fail(XPIR_ECUDA, "mask_answer: no stream");
+    XCK(cs.dev.ensure(len + 32));
+    uint8_t* d = cs.dev.as<uint8_t>();
+    XCK(cudaMemcpyAsync(d, ans, len, cudaMemcpyHostToDevice, cs.s));
+    XCK(cudaMemcpyAsync(d + len, seed, 32, cudaMemcpyHostToDevice, cs.s));
     // one "request" of S = len bytes: out = ans ^ pad
-    if (e == cudaSuccess) e = launch_init_out(d, 1, uint32_t(len), d + len, true, nullptr);
+    XCK(launch_init_out(d, 1, uint32_t(len), d + len, true, cs.s));
     count_launches(1);
-    if (e == cudaSuccess) e = cudaMemcpy(out, d, len, cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    XCK(e);
+    XCK(cudaMemcpyAsync(out, d, len, cudaMemcpyDeviceToHost, cs.s));
+    XCK(cudaStreamSynchronize(cs.s));
     return XPIR_OK;
 }
 
@@ -709,13 +774,13 @@ int xpir_xor_reduce_dev(int device, uint8_t* d_dst, const uint8_t* const* d_srcs
 int xpir_prng_expand(const uint8_t seed[32], uint8_t* out, uint64_t len) {
     if (!seed || (len && !out)) return fail(XPIR_EINVAL, "prng_expand: null buffer");
     if (!len) return XPIR_OK;
-    uint8_t* d = nullptr;
-    XCK(cudaMalloc(&d, len));
-    cudaError_t e = launch_keystream(seed, 0, 0, d, len, nullptr);
+    CallScratch& cs = call_scratch();
+    if (!cs.s) return fail(XPIR_ECUDA, "prng_expand: no stream");
+    XCK(cs.dev.ensure(len));
+    XCK(launch_keystream(seed, 0, 0, cs.dev.as<uint8_t>(), len, cs.s));
     count_launches(1);
-    if (e == cudaSuccess) e = cudaMemcpy(out, d, len, cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    XCK(e);
+    XCK(cudaMemcpyAsync(out, cs.dev.p, len, cudaMemcpyDeviceToHost, cs.s));
+    XCK(cudaStreamSynchronize(cs.s));
     return XPIR_OK;
 }
 
@@ -743,14 +808,15 @@ int xpir_prf_batch(const uint8_t key[16], const uint64_t* inputs, uint64_t n, ui
     if (modulus == 0) return fail(XPIR_EINVAL, "prf: modulus must be positive");
     if (!key || (n && (!inputs || !out))) return fail(XPIR_EINVAL, "prf: null buffer");
     if (!n) return XPIR_OK;
-    uint64_t* d = nullptr;
-    XCK(cudaMalloc(&d, 16 * n));
-    cudaError_t e = cudaMemcpy(d, inputs, 8 * n, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = launch_prf(ld64le(key), ld64le(key + 8), d, n, modulus, d + n, nullptr, nullptr);
+    CallScratch& cs = call_scratch();
+    if (!cs.s) return fail(XPIR_ECUDA, "prf: no stream");
+    XCK(cs.dev.ensure(16 * n));
+    uint64_t* d = cs.dev.as<uint64_t>();
+    XCK(cudaMemcpyAsync(d, inputs, 8 * n, cudaMemcpyHostToDevice, cs.s));
+    XCK(launch_prf(ld64le(key), ld64le(key + 8), d, n, modulus, d + n, nullptr, cs.s));
     count_launches(1);
-    if (e == cudaSuccess) e = cudaMemcpy(out, d + n, 8 * n, cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    XCK(e);
+    XCK(cudaMemcpyAsync(out, d + n, 8 * n, cudaMemcpyDeviceToHost, cs.s));
+    XCK(cudaStreamSynchronize(cs.s));
     return XPIR_OK;
 }
 
@@ -770,17 +836,17 @@ int xpir_make_interest_batch(uint32_t m_bits, uint32_t h, const uint8_t id[16],
     if (m_bits == 0) return fail(XPIR_EINVAL, "bloom_positions: m_bits must be positive");
     if (!id || (n && (!seqs || !out))) return fail(XPIR_EINVAL, "make_interest: null buffer");
     if (!n || !h) return XPIR_OK;
-    uint64_t* ds = nullptr;
-    uint32_t* dp = nullptr;
-    XCK(cudaMalloc(&ds, 8 * n));
-    cudaError_t e = cudaMalloc(&dp, 4 * n * h);
-    if (e == cudaSuccess) e = cudaMemcpy(ds, seqs, 8 * n, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = launch_interest(id, ds, n, h, m_bits, dp, nullptr, nullptr);
+    CallScratch& cs = call_scratch();
+    if (!cs.s) return fail(XPIR_ECUDA, "make_interest: no stream");
+    const uint64_t pos_off = round16(8 * n);
+    XCK(cs.dev.ensure(pos_off + 4 * n * h));
+    uint64_t* ds = cs.dev.as<uint64_t>();
+    uint32_t* dp = reinterpret_cast<uint32_t*>(cs.dev.as<uint8_t>() + pos_off);
+    XCK(cudaMemcpyAsync(ds, seqs, 8 * n, cudaMemcpyHostToDevice, cs.s));
+    XCK(launch_interest(id, ds, n, h, m_bits, dp, nullptr, cs.s));
     count_launches(1);
-    if (e == cudaSuccess) e = cudaMemcpy(out, dp, 4 * n * h, cudaMemcpyDeviceToHost);
-    cudaFree(ds);
-    cudaFree(dp);
-    XCK(e);
+    XCK(cudaMemcpyAsync(out, dp, 4 * n * h, cudaMemcpyDeviceToHost, cs.s));
+    XCK(cudaStreamSynchronize(cs.s));
     return XPIR_OK;
 }
 
@@ -790,15 +856,16 @@ int xpir_bloom_positions(const uint8_t* item, uint64_t len, uint32_t h, uint32_t
     if (len > 120) return fail(XPIR_EINVAL, "bloom_positions: device port takes items <= 120 bytes");
     if ((len && !item) || (h && !out)) return fail(XPIR_EINVAL, "bloom_positions: null buffer");
     if (!h) return XPIR_OK;
-    uint8_t* d = nullptr;
-    XCK(cudaMalloc(&d, 128 + 4 * uint64_t(h)));
-    cudaError_t e = len ? cudaMemcpy(d, item, len, cudaMemcpyHostToDevice) : cudaSuccess;
+    CallScratch& cs = call_scratch();
+    if (!cs.s) return fail(XPIR_ECUDA, "bloom_positions: no stream");
+    XCK(cs.dev.ensure(128 + 4 * uint64_t(h)));
+    uint8_t* d = cs.dev.as<uint8_t>();
+    if (len) XCK(cudaMemcpyAsync(d, item, len, cudaMemcpyHostToDevice, cs.s));
     uint32_t* dp = reinterpret_cast<uint32_t*>(d + 128);
-    if (e == cudaSuccess) e = launch_bloom_item(d, uint32_t(len), h, m_bits, dp, nullptr);
+    XCK(launch_bloom_item(d, uint32_t(len), h, m_bits, dp, cs.s));
     count_launches(1);
-    if (e == cudaSuccess) e = cudaMemcpy(out, dp, 4 * uint64_t(h), cudaMemcpyDeviceToHost);
-    cudaFree(d);
-    XCK(e);
+    XCK(cudaMemcpyAsync(out, dp, 4 * uint64_t(h), cudaMemcpyDeviceToHost, cs.s));
+    XCK(cudaStreamSynchronize(cs.s));
     return XPIR_OK;
 }
 

@@ -152,6 +152,7 @@ struct xpir_store {
     uint8_t* data = nullptr;
     cudaStream_t stream = nullptr;
     DevBuf q, out, seeds, masks, qwin, qx, idx;
+    DevBuf peer_partial, peer_cnt, peer_stats;  // fused cross-GPU epilogue (xpir_answer_batch_seeded_peer_dev)
     std::mutex mu;
     // Query-window scratch of the device-pointer entry points, one per caller
     // stream, so calls on different streams may run concurrently (read batcher).
@@ -180,7 +181,7 @@ struct xpir_table {
     uint8_t* data = nullptr;  // payloads of buckets [lo, hi)
     uint32_t lo = 0, hi = 0;  // a payload shard of the logical table (metadata is whole)
     cudaStream_t stream = nullptr;
-    DevBuf in_b1, in_b2, in_payload, in_reports, gather;
+    DevBuf in_b1, in_b2, in_payload, in_reports, gather, chk;
     CuckooParScratch par;
     bool parallel_prefix = true;  // XPIR_CUCKOO_SEQUENTIAL=1 disables (A/B checks)
     std::mutex mu;
@@ -188,6 +189,11 @@ struct xpir_table {
     uint64_t data_bytes() const { return uint64_t(hi - lo) * d.depth * d.item; }
     bool sharded() const { return lo != 0 || hi != d.buckets; }
 };
+
+// xpir_table_insert_walk_dev without the device-side bucket range check, for
+// callers that validated beta1/beta2 on the host (capi_table.cu).
+int table_walk_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n, uint32_t* d_reports,
+                    void* stream);
 
 struct xpir_window {
     int device;
@@ -210,9 +216,11 @@ struct xpir_server {
         uint64_t epoch;
         uint32_t since_batch;  // table batch id the image is synchronised with
         xpir_store* st;
+        uint32_t pins = 0;     // readers holding the image (xpir_server_snapshot_acquire)
     };
     std::deque<Sealed> ring;           // oldest first
-    std::vector<xpir_store*> spare;    // pre-allocated images (xpir_server_reserve)
+    std::vector<Sealed> retired;       // left the ring while pinned; back to spare on the last release
+    std::vector<xpir_store*> spare;    // images with no epoch (xpir_server_reserve, released retirees)
     std::mutex mu;
 };
 

@@ -10,10 +10,21 @@ static int server_seal(xpir_server* sv, uint64_t* epoch_out) {  // server.cpp:75
     xpir_table* t = sv->table;
     DeviceGuard g(sv->device);
     xpir_server::Sealed e{};
+    bool incremental = false;
     if (sv->ring.size() >= sv->epoch_ring) {
-        // reuse the oldest image: only slots rewritten since it was sealed are copied
+        // the oldest epoch leaves the ring (server.cpp:79); its image is reused
+        // unless a reader still holds it, in which case it is retired until released
         e = sv->ring.front();
         sv->ring.pop_front();
+        if (e.pins) {
+            sv->retired.push_back(e);
+            e = xpir_server::Sealed{};
+        } else {
+            incremental = true;
+        }
+    }
+    if (incremental) {
+        // only slots rewritten since this image was sealed are copied
         XCK(launch_seal_incremental(t->d, t->lo, t->hi, e.since_batch, t->data, e.st->data, num_sms(sv->device),
                                     t->stream));
         count_launches(1);
@@ -29,6 +40,7 @@ static int server_seal(xpir_server* sv, uint64_t* epoch_out) {  // server.cpp:75
         XCK(cudaMemcpyAsync(e.st->data, t->data, e.st->bytes(), cudaMemcpyDeviceToDevice, t->stream));
     }
     XCK(cudaStreamSynchronize(t->stream));
+    e.pins = 0;
     e.since_batch = t->h.batch_id;
     e.epoch = ++sv->latest_epoch;
     e.st->epoch = e.epoch;
@@ -73,6 +85,7 @@ int xpir_server_create_shard(int device, uint32_t buckets, uint32_t depth, uint6
 int xpir_server_destroy(xpir_server* sv) {
     if (!sv) return XPIR_OK;
     for (auto& e : sv->ring) xpir_store_destroy(e.st);
+    for (auto& e : sv->retired) xpir_store_destroy(e.st);
     for (auto* st : sv->spare) xpir_store_destroy(st);
     xpir_table_destroy(sv->table);
     xpir_window_destroy(sv->window);
@@ -102,8 +115,8 @@ static int table_insert_sharded(xpir_table* t, const uint32_t* b1, const uint32_
     XCK(cudaMemcpyAsync(t->in_b1.p, b1, 4 * n, cudaMemcpyHostToDevice, s));
     XCK(cudaMemcpyAsync(t->in_b2.p, b2, 4 * n, cudaMemcpyHostToDevice, s));
     XCK(cudaMemcpyAsync(t->in_payload.p, payload, n * t->d.item, cudaMemcpyHostToDevice, s));
-    int rc = xpir_table_insert_walk_dev(t, t->in_b1.as<uint32_t>(), t->in_b2.as<uint32_t>(), n,
-                                        t->in_reports.as<uint32_t>(), s);
+    // beta ranges were checked on the host (xpir_server_apply_round_sharded)
+    int rc = table_walk_impl(t, t->in_b1.as<uint32_t>(), t->in_b2.as<uint32_t>(), n, t->in_reports.as<uint32_t>(), s);
     if (!rc) rc = xpir_table_apply_gather_dev(t, map, s);
     if (rc) return rc;
     XCK(cudaStreamSynchronize(s));
@@ -191,6 +204,40 @@ int xpir_server_snapshot(xpir_server* sv, uint64_t epoch, xpir_store** st) {  //
     for (auto& e : sv->ring)
         if (e.epoch == epoch) *st = e.st;
     return *st ? XPIR_OK : fail(XPIR_EINVAL, "server_snapshot: epoch not in the ring");
+}
+
+int xpir_server_snapshot_acquire(xpir_server* sv, uint64_t epoch, xpir_store** st, uint64_t* epoch_out) {
+    if (!sv || !st) return fail(XPIR_EINVAL, "server_snapshot_acquire: null argument");
+    std::lock_guard<std::mutex> lk(sv->mu);
+    *st = nullptr;
+    if (epoch == 0) epoch = sv->latest_epoch;
+    for (auto& e : sv->ring)
+        if (e.epoch == epoch) {
+            e.pins += 1;
+            *st = e.st;
+            if (epoch_out) *epoch_out = e.epoch;
+            return XPIR_OK;
+        }
+    return fail(XPIR_EINVAL, "server_snapshot_acquire: epoch not in the ring");
+}
+
+int xpir_server_snapshot_release(xpir_server* sv, xpir_store* st) {
+    if (!sv || !st) return fail(XPIR_EINVAL, "server_snapshot_release: null argument");
+    std::lock_guard<std::mutex> lk(sv->mu);
+    for (auto& e : sv->ring)
+        if (e.st == st && e.pins) {
+            e.pins -= 1;
+            return XPIR_OK;
+        }
+    for (size_t k = 0; k < sv->retired.size(); ++k)
+        if (sv->retired[k].st == st && sv->retired[k].pins) {
+            if (--sv->retired[k].pins == 0) {
+                sv->spare.push_back(st);  // no epoch any more: the next seal copies it whole
+                sv->retired.erase(sv->retired.begin() + long(k));
+            }
+            return XPIR_OK;
+        }
+    return fail(XPIR_EINVAL, "server_snapshot_release: store is not pinned");
 }
 
 // ServerCore::make_freeze (server.cpp:45-56): the deltas that will never change

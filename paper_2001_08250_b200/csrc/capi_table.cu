@@ -26,6 +26,7 @@ static void table_free_all(xpir_table* t) {
     t->in_payload.release();
     t->in_reports.release();
     t->gather.release();
+    t->chk.release();
     t->par.release();
     if (t->stream) cudaStreamDestroy(t->stream);
 }
@@ -106,24 +107,11 @@ int xpir_table_destroy(xpir_table* t) {
     return XPIR_OK;
 }
 
-int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2,
-                                const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
-                                void* stream) {
-    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
-    if (n == 0) return XPIR_OK;
-    if (!d_b1 || !d_b2 || !d_payload) return fail(XPIR_EINVAL, "table_insert: null buffer");
-    if (t->sharded())
-        return fail(XPIR_EINVAL, "table_insert: payload shard: use insert_walk + apply_gather (all shards) + apply_scatter");
-    int rc = xpir_table_insert_walk_dev(t, d_b1, d_b2, n, d_reports, stream);
-    if (rc) return rc;
-    rc = xpir_table_apply_gather_dev(t, nullptr, stream);
-    if (rc) return rc;
-    return xpir_table_apply_scatter_dev(t, d_payload, stream);
-}
+}  // extern "C"
 
-int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n,
-                               uint32_t* d_reports, void* stream) {
-    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+// The walk itself (inputs already range-checked; capi_internal.cuh).
+int table_walk_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n, uint32_t* d_reports,
+                     void* stream) {
     DeviceGuard g(t->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
     t->h.batch_id += 1;
@@ -138,9 +126,10 @@ int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_b1, const uint32
         XCK(cuckoo_parallel_prefix(t->d, t->h, d_b1, d_b2, n < room ? n : room, d_reports, t->par, &applied, s));
         i = applied;
     }
-    for (int guard = 0; i < n; ++guard) {
-        if (t->h.rng_block + 1024 > t->h.draw_base + t->h.draw_count || guard == 0) {
-            // (re)fill the draw window starting at the next unconsumed nonce
+    while (i < n) {
+        if (t->h.rng_block + 1024 > t->h.draw_base + t->h.draw_count) {
+            // (re)fill the draw window starting at the next unconsumed nonce (draws are a
+            // pure function of the nonce, so a window stays valid across rounds)
             t->h.draw_base = t->h.rng_block;
             t->h.draw_count = DRAW_CAP;
             XCK(launch_draws(t->seed, t->h.draw_base, DRAW_CAP, t->d.draws, s));
@@ -158,6 +147,73 @@ int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_b1, const uint32
         if (t->h.status == 1) t->h.draw_count = 0;  // force a refill
     }
     if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+
+// Walk + payload gather/scatter of a whole (unsharded) table.
+static int insert_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, const uint8_t* d_payload,
+                       uint64_t n, uint32_t* d_reports, void* stream) {
+    int rc = table_walk_impl(t, d_b1, d_b2, n, d_reports, stream);
+    if (rc) return rc;
+    rc = xpir_table_apply_gather_dev(t, nullptr, stream);
+    if (rc) return rc;
+    return xpir_table_apply_scatter_dev(t, d_payload, stream);
+}
+
+// cuckoo.cpp:57-58 for device-resident inputs: the index of the first item whose
+// beta1 or beta2 is >= buckets (n when all are in range). The walk kernels index
+// the metadata and payload arrays with these values directly, so a bad one must
+// never reach them.
+static int beta_check(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n, cudaStream_t s,
+                      uint64_t* n_ok) {
+    XCK(t->chk.ensure(8));
+    XCK(launch_beta_check(d_b1, d_b2, n, t->d.buckets, t->chk.as<unsigned long long>(), s));
+    count_launches(1);
+    unsigned long long first_bad = 0;
+    XCK(cudaMemcpyAsync(&first_bad, t->chk.p, 8, cudaMemcpyDeviceToHost, s));
+    XCK(cudaStreamSynchronize(s));
+    *n_ok = first_bad < n ? first_bad : n;
+    return XPIR_OK;
+}
+
+extern "C" {
+
+int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2,
+                                const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
+                                void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+    if (n == 0) return XPIR_OK;
+    if (!d_b1 || !d_b2 || !d_payload) return fail(XPIR_EINVAL, "table_insert: null buffer");
+    if (t->sharded())
+        return fail(XPIR_EINVAL, "table_insert: payload shard: use insert_walk + apply_gather (all shards) + apply_scatter");
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    uint64_t ok = 0;
+    int rc = beta_check(t, d_b1, d_b2, n, s, &ok);
+    if (rc) return rc;
+    if (ok) {  // items before the bad one are inserted, as a loop of Table::insert calls would
+        rc = insert_impl(t, d_b1, d_b2, d_payload, ok, d_reports, stream);
+        if (rc) return rc;
+    }
+    if (ok < n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
+    return XPIR_OK;
+}
+
+int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n,
+                               uint32_t* d_reports, void* stream) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+    if (n == 0) return XPIR_OK;
+    if (!d_b1 || !d_b2) return fail(XPIR_EINVAL, "table_insert: null buffer");
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    uint64_t ok = 0;
+    int rc = beta_check(t, d_b1, d_b2, n, s, &ok);
+    if (rc) return rc;
+    rc = table_walk_impl(t, d_b1, d_b2, ok, d_reports, stream);
+    if (rc) return rc;
+    // EINVAL with the valid prefix walked: the caller still applies gather/scatter
+    if (ok < n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
     return XPIR_OK;
 }
 
@@ -226,9 +282,8 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b
         XCK(cudaMemcpyAsync(t->in_b1.p, b1, 4 * ok, cudaMemcpyHostToDevice, s));
         XCK(cudaMemcpyAsync(t->in_b2.p, b2, 4 * ok, cudaMemcpyHostToDevice, s));
         XCK(cudaMemcpyAsync(t->in_payload.p, payload, ok * t->d.item, cudaMemcpyHostToDevice, s));
-        int rc = xpir_table_insert_batch_dev(t, t->in_b1.as<uint32_t>(), t->in_b2.as<uint32_t>(),
-                                             t->in_payload.as<uint8_t>(), ok,
-                                             t->in_reports.as<uint32_t>(), s);
+        int rc = insert_impl(t, t->in_b1.as<uint32_t>(), t->in_b2.as<uint32_t>(), t->in_payload.as<uint8_t>(),
+                             ok, t->in_reports.as<uint32_t>(), s);
         if (rc) return rc;
         if (reports)
             XCK(cudaMemcpyAsync(reports, t->in_reports.p, 16 * ok, cudaMemcpyDeviceToHost, s));

@@ -128,16 +128,21 @@ int xpir_window_rotate(xpir_window* win) {  // notify.cpp:67-73
     if (!win) return fail(XPIR_EINVAL, "window_rotate: null window");
     std::lock_guard<std::mutex> lk(win->mu);
     DeviceGuard g(win->device);
+    // push an empty delta, pop from the front while size > W: at capacity the
+    // popped delta's buffer is recycled (zeroed in stream order) instead of a
+    // cudaMalloc + cudaFree per rotation
     unsigned long long* d = nullptr;
-    XCK(cudaMalloc(&d, 8 * win->words));
-    XCK(cudaMemsetAsync(d, 0, 8 * win->words, win->stream));
-    win->deltas.push_back(d);
-    while (win->deltas.size() > win->w) {
-        XCK(cudaStreamSynchronize(win->stream));
-        cudaFree(win->deltas.front());
+    if (!win->deltas.empty() && win->deltas.size() >= win->w) {
+        d = win->deltas.front();
         win->deltas.pop_front();
         win->base++;
+    } else {
+        XCK(cudaMalloc(&d, 8 * win->words));
     }
+    XCK(cudaMemsetAsync(d, 0, 8 * win->words, win->stream));
+    // absorbs may come on the caller's stream: the new delta is zero before any of them
+    XCK(cudaStreamSynchronize(win->stream));
+    win->deltas.push_back(d);
     return XPIR_OK;
 }
 

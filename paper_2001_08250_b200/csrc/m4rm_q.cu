@@ -264,7 +264,11 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
         }
         seq0 += s1 - s0;
 
-        // flush: lane i holds half (i&1) of its 32-byte slice in m[0..3]
+        // flush: lane i holds half (i&1) of its 32-byte slice in m[0..3]. Without
+        // peers (or with one segment per tile) the slice goes straight to its row;
+        // with peers and several segments it goes to the local partial buffer and
+        // the tile's last segment pushes the finished rows to their owners.
+        const bool to_partial = peers.n && n_seg > 1;
 #pragma unroll 1
         for (int s = 0; s < 4 * NQ; ++s) {
             uint32_t m[8];
@@ -273,11 +277,11 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
             const uint32_t rl = 4 * uint32_t((s >> 2) * Q_NT + tid) + uint32_t(s & 3);
             const uint32_t r = r_base + rl;
             if (r < B) {
-                uint8_t* const base = peers.n ? peers.owner_out(r) : out;
+                uint8_t* const base = to_partial ? peers.partial : peers.n ? peers.owner_out(r) : out;
                 uint8_t* o = base + uint64_t(r) * S + uint64_t(c) * 32;
                 uint8_t* oa = o + 16 * (i8 & 1);
                 uint8_t* ob = o + 16 * ((i8 & 1) ^ 1);
-                if (peers.n) {  // the owner's rows take every rank's partials: system-scope RMWs
+                if (peers.n && !to_partial) {  // owners' rows take every rank's partials: system scope
                     red_xor64_sys(oa, uint64_t(m[1]) << 32 | m[0]);
                     red_xor64_sys(oa + 8, uint64_t(m[3]) << 32 | m[2]);
                     red_xor64_sys(ob, uint64_t(m[5]) << 32 | m[4]);
@@ -289,6 +293,43 @@ k_scan_m4rm_q(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                     red_xor64(ob + 8, uint64_t(m[7]) << 32 | m[6]);
                 }
             }
+        }
+        if (to_partial) {
+            // arrival (threadFenceReduction pattern): every thread's REDs are ordered
+            // before thread 0's count; the last arriver sees all segments' REDs
+            volatile uint32_t* last = reinterpret_cast<volatile uint32_t*>(smem + C::OFF_ADDR + 4);
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) *last = atomicAdd(peers.tile_cnt + uint64_t(rt) * n_ctiles + c, 1u) == n_seg - 1;
+            __syncthreads();
+            if (*last) {
+                __threadfence();
+                unsigned long long remote = 0, own = 0;
+                const uint32_t rows = (B - r_base) < uint32_t(C::RC) ? B - r_base : uint32_t(C::RC);
+#pragma unroll 1
+                for (uint32_t rl = tid; rl < rows; rl += Q_NT) {
+                    const uint32_t r = r_base + rl;
+                    uint4* p = reinterpret_cast<uint4*>(peers.partial + uint64_t(r) * S + uint64_t(c) * 32);
+                    const uint4 a = __ldcg(p), b = __ldcg(p + 1);
+                    __stcg(p, make_uint4(0, 0, 0, 0));
+                    __stcg(p + 1, make_uint4(0, 0, 0, 0));
+                    const uint32_t g = peers.owner(r);
+                    uint8_t* o = peers.ptr[g] + uint64_t(r) * S + uint64_t(c) * 32;
+                    red_xor64_sys(o, uint64_t(a.y) << 32 | a.x);
+                    red_xor64_sys(o + 8, uint64_t(a.w) << 32 | a.z);
+                    red_xor64_sys(o + 16, uint64_t(b.y) << 32 | b.x);
+                    red_xor64_sys(o + 24, uint64_t(b.w) << 32 | b.z);
+                    if (g == peers.self) own += 32; else remote += 32;
+                }
+                if (peers.stats) {
+                    remote = __reduce_add_sync(0xffffffffu, uint32_t(remote));
+                    own = __reduce_add_sync(0xffffffffu, uint32_t(own));
+                    if (lane == 0 && remote) atomicAdd(peers.stats, remote);
+                    if (lane == 0 && own) atomicAdd(peers.stats + 1, own);
+                }
+                if (tid == 0) peers.tile_cnt[uint64_t(rt) * n_ctiles + c] = 0;  // ready for the next launch
+            }
+            __syncthreads();  // the flag is rewritten by the next unit
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");

@@ -25,17 +25,28 @@ struct ScanArgs {
 // Fused cross-GPU reduction target: answer row r belongs to the rank g with
 // bound[g] <= r < bound[g+1]; every rank's buffer holds all B rows at the same
 // offsets (only the owner's rows are meaningful). n == 0: no peers.
+// Fused cross-GPU reduce of the quad-table scan (m4rm_q.cu): rank g owns answer
+// rows [bound[g], bound[g+1]) in its buffer ptr[g] (CUDA-IPC peer pointers).
+// Segment partials of one (request tile, column tile) accumulate in this GPU's
+// `partial` buffer; the last segment to arrive (tile_cnt) pushes the tile's rows
+// to their owners once — B*S bytes per rank per batch, (G-1)/G of them remote.
+// partial and tile_cnt are zero between launches (the pusher clears its tile).
 struct PeerOut {
     uint8_t* ptr[8];
     uint32_t bound[9];
     uint32_t n;
-    __device__ __forceinline__ uint8_t* owner_out(uint32_t r) const {
+    uint32_t self;                      // this rank
+    uint8_t* partial;                   // B x S local accumulation buffer
+    uint32_t* tile_cnt;                 // arrivals per (request tile, column tile)
+    unsigned long long* stats;          // [0] remote bytes pushed, [1] own-row bytes (nullable)
+    __device__ __forceinline__ uint32_t owner(uint32_t r) const {
         uint32_t g = 0;
 #pragma unroll
         for (int k = 1; k < 8; ++k)
             if (k < int(n) && r >= bound[k]) g = k;
-        return ptr[g];
+        return g;
     }
+    __device__ __forceinline__ uint8_t* owner_out(uint32_t r) const { return ptr[owner(r)]; }
 };
 
 // M4RM scan (m4rm.cu): queries in the group-major layout qT[g*qstride + r].
@@ -94,6 +105,9 @@ cudaError_t launch_bloom_item(const uint8_t* item_dev, uint32_t len, uint32_t h,
 // out-of-range position (or ~0); positions before it are absorbed (notify.cpp:60-65).
 cudaError_t launch_absorb(const uint32_t* pos, uint64_t n, uint32_t m_bits,
                           unsigned long long* words, unsigned long long* scratch, cudaStream_t s);
+// first index whose beta1 or beta2 >= buckets into *first_bad (~0 when none)
+cudaError_t launch_beta_check(const uint32_t* b1, const uint32_t* b2, uint64_t n, uint32_t buckets,
+                              unsigned long long* first_bad, cudaStream_t s);
 cudaError_t launch_draws(const uint8_t* key_host32, uint64_t nonce0, uint32_t count, uint64_t* out,
                          cudaStream_t s);
 

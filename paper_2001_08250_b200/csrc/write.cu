@@ -126,6 +126,14 @@ __global__ void k_absorb_check(const uint32_t* __restrict__ pos, uint64_t n, uin
     if (t < n && pos[t] >= m_bits) atomicMin(first_bad, (unsigned long long)t);
 }
 
+// cuckoo.cpp:57-58 for device-resident write batches: first item with a bucket
+// index out of range (atomicMin; ~0 when none)
+__global__ void k_beta_check(const uint32_t* __restrict__ b1, const uint32_t* __restrict__ b2, uint64_t n,
+                             uint32_t buckets, unsigned long long* __restrict__ first_bad) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < n && (b1[t] >= buckets || b2[t] >= buckets)) atomicMin(first_bad, (unsigned long long)t);
+}
+
 __global__ void k_absorb(const uint32_t* __restrict__ pos, uint64_t n,
                          const unsigned long long* __restrict__ limit,
                          unsigned long long* __restrict__ words) {
@@ -543,6 +551,14 @@ cudaError_t launch_absorb(const uint32_t* pos, uint64_t n, uint32_t m_bits,
     const uint32_t g = uint32_t((n + 255) / 256);
     k_absorb_check<<<g, 256, 0, s>>>(pos, n, m_bits, first_bad);
     k_absorb<<<g, 256, 0, s>>>(pos, n, first_bad, words);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_beta_check(const uint32_t* b1, const uint32_t* b2, uint64_t n, uint32_t buckets,
+                              unsigned long long* first_bad, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(first_bad, 0xff, 8, s);
+    if (e != cudaSuccess || !n) return e;
+    k_beta_check<<<uint32_t((n + 255) / 256), 256, 0, s>>>(b1, b2, n, buckets, first_bad);
     return cudaGetLastError();
 }
 

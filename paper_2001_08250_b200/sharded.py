@@ -11,11 +11,14 @@ exchange is our own: every rank maps its peers' partial buffers through CUDA IPC
 (reduce-scatter: rank g owns requests [g*B/G, (g+1)*B/G)). The mask pad (K3) is
 applied exactly once, after the reduce, by the owner.
 
-Fused mode (B >= 2048, the half-TMEM M4RM kernel): the reduce disappears into
-the scan. Every owner first initialises its rows (mask pad or zero); then each
-rank's scan kernel XORs every accumulator flush straight into the owner rank's
-buffer over NVLink (64-bit peer atomics), so the partial answers never exist as
-separate buffers and the transfer overlaps the scan tile by tile.
+Fused mode (B >= 2048, the quad-table M4RM kernel 8): the reduce disappears
+into the scan. Every owner first initialises its rows (mask pad or zero); then
+each rank's scan kernel accumulates the segment partials of every (request
+tile, column tile) in a local buffer and the tile's last segment pushes the
+finished rows straight into their owners' buffers over NVLink (64-bit
+system-scope XOR reductions) while other tiles are still scanning. Per rank and
+batch that is B*S bytes, (G-1)/G of them remote — the volume of a
+reduce-scatter, overlapped with the scan (``Store.peer_stats`` counts it).
 
 Control plane (handle exchange, barriers) goes through ``torch.distributed``; the
 data plane is peer memory only.
@@ -75,7 +78,7 @@ class ShardedScan:
         self.r0, self.r1 = self.plan.row_range(self.rank, B)
         self.peers: list[int] = []
         self.src_ptrs = None
-        self.fused = (B >= 2048 and S % 128 == 0) if fused is None else bool(fused)
+        self.fused = (B >= 2048 and S % 32 == 0) if fused is None else bool(fused)
         self._exchange_handles()
 
     def _exchange_handles(self):
@@ -139,6 +142,7 @@ class ShardedScan:
         xp = self.xp
         xp.init_rows_dev(self.partial, self.r0, self.r1, self.S, d_mask, device=self.device, stream=stream)
         self._sync_barrier(stream)
-        self.store.answer_batch_seeded_peer_dev(d_seeds, self.B, self.out_ptrs, self.row_bounds, stream=stream)
+        self.store.answer_batch_seeded_peer_dev(d_seeds, self.B, self.out_ptrs, self.row_bounds, self.rank,
+                                                stream=stream)
         self._sync_barrier(stream)
         return self.partial[self.r0:self.r1]

@@ -43,8 +43,17 @@ def main():
     torch.cuda.synchronize()
     ok = True
     for it in range(3):
+        if sh.fused:
+            sh.store.peer_stats(reset=True)
         own = sh.step(seeds, stream=stream, d_mask=masks if it == 2 else None)
         torch.cuda.synchronize()
+        if sh.fused:
+            # the fused epilogue moves reduce-scatter bytes: each row pushed once, to its owner
+            st = sh.store.peer_stats()
+            want_remote = (B - (sh.r1 - sh.r0)) * S
+            print(f"rank {rank} it {it}: remote {st['remote_bytes']} (reduce-scatter {want_remote}), "
+                  f"own {st['own_bytes']}", flush=True)
+            ok = ok and st["remote_bytes"] <= 1.05 * want_remote and st["own_bytes"] <= (sh.r1 - sh.r0) * S
         rows = own.cpu().numpy().copy()
         got = [None] * world
         dist.all_gather_object(got, (sh.r0, sh.r1, rows.tobytes()))

@@ -115,3 +115,45 @@ def test_close_while_callers_are_active(xp, port, cuda):
         t.join()
     assert not bad and ok[0] > 0
     st.close()
+
+
+def test_geometry_batcher_serves_several_stores(xp, port, cuda):
+    """One batcher for every store of a geometry (the drop-in's per-snapshot-epoch
+    reads): requests name their store, batches form per (store, masked), and each
+    caller gets its own store's answer; a store of another geometry is refused."""
+    N, S, K = 3000, 256, 3
+    g = np.random.default_rng(77)
+    dbs = [g.integers(0, 256, N * S, dtype=np.uint8) for _ in range(K)]
+    sts = []
+    for db in dbs:
+        st = xp.Store(N, S)
+        st.upload(db)
+        sts.append(st)
+    bt = xp.Batcher(None, max_batch=32, max_wait_us=300, geometry=(N, S))
+    T, R = 16, 6
+    nb = (N + 7) // 8
+    qs = g.integers(0, 256, (T, R, nb), dtype=np.uint8)
+    which = g.integers(0, K, (T, R))
+    seeds = g.integers(0, 256, (T, R, 32), dtype=np.uint8)
+    got = np.zeros((T, R, S), np.uint8)
+
+    def worker(t):
+        for r in range(R):
+            got[t, r] = bt.answer(qs[t, r], mask_seed=seeds[t, r].tobytes() if r % 2 else None,
+                                  store=sts[which[t, r]])
+
+    _run_threads(worker, T)
+    for t in range(T):
+        for r in range(R):
+            want = port.answer_batch(dbs[which[t, r]], N, S, qs[t, r][None], 1)[0].tobytes()
+            if r % 2:
+                want = port.mask_answer(want, seeds[t, r].tobytes())
+            assert got[t, r].tobytes() == want, (t, r)
+    other = xp.Store(N, S + 16)
+    with pytest.raises(xp.InvalidArgument):
+        bt.answer(qs[0, 0], store=other)
+    with pytest.raises(xp.InvalidArgument):
+        bt.answer(qs[0, 0])  # no default store
+    bt.close()
+    for st in sts + [other]:
+        st.close()

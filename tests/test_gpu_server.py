@@ -120,3 +120,48 @@ def test_sharded_servers_match_whole_server(xp, port, cuda, G, nb, ring, R):
             parts = np.concatenate([r.snapshot(e).download() for r in ranks])
             assert np.array_equal(parts, full), (rnd, e)
         assert all(r.window_digest() == whole.window_digest() for r in ranks)
+
+
+def test_pinned_snapshot_survives_ring_turnover(xp, port, cuda):
+    """snapshot_acquire pins an epoch's image (the reference keeps a pruned epoch
+    alive through its shared_ptr, server.cpp:83-87): seals that push it off the
+    ring retire it instead of re-sealing it in place; the last release returns it
+    to the spare pool and later seals stay exact."""
+    nb, depth, item, ring = 128, 4, 32, 2
+    g = np.random.default_rng(5)
+    seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+    cap = nb * depth // 2
+    sv = xp.Server(nb, depth, cap, item, seed, 1024, 3, 2, 1000, ring)
+    T = port.table(nb, depth, cap, item, seed)
+
+    def round_(n, seal=True):
+        b1 = g.integers(0, nb, n).astype(np.uint32)
+        b2 = g.integers(0, nb, n).astype(np.uint32)
+        pl = g.integers(0, 256, (n, item), dtype=np.uint8)
+        pos = g.integers(0, 1024, (n, 3)).astype(np.uint32)
+        T.insert_batch(b1, b2, pl)
+        return sv.apply_round(b1, b2, pl, pos, seal_after=seal)[1]
+
+    e2 = round_(40)
+    img2 = T.data().copy()
+    st2, pinned = sv.snapshot_acquire(e2)
+    assert pinned == e2
+    st2b, _ = sv.snapshot_acquire(0)  # latest == e2, a second reader
+    for _ in range(4):  # e2 leaves the ring after the next `ring` seals
+        round_(30)
+    with pytest.raises(xp.InvalidArgument):
+        sv.snapshot(e2)
+    assert np.array_equal(st2.download(), img2)  # retired, untouched
+    sv.snapshot_release(st2)
+    assert np.array_equal(st2b.download(), img2)
+    sv.snapshot_release(st2b)  # last reader: back to the spare pool
+    with pytest.raises(xp.InvalidArgument):
+        sv.snapshot_release(st2b)
+    for _ in range(3):
+        e = round_(25)
+        assert np.array_equal(sv.snapshot(e).download(), T.data())
+    q = np.zeros((1, nb // 8), np.uint8)
+    q[0, 1] = 0x81  # buckets 8 and 15
+    img = T.data().reshape(nb, depth * item)
+    assert np.array_equal(sv.snapshot(0).answer_batch(q)[0], img[8] ^ img[15])
+    sv.close()

@@ -25,8 +25,11 @@ def _port():
 
 @pytest.mark.parametrize("world,N,S,B,fused", [
     (2, 8192, 512, 300, "0"), (3, 4096 + 24, 256, 130, "0"), (2, 1024, 4096, 64, "0"),
-    # fused epilogue: peer atomics straight into the owner's rows (TMEM kernel, B >= 2048)
+    # fused epilogue (quad-table kernel 8, B >= 2048): tile fix-up in a local buffer, each
+    # finished tile pushed once to its owners (several segments per tile), or straight
+    # from the accumulators (one segment per tile); remote bytes checked per rank
     (2, 8192, 512, 2100, "1"), (3, 16384 + 40, 1024, 4096, "1"), (4, 4096, 256, 2048 + 3, "1"),
+    (2, 131072, 128, 2048, "1"), (4, 262144 + 8, 64, 4100, "1"), (8, 524288, 32, 8192, "1"),
 ])
 def test_sharded_ipc_reduce(cuda, world, N, S, B, fused):
     env = dict(os.environ, XP_N=str(N), XP_S=str(S), XP_B=str(B), XP_FUSED=fused)

@@ -122,6 +122,35 @@ def test_cuckoo_reference_unit_cases(xp, cuda):
         T.insert_batch([0], [0], np.zeros(5, np.uint8))  # item size mismatch
 
 
+@pytest.mark.parametrize("bad_at,which", [(0, 1), (37, 2), (199, 1), (150, 2)])
+def test_device_inputs_out_of_range_bucket(xp, port, cuda, bad_at, which):
+    """cuckoo.cpp:57-58 on the device-pointer entry points: the items before the
+    first out-of-range beta are inserted (bit-exact vs the oracle's loop), then
+    EINVAL; nothing indexes the table with the bad value."""
+    torch = cuda
+    nb, depth, item, n = 64, 4, 16, 200
+    g = port.detrng(31)
+    seed = g.fill(32)
+    b1 = np.array([g.uniform(nb) for _ in range(n)], np.uint32)
+    b2 = np.array([g.uniform(nb) for _ in range(n)], np.uint32)
+    (b1 if which == 1 else b2)[bad_at] = nb + 5 + bad_at * 1000
+    pl = np.frombuffer(g.fill(n * item), np.uint8).reshape(n, item)
+    T, P = xp.Table(nb, depth, 200, item, seed), port.table(nb, depth, 200, item, seed)
+    P.insert_batch(b1[:bad_at], b2[:bad_at], pl[:bad_at])
+    d1, d2 = torch.from_numpy(b1.view(np.int32)).cuda(), torch.from_numpy(b2.view(np.int32)).cuda()
+    dp, rep = torch.from_numpy(pl.copy()).cuda(), torch.zeros((n, 4), dtype=torch.int32, device="cuda")
+    with pytest.raises(xp.InvalidArgument):
+        T.insert_batch_dev(d1, d2, dp, n, rep)
+    torch.cuda.synchronize()
+    assert T.writes_applied() == bad_at
+    assert T.state_digest() == P.state_digest()
+    # the walk-only entry point (payload shards) behaves the same
+    T2 = xp.Table(nb, depth, 200, item, seed)
+    with pytest.raises(xp.InvalidArgument):
+        T2.insert_walk_dev(d1, d2, n, rep)
+    assert T2.writes_applied() == bad_at
+
+
 def test_window_rotate_and_range(xp, port, cuda):
     for w in (1, 2, 3):
         A, B = xp.Window(1000, 3, w), port.window(1000, 3, w)
