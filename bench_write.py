@@ -57,35 +57,83 @@ def main():
         payload = torch.from_numpy(d["payload"]).to(dev)
         k1 = np.frombuffer(d["k1"], np.uint64)
         k2 = np.frombuffer(d["k2"], np.uint64)
-        gpu_ms = []
+        gpu_ms, dev_ms = [], []
         digest_ok = None
         db1 = torch.empty(n, dtype=torch.int32, device=dev)
         db2 = torch.empty(n, dtype=torch.int32, device=dev)
-        stream = torch.cuda.Stream()
-        stream2 = torch.cuda.Stream()  # the interest update is independent of the table
+        stream = torch.cuda.Stream(priority=-1)  # the table chain is the critical path
+        stream2 = torch.cuda.Stream(priority=0)  # the interest update (independent of the table) fills the gaps
         for rep in range(args.reps + 1):
             T = xp.Table(N, depth, N * depth, item, d["s_cuckoo"])
             T.reserve(n)  # server start-up: per-round scratch sized once, outside the round
             W = xp.Window(m, h, 1)
             torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            stream2.wait_stream(stream)
             t0 = time.perf_counter()
             # K5 betas, K6 placement (+ walk) and payload scatter on one stream; K7
             # interest (make_interest + absorb) concurrently on a second stream: the
             # window and the table are disjoint state, so the result is the same as
             # the reference's insert-then-absorb per write (server.cpp:63-64)
             W.absorb_interest_dev(d["lid"], xs, n, stream=stream2)
-            xp.prf_batch_dev(d["k1"], xs, n, N, d_out32=db1, stream=stream)
-            xp.prf_batch_dev(d["k2"], xs, n, N, d_out32=db2, stream=stream)
+            xp.write_betas_dev(d["k1"], d["k2"], xs, n, N, db1, db2, stream=stream)
             T.insert_batch_dev(db1, db2, payload, n, stream=stream)
+            stream.wait_stream(stream2)
+            ev1.record(stream)
             stream.synchronize()
             stream2.synchronize()
             t = (time.perf_counter() - t0) * 1e3
             if rep:
                 gpu_ms.append(t)
+                dev_ms.append(ev0.elapsed_time(ev1))
             if rep == 1:
                 G = golden["config3"][str(n)]
                 digest_ok = (T.state_digest().hex() == G["state_digest"]
                              and W.digest().hex() == G["window_digest"])
+            T.close()
+            W.close()
+        # the same round as ONE CUDA graph (captured at start-up for the table's fixed
+        # buffers, replayed per round): interest branch + PRF + insert_batch_async, then
+        # xpir_table_finish reconciles on the host
+        graph_dev_ms, graph_wall_ms, graph_ok = [], [], None
+        for rep in range(args.reps + 1):
+            T = xp.Table(N, depth, N * depth, item, d["s_cuckoo"])
+            T.reserve(n)
+            W = xp.Window(m, h, 1)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            pdone = torch.cuda.Event()
+            pdone.record(stream)  # creates the event handle the library records inside the capture
+            torch.cuda.synchronize()
+            after_prefix = os.environ.get("XPIR_BENCH_INTEREST_AFTER_PREFIX") == "1"  # A/B
+            with torch.cuda.graph(g, stream=stream):
+                if not after_prefix:
+                    stream2.wait_stream(stream)
+                    W.absorb_interest_dev(d["lid"], xs, n, stream=stream2)
+                xp.write_betas_dev(d["k1"], d["k2"], xs, n, N, db1, db2, stream=stream)
+                T.insert_batch_async(db1, db2, payload, n, stream, prefix_done=pdone)
+                if after_prefix:
+                    stream2.wait_event(pdone)
+                    W.absorb_interest_dev(d["lid"], xs, n, stream=stream2)
+                stream.wait_stream(stream2)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            with torch.cuda.stream(stream):  # the replay runs on the stream finish() waits on
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+            applied = T.finish()
+            t = (time.perf_counter() - t0) * 1e3
+            assert applied == n
+            if rep:
+                graph_wall_ms.append(t)
+                graph_dev_ms.append(e0.elapsed_time(e1))
+            if rep == 1:
+                G = golden["config3"][str(n)]
+                graph_ok = (T.state_digest().hex() == G["state_digest"] and W.digest().hex() == G["window_digest"])
+            del g
             T.close()
             W.close()
         # end to end: keys and payloads from pinned host memory, InsertReports back
@@ -133,10 +181,16 @@ def main():
             ref_ms = (time.perf_counter() - t0) * 1e3
         line = {"metric": "write round (cuckoo insert + interest Bloom update)", "writes": n,
                 "load": n / (N * depth), "gpu_ms": float(np.median(gpu_ms)), "gpu_writes_per_s": n / (np.median(gpu_ms) * 1e-3),
+                "device_span_ms": float(np.median(dev_ms)),
+                "graph_device_ms": float(np.median(graph_dev_ms)), "graph_wall_ms": float(np.median(graph_wall_ms)),
+                "graph_bit_exact_vs_golden": graph_ok,
                 "e2e_ms": float(np.median(e2e_ms)), "e2e_h2d_bytes": int(hx.numel() * 8 + hp.numel()),
                 "e2e_d2h_bytes": int(hrep.numel() * 4),
                 "ref_ms_1thread": ref_ms, "ref_kind": o.kind, "bit_exact_vs_golden": digest_ok,
-                "timing": "wall clock around PRF + insert walk + payload scatter + interest absorb, "
+                "timing": "gpu_ms: wall clock around PRF + insert walk + payload scatter + interest absorb "
+                          "(device_span_ms: CUDA events from the round's first launch to its last, both streams; "
+                          "graph_*: the round captured once as a CUDA graph and replayed — device span of the "
+                          "replay, and wall clock of replay + xpir_table_finish), "
                           "inputs (keys, payloads) resident in HBM; excludes table/window allocation; "
                           "e2e_ms: the same round with keys + payloads copied from pinned host memory "
                           "and the InsertReports copied back inside the timed region"}

@@ -238,6 +238,10 @@ int xpir_prf_batch(const uint8_t key[16], const uint64_t* inputs, uint64_t n, ui
 /* Same on device buffers; d_out32 (optional) receives the values as uint32 (bucket indices). */
 int xpir_prf_batch_dev(int device, const uint8_t key[16], const uint64_t* d_inputs, uint64_t n,
                        uint64_t modulus, uint64_t* d_out, uint32_t* d_out32, void* stream);
+/* The two bucket choices of a write batch in one kernel: beta1 = prf(k1, key, buckets),
+ * beta2 = prf(k2, key, buckets) (logproto.cpp:74-75 over crypto::prf). */
+int xpir_write_betas_dev(int device, const uint8_t k1[16], const uint8_t k2[16], const uint64_t* d_keys, uint64_t n,
+                         uint32_t buckets, uint32_t* d_beta1, uint32_t* d_beta2, void* stream);
 /* notify::make_interest (notify.cpp:30-35): out[i*h + k] */
 int xpir_make_interest_batch(uint32_t m_bits, uint32_t h, const uint8_t id[16],
                              const uint64_t* seqs, uint64_t n, uint32_t* out);
@@ -266,6 +270,24 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* beta1, const uint32_t
 int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_beta1, const uint32_t* d_beta2,
                                 const uint8_t* d_payload, uint64_t n, uint32_t* d_reports,
                                 void* stream);
+/* The same batch as a pure stream sequence (no host round trip, no allocation:
+ * prefix_done, a cudaEvent_t or NULL, is recorded after the parallel-prefix
+ * kernel — a grid-synchronised cooperative launch, so independent bulk work
+ * such as the round's interest update is best started after it;
+ * capturable in a CUDA graph, e.g. a server's whole write round): the parallel
+ * eviction-free prefix, the eviction walk from where it stops, and the payload
+ * moves, all reading and advancing the device copy of the table state. Requires
+ * xpir_table_reserve(t, >= n) at start-up. xpir_table_finish (after the stream
+ * work, outside any capture) reconciles the host mirror, completes what could
+ * not run on device (a walk that ran out of staged draws, a batch that moved more
+ * slots than the staging holds), and returns XPIR_EINVAL for a bucket index out
+ * of range (*n_applied = the inserts before it, as insert_batch_dev). It waits
+ * for `stream`: a graph holding the batch must be replayed on that stream (or
+ * the caller synchronises before finish). */
+int xpir_table_insert_batch_async(xpir_table* t, const uint32_t* d_beta1, const uint32_t* d_beta2,
+                                  const uint8_t* d_payload, uint64_t n, uint32_t* d_reports, void* stream,
+                                  void* prefix_done);
+int xpir_table_finish(xpir_table* t, uint64_t* n_applied);
 /* Bucket-range payload shards (the payload scatter goes to the GPU
  * owning each bucket range). A shard table keeps the whole metadata (the walk
  * is replicated: every shard runs the same insert_walk) and the payloads of

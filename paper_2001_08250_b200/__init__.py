@@ -98,6 +98,9 @@ _SIGS = {
     "xpir_answer_batch_seeded_peer_dev": ([_vp, _vp, C.c_uint32, C.POINTER(_vp), _u32p, C.c_uint32, C.c_uint32,
                                            _vp], C.c_int),
     "xpir_store_peer_stats": ([_vp, _u64p, _u64p, C.c_int], C.c_int),
+    "xpir_table_insert_batch_async": ([_vp, _vp, _vp, _vp, C.c_uint64, _vp, _vp, _vp], C.c_int),
+    "xpir_table_finish": ([_vp, _u64p], C.c_int),
+    "xpir_write_betas_dev": ([C.c_int, _u8p, _u8p, _vp, C.c_uint64, C.c_uint32, _vp, _vp, _vp], C.c_int),
     "xpir_init_rows_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp], C.c_int),
     "xpir_expand_queries_dev": ([C.c_int, _vp, C.c_uint32, C.c_uint64, C.c_uint64, _vp, C.c_uint64, _vp], C.c_int),
     "xpir_mask_answer": ([_u8p, C.c_uint64, _u8p, _u8p], C.c_int),
@@ -591,6 +594,13 @@ def prf_batch_dev(key16: bytes, d_inputs, n: int, modulus: int, d_out=None, d_ou
                                     _ptr(d_out32), _stream(stream)))
 
 
+def write_betas_dev(k1: bytes, k2: bytes, d_keys, n: int, buckets: int, d_beta1, d_beta2, device: int = 0,
+                    stream=None) -> None:
+    """beta1/beta2 of a write batch (logproto.cpp:74-75), one kernel."""
+    _check(lib().xpir_write_betas_dev(device, _p(_u8(k1)), _p(_u8(k2)), _ptr(d_keys), n, buckets, _ptr(d_beta1),
+                                      _ptr(d_beta2), _stream(stream)))
+
+
 def make_interest_batch(m_bits: int, h: int, id16: bytes, seqs) -> np.ndarray:
     s = np.ascontiguousarray(seqs, np.uint64)
     out = np.empty((max(len(s), 1), max(h, 1)), np.uint32)
@@ -670,6 +680,19 @@ class Table:
     def insert_batch_dev(self, d_b1, d_b2, d_payload, n: int, d_reports=None, stream=None) -> None:
         _check(lib().xpir_table_insert_batch_dev(self.h, _ptr(d_b1), _ptr(d_b2), _ptr(d_payload), n,
                                                  _ptr(d_reports), _stream(stream)))
+
+    def insert_batch_async(self, d_b1, d_b2, d_payload, n: int, stream, d_reports=None, prefix_done=None) -> None:
+        """The batch as stream work only (CUDA-graph capturable); then finish().
+        prefix_done: a torch.cuda.Event recorded after the parallel-prefix kernel."""
+        ev = None if prefix_done is None else prefix_done.cuda_event
+        _check(lib().xpir_table_insert_batch_async(self.h, _ptr(d_b1), _ptr(d_b2), _ptr(d_payload), n,
+                                                   _ptr(d_reports), _stream(stream), ev))
+
+    def finish(self) -> int:
+        """Completes an insert_batch_async batch; returns the inserts applied."""
+        k = C.c_uint64()
+        _check(lib().xpir_table_finish(self.h, C.byref(k)))
+        return k.value
 
     # the three steps of a round on payload shards (see include/xpir.h)
     def insert_walk_dev(self, d_b1, d_b2, n: int, d_reports=None, stream=None) -> None:

@@ -163,6 +163,9 @@ ServerCore::ServerCore(const Config& cfg, uint32_t index)
     check(xpir_server_create(0, cs->buckets, cfg_.depth_d, cfg_.capacity_n, cs->item, cfg_.s_cuckoo.data(),
                              bp.m_bits, bp.h, cfg_.window_deltas, cfg_.rotate_writes(), cfg_.epoch_ring, &cs->sv),
           "server: create");
+    // start-up reservation: every ring image and the per-write scratch allocated now,
+    // so no apply_write / seal_epoch allocates device memory
+    check(xpir_server_reserve(cs->sv, 64), "server: reserve");
     check(xpir_server_info(cs->sv, nullptr, &latest_epoch_, nullptr, &cs->table, &cs->window), "server: info");
     auto anchor = std::make_shared<Anchor>();
     anchor->cs = cs;

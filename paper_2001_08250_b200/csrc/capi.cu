@@ -705,7 +705,10 @@ int xpir_store_peer_stats(xpir_store* st, uint64_t* remote_bytes, uint64_t* own_
         DeviceGuard g(st->device);
         XCK(cudaDeviceSynchronize());
         XCK(cudaMemcpy(v, st->peer_stats.p, 16, cudaMemcpyDeviceToHost));
-        if (reset) XCK(cudaMemset(st->peer_stats.p, 0, 16));
+        if (reset) {
+            XCK(cudaMemset(st->peer_stats.p, 0, 16));
+            XCK(cudaDeviceSynchronize());
+        }
     }
     if (remote_bytes) *remote_bytes = v[0];
     if (own_bytes) *own_bytes = v[1];
@@ -827,6 +830,17 @@ int xpir_prf_batch_dev(int device, const uint8_t key[16], const uint64_t* d_in, 
     DeviceGuard g(device);
     XCK(launch_prf(ld64le(key), ld64le(key + 8), d_in, n, modulus, d_out, d_out32,
                    static_cast<cudaStream_t>(stream)));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+int xpir_write_betas_dev(int device, const uint8_t k1[16], const uint8_t k2[16], const uint64_t* d_keys, uint64_t n,
+                         uint32_t buckets, uint32_t* d_beta1, uint32_t* d_beta2, void* stream) {
+    if (buckets == 0) return fail(XPIR_EINVAL, "prf: modulus must be positive");
+    if (!k1 || !k2 || (n && (!d_keys || !d_beta1 || !d_beta2))) return fail(XPIR_EINVAL, "write_betas: null buffer");
+    DeviceGuard g(device);
+    const uint64_t a[2] = {ld64le(k1), ld64le(k1 + 8)}, c[2] = {ld64le(k2), ld64le(k2 + 8)};
+    XCK(launch_prf2(a, c, d_keys, n, buckets, d_beta1, d_beta2, static_cast<cudaStream_t>(stream)));
     count_launches(1);
     return XPIR_OK;
 }

@@ -94,6 +94,41 @@ struct DevBuf {
 
 inline uint64_t round16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
 
+// Grow-only pinned host staging buffer. A caller packs host inputs into it and
+// issues ONE async H2D copy; `ready` (recorded after the copies that read it)
+// guards the next reuse, so no stream synchronisation is needed in between.
+struct PinnedBuf {
+    uint8_t* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ready = nullptr;
+    cudaError_t ensure(size_t n) {  // waits for the previous user of the buffer
+        if (ready) {
+            cudaError_t e = cudaEventSynchronize(ready);
+            if (e != cudaSuccess) return e;
+        } else {
+            cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
+        if (n <= cap) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        const size_t want = std::max({n, size_t(4096), cap + cap / 2});
+        cap = 0;
+        cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), want, cudaHostAllocPortable);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    cudaError_t release_after(cudaStream_t s) { return ready ? cudaEventRecord(ready, s) : cudaSuccess; }
+    void release() {
+        if (ready) cudaEventSynchronize(ready);
+        if (p) cudaFreeHost(p);
+        if (ready) cudaEventDestroy(ready);
+        p = nullptr;
+        cap = 0;
+        ready = nullptr;
+    }
+};
+
 // Host BLAKE2b (same algorithm as the device port in prims.cuh), incremental,
 // used for the digests that the reference computes over whole tables/windows.
 struct HostBlake2b {
@@ -181,7 +216,20 @@ struct xpir_table {
     uint8_t* data = nullptr;  // payloads of buckets [lo, hi)
     uint32_t lo = 0, hi = 0;  // a payload shard of the logical table (metadata is whole)
     cudaStream_t stream = nullptr;
-    DevBuf in_b1, in_b2, in_payload, in_reports, gather, chk;
+    DevBuf in_b1, in_b2, in_payload, in_reports, gather, chk, in_pack;
+    PinnedBuf stage;              // host inputs of xpir_table_insert_batch, packed for one H2D
+    PinnedBuf state_h;            // pinned mirror of the walk state (async H2D / D2H)
+    bool walked = false;          // a walk kernel ran this batch (pre-existing items may have moved)
+    bool async_pending = false;   // xpir_table_insert_batch_async issued, xpir_table_finish not yet called
+    struct {
+        const uint32_t *b1, *b2;
+        const uint8_t* payload;
+        uint32_t* reports;
+        uint64_t n;
+        cudaStream_t s;
+    } async{};
+    bool state_on_device = false; // the walk of the current call ran without a host round trip:
+    uint32_t max_touched = 0;     //   h is stale, n_touched <= max_touched until synced
     CuckooParScratch par;
     bool parallel_prefix = true;  // XPIR_CUCKOO_SEQUENTIAL=1 disables (A/B checks)
     std::mutex mu;
@@ -203,8 +251,13 @@ struct xpir_window {
     std::deque<unsigned long long*> deltas;
     cudaStream_t stream = nullptr;
     DevBuf pos, seqs, scratch, enc;
+    PinnedBuf stage;  // host positions of xpir_window_absorb_prechecked
     std::mutex mu;
 };
+
+// Window::absorb of positions already checked against m_bits on the host: one
+// packed H2D + the OR kernel on the window's stream, no host round trip.
+int window_absorb_prechecked(xpir_window* win, const uint32_t* pos, uint64_t n);
 
 struct xpir_server {
     int device;

@@ -140,18 +140,31 @@ int xpir_server_apply_round_sharded(xpir_server* sv, const uint32_t* beta1, cons
     if (n && (!beta1 || !beta2 || !payload || (h_per_write && !interest)))
         return fail(XPIR_EINVAL, "server_apply: null buffer");
     std::lock_guard<std::mutex> lk(sv->mu);
-    // apply_write (server.cpp:58-73) for writes in order: beta range check
-    // (server.cpp:60-61) happens before any state changes of that write.
-    uint64_t ok = n;
-    for (uint64_t k = 0; k < n; ++k)
-        if (beta1[k] >= sv->table->d.buckets || beta2[k] >= sv->table->d.buckets) {
-            ok = k;
-            break;
-        }
-    if (ok) {
+    // apply_write (server.cpp:58-73) for writes in order. Both precondition checks
+    // are resolved on the host first, so the device work is exactly the reference's:
+    //  * write kb with a bucket out of range throws before any state change
+    //    (server.cpp:60-61): writes [0, kb) are applied;
+    //  * write kp with an interest position >= m is inserted, its positions before
+    //    the bad one are absorbed, then absorb throws (notify.cpp:62) and the write
+    //    is not counted.
+    const uint32_t m_bits = sv->window->m;
+    uint64_t kb = n, kp = n, jp = 0;
+    for (uint64_t k = 0; k < n && kb == n; ++k)
+        if (beta1[k] >= sv->table->d.buckets || beta2[k] >= sv->table->d.buckets) kb = k;
+    for (uint64_t k = 0; k < kb && kp == n; ++k)
+        for (uint32_t j = 0; j < h_per_write; ++j)
+            if (interest[k * h_per_write + j] >= m_bits) {
+                kp = k;
+                jp = j;
+                break;
+            }
+    const uint64_t n_ins = kp < kb ? kp + 1 : kb;  // writes that reach Table::insert
+    const uint64_t ok = kp < kb ? kp : kb;         // writes that complete
+    if (n_ins) {
         int rc = sv->table->sharded()
-                     ? table_insert_sharded(sv->table, beta1, beta2, payload, ok, reports, map, barrier, barrier_ctx)
-                     : xpir_table_insert_batch(sv->table, beta1, beta2, payload, ok, reports);
+                     ? table_insert_sharded(sv->table, beta1, beta2, payload, n_ins, reports, map, barrier,
+                                            barrier_ctx)
+                     : xpir_table_insert_batch(sv->table, beta1, beta2, payload, n_ins, reports);
         if (rc) return rc;
         // interest positions per rotation segment, then rotate (server.cpp:64-70)
         uint64_t a = 0;
@@ -159,7 +172,7 @@ int xpir_server_apply_round_sharded(xpir_server* sv, const uint32_t* beta1, cons
             const uint64_t to_rot = sv->rotate_writes - (sv->writes % sv->rotate_writes);
             const uint64_t b = std::min(ok, a + to_rot);
             if (h_per_write) {
-                rc = xpir_window_absorb(sv->window, interest + a * h_per_write, (b - a) * h_per_write);
+                rc = window_absorb_prechecked(sv->window, interest + a * h_per_write, (b - a) * h_per_write);
                 if (rc) return rc;
             }
             sv->writes += b - a;
@@ -169,8 +182,13 @@ int xpir_server_apply_round_sharded(xpir_server* sv, const uint32_t* beta1, cons
             }
             a = b;
         }
+        if (kp < kb) {
+            rc = window_absorb_prechecked(sv->window, interest + kp * h_per_write, jp);
+            if (rc) return rc;
+            return fail(XPIR_EINVAL, "Window: position out of range");
+        }
     }
-    if (ok < n) return fail(XPIR_EINVAL, "write targets a bucket outside the table");
+    if (kb < n) return fail(XPIR_EINVAL, "write targets a bucket outside the table");
     if (seal_after) return server_seal(sv, sealed_epoch);
     return XPIR_OK;
 }

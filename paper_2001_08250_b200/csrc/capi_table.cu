@@ -27,6 +27,9 @@ static void table_free_all(xpir_table* t) {
     t->in_reports.release();
     t->gather.release();
     t->chk.release();
+    t->in_pack.release();
+    t->stage.release();
+    t->state_h.release();
     t->par.release();
     if (t->stream) cudaStreamDestroy(t->stream);
 }
@@ -86,6 +89,9 @@ int xpir_table_create_shard(int device, uint32_t buckets, uint32_t depth, uint64
     M(reinterpret_cast<void**>(&t->data), uint64_t(hi - lo) * depth * item_size);
     if (e == cudaSuccess) e = cudaMemset(t->d.fifo, 0xff, 8 * fc);  // -1: no entry
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
+    // the memsets above ran on the legacy stream, which the table's non-blocking
+    // stream does not wait for
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         table_free_all(t);
         delete t;
@@ -93,6 +99,13 @@ int xpir_table_create_shard(int device, uint32_t buckets, uint32_t depth, uint64
                     std::string("table_create: ") + cudaGetErrorString(e));
     }
     t->h = CuckooState{};
+    t->h.limit = ~0ull;
+    // pinned state mirror allocated now: cudaHostAlloc inside a write can take milliseconds
+    if (t->state_h.ensure(sizeof(CuckooState)) != cudaSuccess) {
+        table_free_all(t);
+        delete t;
+        return fail(XPIR_ENOMEM, "table_create: pinned state mirror");
+    }
     if (const char* ev = std::getenv("XPIR_CUCKOO_SEQUENTIAL")) t->parallel_prefix = ev[0] != '1';
     *out = t;
     return XPIR_OK;
@@ -109,35 +122,40 @@ int xpir_table_destroy(xpir_table* t) {
 
 }  // extern "C"
 
-// The walk itself (inputs already range-checked; capi_internal.cuh).
-int table_walk_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n, uint32_t* d_reports,
-                     void* stream) {
-    DeviceGuard g(t->device);
-    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
-    t->h.batch_id += 1;
-    t->h.n_touched = 0;
-    uint64_t i = 0;
-    // K6a: the eviction-free, GC-free prefix of the round is placed in parallel
-    // (exactly what the sequential walk would do); the walk continues from the
-    // first insert that needs an eviction or a FIFO GC.
-    if (t->parallel_prefix && n >= 64 && t->h.live < t->d.capacity) {
-        const uint64_t room = t->d.capacity - t->h.live;
-        uint64_t applied = 0;
-        XCK(cuckoo_parallel_prefix(t->d, t->h, d_b1, d_b2, n < room ? n : room, d_reports, t->par, &applied, s));
-        i = applied;
+// Host round trip of the walk state after an asynchronous walk (one sync).
+static int sync_state(xpir_table* t, cudaStream_t s) {
+    if (!t->state_on_device) return XPIR_OK;
+    XCK(t->state_h.ensure(sizeof(CuckooState)));
+    XCK(cudaMemcpyAsync(t->state_h.p, t->dstate, sizeof(CuckooState), cudaMemcpyDeviceToHost, s));
+    XCK(cudaStreamSynchronize(s));
+    std::memcpy(&t->h, t->state_h.p, sizeof(CuckooState));
+    t->state_on_device = false;
+    if (t->h.status == 2) return fail(XPIR_ESTATE, "table_insert: FIFO ring overflow");
+    return XPIR_OK;
+}
+
+static int refill_draws(xpir_table* t, uint64_t need, cudaStream_t s) {
+    if (t->h.rng_block + need > t->h.draw_base + t->h.draw_count) {
+        // (re)fill the draw window starting at the next unconsumed nonce (draws are a
+        // pure function of the nonce, so a window stays valid across rounds)
+        t->h.draw_base = t->h.rng_block;
+        t->h.draw_count = DRAW_CAP;
+        XCK(launch_draws(t->seed, t->h.draw_base, DRAW_CAP, t->d.draws, s));
+        count_launches(1);
     }
+    return XPIR_OK;
+}
+
+// The host-driven walk loop from insert i: one launch per draw window.
+static int walk_loop(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t i, uint64_t n,
+                     uint32_t* d_reports, cudaStream_t s) {
     while (i < n) {
-        if (t->h.rng_block + 1024 > t->h.draw_base + t->h.draw_count) {
-            // (re)fill the draw window starting at the next unconsumed nonce (draws are a
-            // pure function of the nonce, so a window stays valid across rounds)
-            t->h.draw_base = t->h.rng_block;
-            t->h.draw_count = DRAW_CAP;
-            XCK(launch_draws(t->seed, t->h.draw_base, DRAW_CAP, t->d.draws, s));
-            count_launches(1);
-        }
+        int rc = refill_draws(t, 1024, s);
+        if (rc) return rc;
         XCK(cudaMemcpyAsync(t->dstate, &t->h, sizeof(CuckooState), cudaMemcpyHostToDevice, s));
         XCK(launch_cuckoo_walk(t->d, t->dstate, d_b1, d_b2, i, n, d_reports, s));
         count_launches(1);
+        t->walked = true;
         XCK(cudaMemcpyAsync(&t->h, t->dstate, sizeof(CuckooState), cudaMemcpyDeviceToHost, s));
         XCK(cudaStreamSynchronize(s));
         if (t->h.status == 2) return fail(XPIR_ESTATE, "table_insert: FIFO ring overflow");
@@ -146,19 +164,7 @@ int table_walk_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, u
         i = t->h.resume_at;
         if (t->h.status == 1) t->h.draw_count = 0;  // force a refill
     }
-    if (!stream) XCK(cudaStreamSynchronize(s));
     return XPIR_OK;
-}
-
-
-// Walk + payload gather/scatter of a whole (unsharded) table.
-static int insert_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, const uint8_t* d_payload,
-                       uint64_t n, uint32_t* d_reports, void* stream) {
-    int rc = table_walk_impl(t, d_b1, d_b2, n, d_reports, stream);
-    if (rc) return rc;
-    rc = xpir_table_apply_gather_dev(t, nullptr, stream);
-    if (rc) return rc;
-    return xpir_table_apply_scatter_dev(t, d_payload, stream);
 }
 
 // cuckoo.cpp:57-58 for device-resident inputs: the index of the first item whose
@@ -177,6 +183,171 @@ static int beta_check(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2,
     return XPIR_OK;
 }
 
+// Push the host mirror of the walk state to the device (pinned staging, async).
+static int push_state(xpir_table* t, cudaStream_t s) {
+    XCK(t->state_h.ensure(sizeof(CuckooState)));
+    std::memcpy(t->state_h.p, &t->h, sizeof(CuckooState));
+    XCK(cudaMemcpyAsync(t->dstate, t->state_h.p, sizeof(CuckooState), cudaMemcpyHostToDevice, s));
+    XCK(t->state_h.release_after(s));
+    return XPIR_OK;
+}
+
+// The rest of a batch started on device (parallel prefix + walk from its resume
+// point, or the small asynchronous walk): one host round trip for the state;
+// *n_ok = the first insert with a bucket out of range (n when none); a walk that
+// paused for draws is finished on the host-driven path.
+static int finish_walk(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n, uint32_t* d_reports,
+                       cudaStream_t s, uint64_t* n_ok) {
+    int rc = sync_state(t, s);
+    if (rc) return rc;
+    *n_ok = t->h.limit < n ? t->h.limit : n;
+    t->h.limit = ~0ull;
+    if (t->h.status == 1) {
+        t->h.status = 0;
+        t->h.draw_count = 0;  // refill, then resume
+        return walk_loop(t, d_b1, d_b2, t->h.resume_at, *n_ok, d_reports, s);
+    }
+    return push_state(t, s);  // the device copy stays authoritative
+}
+
+// The walk of a batch. checked: beta1/beta2 already validated (host inputs);
+// otherwise the range check runs on device — inside the parallel-prefix kernel
+// when that runs, else as its own kernel — and *n_ok is the first bad insert
+// (n when none): only inserts before it are walked.
+//  * n >= 64: the parallel prefix and the walk from its resume point are launched
+//    back to back from and into the device state (no host round trip between);
+//  * a batch small against the table (one apply_write) is walked with its draws
+//    pre-staged and the state pushed asynchronously;
+// with allow_async both leave t->state_on_device (the caller finishes the batch
+// and calls finish_walk), else the batch is finished here.
+static int walk_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n, uint32_t* d_reports,
+                     cudaStream_t s, bool allow_async, bool checked, uint64_t* n_ok) {
+    int rc = sync_state(t, s);
+    if (rc) return rc;
+    *n_ok = n;
+    t->h.n_touched = 0;
+    t->h.walked = 0;
+    t->h.limit = ~0ull;
+    t->walked = false;
+    const uint64_t slots = t->slots();
+    if (t->parallel_prefix && n >= 64) {
+        // K6a: the eviction-free, GC-free prefix of the round is placed in parallel
+        // (exactly what the sequential walk would do); the walk continues on device
+        // from the first insert that needs an eviction or a FIFO GC
+        if ((rc = refill_draws(t, 1024, s)) || (rc = push_state(t, s))) return rc;
+        XCK(cuckoo_parallel_prefix(t->d, t->dstate, d_b1, d_b2, n, d_reports, t->par, s));
+        XCK(launch_cuckoo_walk(t->d, t->dstate, d_b1, d_b2, WALK_FROM_STATE, n, d_reports, s));
+        count_launches(1);
+        t->walked = true;  // the device flag says whether the walk had work
+        t->state_on_device = true;
+        t->max_touched = uint32_t(slots);
+        if (!allow_async) return finish_walk(t, d_b1, d_b2, n, d_reports, s, n_ok);
+        return XPIR_OK;
+    }
+    t->h.batch_id += 1;
+    if (!checked) {
+        if ((rc = beta_check(t, d_b1, d_b2, n, s, n_ok))) return rc;
+        n = *n_ok;
+    }
+    if (allow_async && n * 256 < slots && n <= 64) {
+        // worst case per insert: uniform(2) + 500 hops (cuckoo.cpp:86-120), with slack
+        if ((rc = refill_draws(t, n * 1024 + 1024, s)) || (rc = push_state(t, s))) return rc;
+        XCK(launch_cuckoo_walk(t->d, t->dstate, d_b1, d_b2, 0, n, d_reports, s));
+        count_launches(1);
+        t->walked = true;
+        t->state_on_device = true;
+        // a GC plus a chain of at most 500 moves per insert
+        const uint64_t bound = n * 502;
+        t->max_touched = uint32_t(bound < slots ? bound : slots);
+        return XPIR_OK;
+    }
+    return walk_loop(t, d_b1, d_b2, 0, n, d_reports, s);
+}
+
+int table_walk_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, uint64_t n, uint32_t* d_reports,
+                    void* stream) {
+    DeviceGuard g(t->device);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
+    uint64_t ok = n;
+    int rc = walk_impl(t, d_b1, d_b2, n, d_reports, s, false, true, &ok);
+    if (rc) return rc;
+    if (!stream) XCK(cudaStreamSynchronize(s));
+    return XPIR_OK;
+}
+
+// Payload moves of the batch. With the state on device the touched count is read
+// there (no host round trip); the staging buffer is NOT grown then — a batch that
+// touched more slots than it holds makes the gather flag status 3 and both kernels
+// skip, and the caller redoes them with the host count.
+static int gather_impl(xpir_table* t, const ShardMap& m, cudaStream_t s) {
+    // only eviction chains and FIFO GC (the walk kernels) move pre-existing items;
+    // a round placed entirely by the parallel prefix has nothing to stage
+    if (!t->walked || (!t->state_on_device && !t->h.walked)) return XPIR_OK;
+    uint32_t cap;
+    if (t->state_on_device) {
+        if (t->max_touched < uint32_t(1) << 16) XCK(t->gather.ensure(uint64_t(t->max_touched) * t->d.item));
+        cap = uint32_t(t->gather.cap / t->d.item);
+    } else {
+        XCK(t->gather.ensure(uint64_t(t->h.n_touched) * t->d.item));
+        cap = t->h.n_touched;
+    }
+    t->d.gather = t->gather.as<uint8_t>();
+    XCK(launch_cuckoo_gather_sharded(t->d, &t->h, t->lo, t->hi, t->data, m, s,
+                                     t->state_on_device ? t->dstate : nullptr, t->max_touched, cap));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+static int scatter_impl(xpir_table* t, const uint8_t* d_payload, cudaStream_t s) {
+    XCK(launch_cuckoo_scatter_sharded(t->d, &t->h, t->lo, t->hi, t->data, d_payload, s,
+                                      t->state_on_device ? t->dstate : nullptr, t->max_touched));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+// Walk + payload gather/scatter of a whole (unsharded) table, one host round
+// trip when the batch ran on device (the optional D2H of its reports into
+// rep_host is queued before it). If the walk paused (draw window) or the gather
+// staging was too small, the device-count gather/scatter were no-ops and the
+// batch is finished on the host-driven path. On return the reports are in
+// rep_host (if given). *n_ok: inserts applied (the first with a bucket out of
+// range when unchecked).
+static int insert_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, const uint8_t* d_payload,
+                       uint64_t n, uint32_t* d_reports, cudaStream_t s, uint8_t* rep_host, bool checked,
+                       uint64_t* n_ok) {
+    int rc = walk_impl(t, d_b1, d_b2, n, d_reports, s, true, checked, n_ok);
+    if (rc) return rc;
+    const ShardMap none{};
+    bool done = false;
+    if (t->state_on_device) {
+        if ((rc = gather_impl(t, none, s)) || (rc = scatter_impl(t, d_payload, s))) return rc;
+        if (rep_host && d_reports && *n_ok) XCK(cudaMemcpyAsync(rep_host, d_reports, 16 * *n_ok,
+                                                                cudaMemcpyDeviceToHost, s));
+        if ((rc = sync_state(t, s))) return rc;
+        const uint32_t status = t->h.status;
+        *n_ok = t->h.limit < *n_ok ? t->h.limit : *n_ok;
+        t->h.limit = ~0ull;
+        if (status == 0) {
+            done = true;
+        } else if (status == 1) {  // the walk paused: refill and finish it from resume_at
+            t->h.status = 0;
+            t->h.draw_count = 0;
+            if ((rc = walk_loop(t, d_b1, d_b2, t->h.resume_at, *n_ok, d_reports, s))) return rc;
+        } else {  // 3: gather staging too small; the walk is complete
+            t->h.status = 0;
+        }
+        if ((rc = push_state(t, s))) return rc;  // the device copy stays authoritative
+    }
+    if (!done) {
+        if ((rc = gather_impl(t, none, s)) || (rc = scatter_impl(t, d_payload, s))) return rc;
+        if (rep_host && d_reports && *n_ok) {
+            XCK(cudaMemcpyAsync(rep_host, d_reports, 16 * *n_ok, cudaMemcpyDeviceToHost, s));
+            XCK(cudaStreamSynchronize(s));
+        }
+    }
+    return XPIR_OK;
+}
+
 extern "C" {
 
 int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2,
@@ -189,14 +360,71 @@ int xpir_table_insert_batch_dev(xpir_table* t, const uint32_t* d_b1, const uint3
         return fail(XPIR_EINVAL, "table_insert: payload shard: use insert_walk + apply_gather (all shards) + apply_scatter");
     DeviceGuard g(t->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
-    uint64_t ok = 0;
-    int rc = beta_check(t, d_b1, d_b2, n, s, &ok);
+    // items before the first bad one are inserted, as a loop of Table::insert calls would
+    uint64_t ok = n;
+    int rc = insert_impl(t, d_b1, d_b2, d_payload, n, d_reports, s, nullptr, false, &ok);
     if (rc) return rc;
-    if (ok) {  // items before the bad one are inserted, as a loop of Table::insert calls would
-        rc = insert_impl(t, d_b1, d_b2, d_payload, ok, d_reports, stream);
-        if (rc) return rc;
-    }
+    if (!stream) XCK(cudaStreamSynchronize(s));
     if (ok < n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
+    return XPIR_OK;
+}
+
+int xpir_table_insert_batch_async(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2,
+                                  const uint8_t* d_payload, uint64_t n, uint32_t* d_reports, void* stream,
+                                  void* prefix_done) {
+    if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
+    if (!d_b1 || !d_b2 || !d_payload || !stream) return fail(XPIR_EINVAL, "table_insert_async: null argument");
+    if (t->sharded()) return fail(XPIR_EINVAL, "table_insert_async: whole tables only");
+    if (t->state_on_device || t->async_pending)
+        return fail(XPIR_ESTATE, "table_insert_async: finish the previous batch first");
+    if (n == 0) return XPIR_OK;
+    DeviceGuard g(t->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // everything from and into the device state: capturable in a CUDA graph
+    XCK(cuckoo_parallel_prefix(t->d, t->dstate, d_b1, d_b2, n, d_reports, t->par, s));
+    if (prefix_done) XCK(cudaEventRecord(static_cast<cudaEvent_t>(prefix_done), s));
+    XCK(launch_cuckoo_walk(t->d, t->dstate, d_b1, d_b2, WALK_FROM_STATE, n, d_reports, s));
+    count_launches(1);
+    t->walked = true;
+    t->state_on_device = true;
+    t->max_touched = uint32_t(t->slots());
+    const ShardMap none{};
+    int rc = gather_impl(t, none, s);
+    if (!rc) rc = scatter_impl(t, d_payload, s);
+    if (rc) return rc;
+    t->async_pending = true;
+    t->async = {d_b1, d_b2, d_payload, d_reports, n, s};
+    return XPIR_OK;
+}
+
+int xpir_table_finish(xpir_table* t, uint64_t* n_applied) {
+    if (!t) return fail(XPIR_EINVAL, "table_finish: null table");
+    if (!t->async_pending) {
+        if (n_applied) *n_applied = 0;
+        return XPIR_OK;
+    }
+    DeviceGuard g(t->device);
+    const auto a = t->async;
+    t->async_pending = false;
+    cudaStream_t s = a.s;
+    int rc = sync_state(t, s);
+    if (rc) return rc;
+    const uint32_t status = t->h.status;
+    uint64_t ok = t->h.limit < a.n ? t->h.limit : a.n;
+    t->h.limit = ~0ull;
+    t->h.status = 0;
+    if (status != 0) {
+        if (status == 1) {  // the walk paused for draws: refill and finish it from resume_at
+            t->h.draw_count = 0;
+            if ((rc = walk_loop(t, a.b1, a.b2, t->h.resume_at, ok, a.reports, s))) return rc;
+        }
+        const ShardMap none{};
+        if ((rc = gather_impl(t, none, s)) || (rc = scatter_impl(t, a.payload, s))) return rc;
+    }
+    if ((rc = push_state(t, s))) return rc;
+    XCK(cudaStreamSynchronize(s));
+    if (n_applied) *n_applied = ok;
+    if (ok < a.n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
     return XPIR_OK;
 }
 
@@ -207,11 +435,10 @@ int xpir_table_insert_walk_dev(xpir_table* t, const uint32_t* d_b1, const uint32
     if (!d_b1 || !d_b2) return fail(XPIR_EINVAL, "table_insert: null buffer");
     DeviceGuard g(t->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
-    uint64_t ok = 0;
-    int rc = beta_check(t, d_b1, d_b2, n, s, &ok);
+    uint64_t ok = n;
+    int rc = walk_impl(t, d_b1, d_b2, n, d_reports, s, false, false, &ok);
     if (rc) return rc;
-    rc = table_walk_impl(t, d_b1, d_b2, ok, d_reports, stream);
-    if (rc) return rc;
+    if (!stream) XCK(cudaStreamSynchronize(s));
     // EINVAL with the valid prefix walked: the caller still applies gather/scatter
     if (ok < n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
     return XPIR_OK;
@@ -232,21 +459,21 @@ int xpir_table_apply_gather_dev(xpir_table* t, const xpir_shard_map* map, void* 
     }
     DeviceGuard g(t->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
-    XCK(t->gather.ensure(uint64_t(t->h.n_touched) * t->d.item));
-    t->d.gather = t->gather.as<uint8_t>();
-    XCK(launch_cuckoo_gather_sharded(t->d, &t->h, t->lo, t->hi, t->data, m, s));
-    count_launches(1);
+    int rc = sync_state(t, s);
+    if (!rc) rc = gather_impl(t, m, s);
+    if (rc) return rc;
     if (!stream) XCK(cudaStreamSynchronize(s));
     return XPIR_OK;
 }
 
 int xpir_table_apply_scatter_dev(xpir_table* t, const uint8_t* d_payload, void* stream) {
     if (!t) return fail(XPIR_EINVAL, "table_apply: null table");
-    if (t->h.n_touched && !d_payload) return fail(XPIR_EINVAL, "table_apply: null payload");
     DeviceGuard g(t->device);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : t->stream;
-    XCK(launch_cuckoo_scatter_sharded(t->d, &t->h, t->lo, t->hi, t->data, d_payload, s));
-    count_launches(1);
+    int rc = sync_state(t, s);
+    if (rc) return rc;
+    if (t->h.n_touched && !d_payload) return fail(XPIR_EINVAL, "table_apply: null payload");
+    if ((rc = scatter_impl(t, d_payload, s))) return rc;
     if (!stream) XCK(cudaStreamSynchronize(s));
     return XPIR_OK;
 }
@@ -263,6 +490,8 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b
     if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
     if (n == 0) return XPIR_OK;
     if (!b1 || !b2 || !payload) return fail(XPIR_EINVAL, "table_insert: null buffer");
+    if (t->sharded())
+        return fail(XPIR_EINVAL, "table_insert: payload shard: use insert_walk + apply_gather (all shards) + apply_scatter");
     // cuckoo.cpp:57-58 — validated per item in order; items before the bad one
     // are inserted, exactly as a loop of Table::insert calls would leave them.
     uint64_t ok = n;
@@ -275,19 +504,23 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b
     DeviceGuard g(t->device);
     cudaStream_t s = t->stream;
     if (ok > 0) {
-        XCK(t->in_b1.ensure(4 * ok));
-        XCK(t->in_b2.ensure(4 * ok));
-        XCK(t->in_payload.ensure(ok * t->d.item));
-        XCK(t->in_reports.ensure(16 * ok));
-        XCK(cudaMemcpyAsync(t->in_b1.p, b1, 4 * ok, cudaMemcpyHostToDevice, s));
-        XCK(cudaMemcpyAsync(t->in_b2.p, b2, 4 * ok, cudaMemcpyHostToDevice, s));
-        XCK(cudaMemcpyAsync(t->in_payload.p, payload, ok * t->d.item, cudaMemcpyHostToDevice, s));
-        int rc = insert_impl(t, t->in_b1.as<uint32_t>(), t->in_b2.as<uint32_t>(), t->in_payload.as<uint8_t>(),
-                             ok, t->in_reports.as<uint32_t>(), s);
+        // [beta1 | beta2 | payload | reports] packed: one pinned staging buffer, one H2D
+        const uint64_t o2 = round16(4 * ok), op = o2 + round16(4 * ok), orep = op + round16(ok * t->d.item);
+        const uint64_t total = orep + 16 * ok;
+        XCK(t->stage.ensure(total));
+        std::memcpy(t->stage.p, b1, 4 * ok);
+        std::memcpy(t->stage.p + o2, b2, 4 * ok);
+        std::memcpy(t->stage.p + op, payload, ok * t->d.item);
+        XCK(t->in_pack.ensure(total));
+        uint8_t* dp = t->in_pack.as<uint8_t>();
+        XCK(cudaMemcpyAsync(dp, t->stage.p, orep, cudaMemcpyHostToDevice, s));
+        uint64_t applied = ok;
+        int rc = insert_impl(t, reinterpret_cast<const uint32_t*>(dp), reinterpret_cast<const uint32_t*>(dp + o2),
+                             dp + op, ok, reinterpret_cast<uint32_t*>(dp + orep), s, t->stage.p + orep, true,
+                             &applied);
+        XCK(t->stage.release_after(s));
         if (rc) return rc;
-        if (reports)
-            XCK(cudaMemcpyAsync(reports, t->in_reports.p, 16 * ok, cudaMemcpyDeviceToHost, s));
-        XCK(cudaStreamSynchronize(s));
+        if (reports) std::memcpy(reports, t->stage.p + orep, 16 * ok);
     }
     if (ok < n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
     return XPIR_OK;
@@ -304,7 +537,15 @@ int xpir_table_reserve(xpir_table* t, uint64_t max_batch) {
     XCK(t->in_b1.ensure(4 * max_batch));
     XCK(t->in_b2.ensure(4 * max_batch));
     XCK(t->in_reports.ensure(16 * max_batch));
-    XCK(cuckoo_reserve(t->par, max_batch, t->d.buckets, t->stream));  // claim-sort scratch
+    // the packed host-input staging of xpir_table_insert_batch, pinned, for max_batch writes
+    const uint64_t pack = 2 * round16(4 * max_batch) + round16(max_batch * t->d.item) + 16 * max_batch;
+    XCK(t->stage.ensure(pack));
+    XCK(t->in_pack.ensure(pack));
+    XCK(cuckoo_reserve(t->par, max_batch, t->d.buckets, t->stream));  // parallel-prefix scratch
+    // a full draw window, so a round's eviction walk rarely has to pause for draws
+    int rc = sync_state(t, t->stream);
+    if (rc) return rc;
+    if ((rc = refill_draws(t, uint64_t(DRAW_CAP) / 2, t->stream)) || (rc = push_state(t, t->stream))) return rc;
     XCK(cudaStreamSynchronize(t->stream));
     return XPIR_OK;
 }

@@ -43,8 +43,10 @@ int xpir_window_create(int device, uint32_t m_bits, uint32_t h, uint32_t w, xpir
     win->words = (uint64_t(m_bits) + 63) / 64;
     unsigned long long* d = nullptr;
     cudaError_t e = cudaMalloc(&d, 8 * win->words);
-    if (e == cudaSuccess) e = cudaMemset(d, 0, 8 * win->words);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&win->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMemsetAsync(d, 0, 8 * win->words, win->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(win->stream);
+    if (e == cudaSuccess) e = win->stage.ensure(4096);  // pinned position staging (absorb)
     if (e != cudaSuccess) {
         if (d) cudaFree(d);
         delete win;
@@ -64,6 +66,7 @@ int xpir_window_destroy(xpir_window* win) {
     win->seqs.release();
     win->scratch.release();
     win->enc.release();
+    win->stage.release();
     cudaStreamDestroy(win->stream);
     delete win;
     return XPIR_OK;
@@ -95,6 +98,24 @@ int xpir_window_absorb(xpir_window* win, const uint32_t* pos, uint64_t n) {
     XCK(cudaMemcpyAsync(win->pos.p, pos, 4 * n, cudaMemcpyHostToDevice, win->stream));
     return xpir_window_absorb_dev(win, win->pos.as<uint32_t>(), n, win->stream);
 }
+
+}  // extern "C"
+
+int window_absorb_prechecked(xpir_window* win, const uint32_t* pos, uint64_t n) {
+    if (!n) return XPIR_OK;
+    std::lock_guard<std::mutex> lk(win->mu);
+    DeviceGuard g(win->device);
+    XCK(win->stage.ensure(4 * n));
+    std::memcpy(win->stage.p, pos, 4 * n);
+    XCK(win->pos.ensure(4 * n));
+    XCK(cudaMemcpyAsync(win->pos.p, win->stage.p, 4 * n, cudaMemcpyHostToDevice, win->stream));
+    XCK(win->stage.release_after(win->stream));
+    XCK(launch_absorb_unchecked(win->pos.as<uint32_t>(), n, win->deltas.back(), win->stream));
+    count_launches(1);
+    return XPIR_OK;
+}
+
+extern "C" {
 
 int xpir_window_absorb_interest(xpir_window* win, const uint8_t id[16], const uint64_t* seqs,
                                 uint64_t n) {

@@ -94,6 +94,8 @@ cudaError_t launch_keystream(const uint8_t* key_host32, uint64_t nonce, uint64_t
                              uint8_t* out, uint64_t len, cudaStream_t s);
 cudaError_t launch_keystream_rows(const uint8_t* key_host32, uint64_t nonce0, uint32_t rows,
                                   uint64_t len, uint8_t* out, uint64_t row_stride, cudaStream_t s);
+cudaError_t launch_prf2(const uint64_t k1[2], const uint64_t k2[2], const uint64_t* in, uint64_t n,
+                        uint64_t modulus, uint32_t* o1, uint32_t* o2, cudaStream_t s);
 cudaError_t launch_prf(uint64_t k0, uint64_t k1, const uint64_t* in, uint64_t n, uint64_t modulus,
                        uint64_t* out, uint32_t* out32, cudaStream_t s);
 cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint64_t n, uint32_t h,
@@ -105,6 +107,7 @@ cudaError_t launch_bloom_item(const uint8_t* item_dev, uint32_t len, uint32_t h,
 // out-of-range position (or ~0); positions before it are absorbed (notify.cpp:60-65).
 cudaError_t launch_absorb(const uint32_t* pos, uint64_t n, uint32_t m_bits,
                           unsigned long long* words, unsigned long long* scratch, cudaStream_t s);
+cudaError_t launch_absorb_unchecked(const uint32_t* pos, uint64_t n, unsigned long long* words, cudaStream_t s);
 // first index whose beta1 or beta2 >= buckets into *first_bad (~0 when none)
 cudaError_t launch_beta_check(const uint32_t* b1, const uint32_t* b2, uint64_t n, uint32_t buckets,
                               unsigned long long* first_bad, cudaStream_t s);
@@ -157,7 +160,30 @@ struct CuckooState {
     uint32_t batch_id;
     uint32_t status;          // 0 ok, 1 need more draws (resume_at valid), 2 fifo overflow
     uint64_t resume_at;       // first insert not yet processed
+    uint32_t walked;          // a walk kernel processed inserts this batch (items may have moved)
+    uint32_t pad_;
+    uint64_t limit;           // inserts at or past it are never walked (first out-of-range beta)
 };
+// Device-side start of a walk: i0 == WALK_FROM_STATE starts at gst->resume_at
+// (left there by the parallel prefix); a walk with nothing to do returns at once.
+constexpr uint64_t WALK_FROM_STATE = ~0ull;
+__device__ __forceinline__ bool walk_prologue(CuckooState* gst, uint64_t& i0, uint64_t& n) {
+    if (i0 == WALK_FROM_STATE) i0 = *reinterpret_cast<volatile uint64_t*>(&gst->resume_at);
+    const uint64_t lim = *reinterpret_cast<volatile uint64_t*>(&gst->limit);
+    if (lim < n) n = lim;
+    if (i0 >= n) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            gst->status = 0;
+            gst->resume_at = n;
+        }
+        return false;
+    }
+    __syncthreads();  // every thread has read resume_at before it can change
+    if (threadIdx.x == 0) gst->walked = 1;
+    __syncthreads();
+    return true;
+}
 
 cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32_t* beta1,
                                const uint32_t* beta2, uint64_t i0, uint64_t n, uint32_t* reports,
@@ -168,8 +194,11 @@ bool walk_x_supported(const CuckooDev& d);
 cudaError_t launch_cuckoo_walk_x(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
                                  uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s);
 bool walk_w_supported(const CuckooDev& d);
+// force_global: the global-map variant even when the shared-memory maps fit (small
+// batches: staging the maps costs O(slots) per launch, the global variant nothing)
 cudaError_t launch_cuckoo_walk_w(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
-                                 uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s);
+                                 uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s,
+                                 bool force_global = false);
 // Bucket-range payload shards of one logical table (metadata replicated on every
 // shard, each shard holds the payloads of buckets [lo[g], lo[g+1])). data[g] may
 // be a CUDA-IPC-mapped peer pointer (NVLink).
@@ -181,26 +210,36 @@ struct ShardMap {
 // Phase 1: stage the pre-round payloads that move INTO this shard's range (from
 // any shard); phase 2 (after every shard's phase 1): write this shard's touched
 // slots. The payload array `table` holds buckets [lo, hi) of this shard.
+// With dev_state != null the touched count is read on device from it (the host
+// copy `st` is stale; max_touched bounds the grid) — no host round trip between
+// the walk and the payload moves.
 cudaError_t launch_cuckoo_gather_sharded(const CuckooDev& d, const CuckooState* st, uint32_t lo, uint32_t hi,
-                                         const uint8_t* table, const ShardMap& map, cudaStream_t s);
+                                         const uint8_t* table, const ShardMap& map, cudaStream_t s,
+                                         CuckooState* dev_state = nullptr, uint32_t max_touched = 0,
+                                         uint32_t cap = 0);
 cudaError_t launch_cuckoo_scatter_sharded(const CuckooDev& d, const CuckooState* st, uint32_t lo, uint32_t hi,
-                                          uint8_t* table, const uint8_t* payload, cudaStream_t s);
+                                          uint8_t* table, const uint8_t* payload, cudaStream_t s,
+                                          const CuckooState* dev_state = nullptr, uint32_t max_touched = 0);
 
 // Grow-only scratch of the parallel eviction-free prefix (cuckoo_par.cu).
 struct CuckooParScratch {
     void *keys_a = nullptr, *keys_b = nullptr, *outcome = nullptr, *succ = nullptr;
-    void *slot_of = nullptr, *flags = nullptr, *cub_tmp = nullptr;
+    void *slot_of = nullptr, *flags = nullptr, *cub_tmp = nullptr, *rank = nullptr;
     size_t keys_a_cap = 0, keys_b_cap = 0, outcome_cap = 0, succ_cap = 0, slot_cap = 0, flags_cap = 0,
-           cub_cap = 0;
+           cub_cap = 0, rank_cap = 0;
     void release() {
-        for (void* p : {keys_a, keys_b, outcome, succ, slot_of, flags, cub_tmp})
+        for (void* p : {keys_a, keys_b, outcome, succ, slot_of, flags, cub_tmp, rank})
             if (p) cudaFree(p);
         *this = CuckooParScratch{};
     }
 };
 cudaError_t cuckoo_reserve(CuckooParScratch& sc, uint64_t n, uint32_t buckets, cudaStream_t s);
-cudaError_t cuckoo_parallel_prefix(const CuckooDev& d, CuckooState& h, const uint32_t* b1, const uint32_t* b2,
-                                   uint64_t n, uint32_t* reports, CuckooParScratch& sc, uint64_t* applied,
-                                   cudaStream_t s);
+// Launches the parallel eviction-free prefix of a batch of n inserts on stream s,
+// entirely from and into the device state `st` (no host round trip): it starts
+// the batch (batch_id + 1, n_touched = 0), places the prefix, and leaves
+// resume_at = prefix length, limit = first insert with a bucket out of range
+// (n when none) for the walk launched after it with i0 = WALK_FROM_STATE.
+cudaError_t cuckoo_parallel_prefix(const CuckooDev& d, CuckooState* st, const uint32_t* b1, const uint32_t* b2,
+                                   uint64_t n, uint32_t* reports, CuckooParScratch& sc, cudaStream_t s);
 
 }  // namespace xpir

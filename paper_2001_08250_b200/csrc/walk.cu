@@ -62,6 +62,7 @@ template <bool G, uint32_t DEP>
 __global__ void __launch_bounds__(256, 1)
 k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __restrict__ beta1,
                 const uint32_t* __restrict__ beta2, uint64_t i0, uint64_t n, uint32_t* __restrict__ reports) {
+    if (!walk_prologue(gst, i0, n)) return;
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t slots = G ? 0u : d.buckets * (DEP ? DEP : d.depth);
     const uint32_t words = (slots + 31) / 32;
@@ -363,9 +364,9 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
 }
 
 cudaError_t launch_cuckoo_walk_w(const CuckooDev& d, CuckooState* st, const uint32_t* beta1, const uint32_t* beta2,
-                                 uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s) {
+                                 uint64_t i0, uint64_t n, uint32_t* reports, cudaStream_t s, bool force_global) {
     const uint64_t slots = uint64_t(d.buckets) * d.depth;
-    const bool g = slots > WALKW_MAX_SLOTS;
+    const bool g = force_global || slots > WALKW_MAX_SLOTS;
     const size_t smem = walk_w_smem_bytes(g ? 0 : slots);
     auto k = d.depth == 4 ? (g ? k_cuckoo_walk_w<true, 4> : k_cuckoo_walk_w<false, 4>)
                           : (g ? k_cuckoo_walk_w<true, 0> : k_cuckoo_walk_w<false, 0>);

@@ -111,6 +111,7 @@ template <uint32_t DEP>
 __global__ void __launch_bounds__(256, 1)
 k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __restrict__ beta1,
                 const uint32_t* __restrict__ beta2, uint64_t i0, uint64_t n, uint32_t* __restrict__ reports) {
+    if (!walk_prologue(gst, i0, n)) return;
     extern __shared__ __align__(16) uint8_t smx[];
     const uint32_t slots = d.buckets * (DEP ? DEP : d.depth);
     const XLayout L(slots);

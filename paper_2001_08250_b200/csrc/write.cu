@@ -89,6 +89,23 @@ __global__ void k_prf(uint64_t k0, uint64_t k1, const uint64_t* __restrict__ in,
     if (out32) out32[t] = uint32_t(v);
 }
 
+// beta1 = prf(K1, x), beta2 = prf(K2, x) of every write key (logproto.cpp:74-75)
+__global__ void k_prf2(uint64_t a0, uint64_t a1, uint64_t c0, uint64_t c1, const uint64_t* __restrict__ in,
+                       uint64_t n, uint64_t modulus, uint32_t* __restrict__ o1, uint32_t* __restrict__ o2) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint64_t x = in[t];
+    o1[t] = uint32_t(prf(a0, a1, x, modulus));
+    o2[t] = uint32_t(prf(c0, c1, x, modulus));
+}
+
+cudaError_t launch_prf2(const uint64_t k1[2], const uint64_t k2[2], const uint64_t* in, uint64_t n,
+                        uint64_t modulus, uint32_t* o1, uint32_t* o2, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    k_prf2<<<uint32_t((n + 127) / 128), 128, 0, s>>>(k1[0], k1[1], k2[0], k2[1], in, n, modulus, o1, o2);
+    return cudaGetLastError();
+}
+
 struct Id16 {
     uint8_t b[16];
 };
@@ -96,22 +113,26 @@ struct Id16 {
 __global__ void k_interest(Id16 id, const uint64_t* __restrict__ seqs, uint64_t n, uint32_t h,
                            uint32_t m_bits, uint32_t* __restrict__ pos_out,
                            unsigned long long* __restrict__ words) {
-    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= n * h) return;
-    const uint64_t w = t / h;
-    const uint32_t k = uint32_t(t - w * h);
     uint64_t w0 = 0, w1 = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         w0 |= uint64_t(id.b[i]) << (8 * i);
         w1 |= uint64_t(id.b[8 + i]) << (8 * i);
     }
-    // item = LogId || BE64(seq) (notify.cpp:33): the BE64 bytes read as an LE word
-    const uint64_t w2 = __byte_perm(uint32_t(seqs[w] >> 32), 0, 0x0123) |
-                        uint64_t(__byte_perm(uint32_t(seqs[w]), 0, 0x0123)) << 32;
-    const uint32_t pos = bloom_position_interest(w0, w1, w2, k, m_bits);
-    if (pos_out) pos_out[t] = pos;
-    if (words) atomicOr(words + (pos >> 6), 1ull << (pos & 63));
+    // grid-stride: the grid holds a few blocks per SM, so a concurrent write-round
+    // chain (the cooperative placement kernel, the payload scatter) finds room
+    const uint64_t total = n * h, stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const uint64_t w = t / h;
+        const uint32_t k = uint32_t(t - w * h);
+        // item = LogId || BE64(seq) (notify.cpp:33): the BE64 bytes read as an LE word
+        const uint64_t sq = seqs[w];
+        const uint64_t w2 = __byte_perm(uint32_t(sq >> 32), 0, 0x0123) |
+                            uint64_t(__byte_perm(uint32_t(sq), 0, 0x0123)) << 32;
+        const uint32_t pos = bloom_position_interest(w0, w1, w2, k, m_bits);
+        if (pos_out) pos_out[t] = pos;
+        if (words) atomicOr(words + (pos >> 6), 1ull << (pos & 63));
+    }
 }
 
 __global__ void k_bloom_item(const uint8_t* __restrict__ item, uint32_t len, uint32_t h,
@@ -166,6 +187,7 @@ __global__ void __launch_bounds__(256)
 k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __restrict__ beta1,
               const uint32_t* __restrict__ beta2, uint64_t i0, uint64_t n,
               uint32_t* __restrict__ reports, int use_smem) {
+    if (!walk_prologue(gst, i0, n)) return;
     extern __shared__ __align__(16) uint32_t sm[];
     const uint64_t slots = uint64_t(d.buckets) * d.depth;
     const uint32_t words = use_smem ? uint32_t((slots + 31) / 32) : 0;
@@ -381,7 +403,16 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
 // owning each bucket range"). The walk is replicated, so every shard knows every
 // touched slot and its origin; a shard only materialises the slots of its range.
 __global__ void k_cuckoo_gather_sharded(CuckooDev d, uint32_t n_touched, uint64_t f_lo, uint64_t f_hi,
-                                        const uint8_t* __restrict__ table, ShardMap map) {
+                                        const uint8_t* __restrict__ table, ShardMap map,
+                                        CuckooState* __restrict__ dev_state, uint32_t cap) {
+    if (dev_state) {  // the walk ran on device: its count, unless it paused (host finishes it)
+        if (dev_state->status || !dev_state->walked) return;
+        n_touched = dev_state->n_touched;
+        if (n_touched > cap) {  // staging too small: the host redoes gather + scatter
+            if (blockIdx.x == 0 && threadIdx.x == 0) dev_state->status = 3;
+            return;
+        }
+    }
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_touched; k += nw) {
@@ -410,7 +441,12 @@ __global__ void k_cuckoo_gather_sharded(CuckooDev d, uint32_t n_touched, uint64_
 
 __global__ void k_cuckoo_scatter_sharded(CuckooDev d, uint32_t n_touched, uint64_t f_lo, uint64_t f_hi,
                                          uint8_t* __restrict__ table, const uint8_t* __restrict__ payload,
-                                         uint32_t batch_id) {
+                                         uint32_t batch_id, const CuckooState* __restrict__ dev_state) {
+    if (dev_state) {  // the walk ran on device: its count and batch, unless it paused / overflowed
+        if (dev_state->status) return;
+        n_touched = dev_state->n_touched;
+        batch_id = dev_state->batch_id;
+    }
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_touched; k += nw) {
@@ -433,22 +469,28 @@ __global__ void k_cuckoo_scatter_sharded(CuckooDev d, uint32_t n_touched, uint64
 }
 
 cudaError_t launch_cuckoo_gather_sharded(const CuckooDev& d, const CuckooState* st, uint32_t lo, uint32_t hi,
-                                         const uint8_t* table, const ShardMap& map, cudaStream_t s) {
-    if (!st->n_touched) return cudaSuccess;
-    uint32_t g = (st->n_touched + 7) / 8;
-    if (g > 148 * 16) g = 148 * 16;
+                                         const uint8_t* table, const ShardMap& map, cudaStream_t s,
+                                         CuckooState* dev_state, uint32_t max_touched, uint32_t cap) {
+    const uint32_t nt = dev_state ? max_touched : st->n_touched;
+    if (!nt) return cudaSuccess;
+    // warp per slot, grid-stride; with the count on device the grid is sized for the
+    // bound, and a batch with nothing to move returns from every block at once
+    uint32_t g = (nt + 7) / 8;
+    if (g > (dev_state ? 148 * 4 : 148 * 16)) g = dev_state ? 148 * 4 : 148 * 16;
     k_cuckoo_gather_sharded<<<g, 256, 0, s>>>(d, st->n_touched, uint64_t(lo) * d.depth, uint64_t(hi) * d.depth,
-                                              table, map);
+                                              table, map, dev_state, cap);
     return cudaGetLastError();
 }
 
 cudaError_t launch_cuckoo_scatter_sharded(const CuckooDev& d, const CuckooState* st, uint32_t lo, uint32_t hi,
-                                          uint8_t* table, const uint8_t* payload, cudaStream_t s) {
-    if (!st->n_touched) return cudaSuccess;
-    uint32_t g = (st->n_touched + 7) / 8;
+                                          uint8_t* table, const uint8_t* payload, cudaStream_t s,
+                                          const CuckooState* dev_state, uint32_t max_touched) {
+    const uint32_t nt = dev_state ? max_touched : st->n_touched;
+    if (!nt) return cudaSuccess;
+    uint32_t g = (nt + 7) / 8;
     if (g > 148 * 16) g = 148 * 16;
     k_cuckoo_scatter_sharded<<<g, 256, 0, s>>>(d, st->n_touched, uint64_t(lo) * d.depth, uint64_t(hi) * d.depth,
-                                               table, payload, st->batch_id);
+                                               table, payload, st->batch_id, dev_state);
     return cudaGetLastError();
 }
 
@@ -531,7 +573,16 @@ cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint
     if (!t) return cudaSuccess;
     Id16 id;
     std::memcpy(id.b, id16_host, 16);
-    k_interest<<<uint32_t((t + 127) / 128), 128, 0, s>>>(id, seqs, n, h, m_bits, pos_out, words);
+    static const uint32_t per_sm = [] {  // XPIR_INTEREST_CTAS_PER_SM (A/B runs), default 16 = full occupancy
+        const char* e = std::getenv("XPIR_INTEREST_CTAS_PER_SM");
+        const int v = e ? std::atoi(e) : 16;
+        return uint32_t(v > 0 ? v : 16);
+    }();
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint64_t want = (t + 127) / 128, cap = uint64_t(sms) * per_sm;
+    k_interest<<<uint32_t(want < cap ? want : cap), 128, 0, s>>>(id, seqs, n, h, m_bits, pos_out, words);
     return cudaGetLastError();
 }
 
@@ -554,6 +605,18 @@ cudaError_t launch_absorb(const uint32_t* pos, uint64_t n, uint32_t m_bits,
     return cudaGetLastError();
 }
 
+// positions already checked against m_bits (host): OR them in, no limit
+__global__ void k_absorb_all(const uint32_t* __restrict__ pos, uint64_t n, unsigned long long* __restrict__ words) {
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < n) atomicOr(words + (pos[t] >> 6), 1ull << (pos[t] & 63));
+}
+
+cudaError_t launch_absorb_unchecked(const uint32_t* pos, uint64_t n, unsigned long long* words, cudaStream_t s) {
+    if (!n) return cudaSuccess;
+    k_absorb_all<<<uint32_t((n + 255) / 256), 256, 0, s>>>(pos, n, words);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_beta_check(const uint32_t* b1, const uint32_t* b2, uint64_t n, uint32_t buckets,
                               unsigned long long* first_bad, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(first_bad, 0xff, 8, s);
@@ -571,11 +634,17 @@ cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32
         const char* e = std::getenv("XPIR_CUCKOO_WALK");
         return e ? e[0] - '0' : 0;
     }();
-    if (choice != 1 && choice != 2 && walk_x_supported(d))
-        return launch_cuckoo_walk_x(d, st, beta1, beta2, i0, n, reports, s);
-    if (choice != 1 && walk_w_supported(d)) return launch_cuckoo_walk_w(d, st, beta1, beta2, i0, n, reports, s);
+    // a batch small against the table (e.g. one ServerCore::apply_write) skips the
+    // O(slots) on-chip staging of the other variants: global-map warp walk (a walk
+    // that starts where the parallel prefix stopped is sized by the whole batch)
     const uint64_t slots = uint64_t(d.buckets) * d.depth;
-    const bool use_smem = slots <= WALK_SMEM_MAX_SLOTS;
+    const uint64_t span = i0 == WALK_FROM_STATE ? n : n - i0;
+    const bool small = span * 256 < slots;
+    if (choice != 1 && choice != 2 && !small && walk_x_supported(d))
+        return launch_cuckoo_walk_x(d, st, beta1, beta2, i0, n, reports, s);
+    if (choice != 1 && walk_w_supported(d))
+        return launch_cuckoo_walk_w(d, st, beta1, beta2, i0, n, reports, s, small);
+    const bool use_smem = slots <= WALK_SMEM_MAX_SLOTS && !small;
     const size_t words = use_smem ? (slots + 31) / 32 : 0;
     const size_t smem = ((2 * words + 3) & ~size_t(3)) * 4 + WALK_DRAWS_SMEM * 8 + 2 * WALK_CHUNK * 4 + 16;
     cudaError_t e = cudaFuncSetAttribute(k_cuckoo_walk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

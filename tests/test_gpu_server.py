@@ -165,3 +165,53 @@ def test_pinned_snapshot_survives_ring_turnover(xp, port, cuda):
     img = T.data().reshape(nb, depth * item)
     assert np.array_equal(sv.snapshot(0).answer_batch(q)[0], img[8] ^ img[15])
     sv.close()
+
+
+@pytest.mark.parametrize("nb,depth,cap", [(128, 4, 400), (200, 3, 500)])
+def test_single_write_rounds_async_walk(xp, port, cuda, nb, depth, cap):
+    """One apply_write per call (the ServerCore drop-in's path): the walk, payload
+    gather and scatter run back to back with one host round trip. Filled past
+    capacity (FIFO GC) with evictions, bit-exact against the oracle throughout;
+    a bad interest position mid-round follows notify.cpp:62 (write inserted,
+    positions before the bad one absorbed, write not counted)."""
+    m, h, W, R, ring = 2048, 3, 3, 7, 2
+    item = 24
+    g = np.random.default_rng(nb + depth)
+    seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+    sv = xp.Server(nb, depth, cap, item, seed, m, h, W, R, ring)
+    T = port.table(nb, depth, cap, item, seed)
+    PW = port.window(m, h, W)
+    PW.rotate()
+    writes = 0
+    for k in range(cap + 150):
+        b1 = g.integers(0, nb, 1).astype(np.uint32)
+        b2 = g.integers(0, nb, 1).astype(np.uint32)
+        pl = g.integers(0, 256, (1, item), dtype=np.uint8)
+        pos = g.integers(0, m, (1, h)).astype(np.uint32)
+        rep, _ = sv.apply_round(b1, b2, pl, pos)
+        assert np.array_equal(rep, T.insert_batch(b1, b2, pl)), k
+        PW.absorb(pos[0])
+        writes += 1
+        if writes % R == 0:
+            PW.rotate()
+        if k % 50 == 0:
+            assert sv.table_digest() == T.state_digest(), k
+            assert sv.window_digest() == PW.digest(), k
+    # a round of 3 writes whose second has a position out of range
+    b1 = g.integers(0, nb, 3).astype(np.uint32)
+    b2 = g.integers(0, nb, 3).astype(np.uint32)
+    pl = g.integers(0, 256, (3, item), dtype=np.uint8)
+    pos = g.integers(0, m, (3, h)).astype(np.uint32)
+    pos[1, 2] = m + 5
+    with pytest.raises(xp.InvalidArgument):
+        sv.apply_round(b1, b2, pl, pos)
+    T.insert_batch(b1[:2], b2[:2], pl[:2])
+    PW.absorb(pos[0])
+    writes += 1
+    if writes % R == 0:
+        PW.rotate()
+    PW.absorb(pos[1, :2])
+    assert sv.table_digest() == T.state_digest()
+    assert sv.window_digest() == PW.digest()
+    assert sv.info()["writes"] == writes
+    sv.close()

@@ -151,6 +151,22 @@ def test_device_inputs_out_of_range_bucket(xp, port, cuda, bad_at, which):
     assert T2.writes_applied() == bad_at
 
 
+def test_write_betas_match_prf(xp, port, cuda):
+    """beta1/beta2 of a write batch in one kernel == crypto::prf per key (crypto.cpp:17-33)."""
+    torch = cuda
+    g = np.random.default_rng(12)
+    k1, k2 = g.integers(0, 256, 16, dtype=np.uint8).tobytes(), g.integers(0, 256, 16, dtype=np.uint8).tobytes()
+    xs = g.integers(0, 2**63, 3000, dtype=np.uint64)
+    for m in (32768, 1000, 3):
+        d1 = torch.empty(3000, dtype=torch.int32, device="cuda")
+        d2 = torch.empty_like(d1)
+        xp.write_betas_dev(k1, k2, torch.from_numpy(xs.view(np.int64)).cuda(), 3000, m, d1, d2)
+        torch.cuda.synchronize()
+        want1 = [port.prf(k1, int(x), m) for x in xs[:300]]
+        want2 = [port.prf(k2, int(x), m) for x in xs[:300]]
+        assert d1.cpu().numpy()[:300].tolist() == want1 and d2.cpu().numpy()[:300].tolist() == want2
+
+
 def test_window_rotate_and_range(xp, port, cuda):
     for w in (1, 2, 3):
         A, B = xp.Window(1000, 3, w), port.window(1000, 3, w)
