@@ -146,12 +146,13 @@ class CpuReference:
                                   for s in seeds])
         return self.q[B]
 
-    def time(self, B) -> float:
+    def time(self, B, threads: int | None = None) -> float:
         q = self.queries(B)
+        th = self.threads if threads is None else threads
         if self.kind == "reference":
-            return self.snap.answer_batch(q, B, self.threads)[1]
+            return self.snap.answer_batch(q, B, th)[1]
         t0 = time.perf_counter()
-        self.o.answer_batch(self.db, N_BUCKETS, BUCKET_BYTES, q, B, threads=self.threads)
+        self.o.answer_batch(self.db, N_BUCKETS, BUCKET_BYTES, q, B, threads=th)
         return time.perf_counter() - t0
 
     def calibrate(self, target_s: float, max_per_thread: int = 256) -> int:
@@ -169,10 +170,13 @@ class CpuReference:
 
 
 def cpu_reference_sample(target_s: float = 15.0):
+    """All-core rate on a calibrated sample, plus the single-thread rate (the
+    reference's answer_batch as it ships, one core) on 4 requests."""
     ref = CpuReference()
     B = ref.calibrate(target_s)
     secs = ref.time(B)
-    return B / secs, ref.threads, ref.describe(B, secs), ref.kind
+    one = 4 / ref.time(4, threads=1)
+    return B / secs, ref.threads, ref.describe(B, secs), ref.kind, one
 
 
 def run_reference(args):
@@ -309,6 +313,8 @@ def main():
         dist.barrier()
     xp.scan_timing_collect()
     xp.scan_timing(True)
+    if sh is not None and sh.fused:
+        sh.store.peer_stats(reset=True)
     l0 = xp.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -328,6 +334,15 @@ def main():
     ms = max_over_ranks(e0.elapsed_time(e1))
     ms_per_step = ms / args.steps
     value = B / (ms_per_step * 1e-3)
+
+    # bytes the fused epilogue pushed over NVLink per rank per step, against a reduce-scatter's
+    peer_bytes = None
+    if sh is not None and sh.fused:
+        ps = sh.store.peer_stats()
+        remote = max_over_ranks(float(ps["remote_bytes"])) / args.steps
+        peer_bytes = {"remote_per_rank_per_step_max": remote,
+                      "reduce_scatter_bytes_per_rank": B * BUCKET_BYTES * (world - 1) / world,
+                      "ratio": remote / (B * BUCKET_BYTES * (world - 1) / world)}
 
     # parity of the last timed step's output: every reference-sampled row this rank owns
     parity = "unchecked (not the config-4 workload)"
@@ -408,7 +423,7 @@ def main():
     roof = {
         "bound": "alu",
         "kernel": {1: "k_scan_direct", 2: "k_scan_m4rm", 5: "k_scan_m4rm_tmem",
-                   6: "k_scan_nib", 7: "k_scan_m4rm4", 8: "k_scan_m4rm_q"}.get(xp.last_scan_kernel(), "?"),
+                   7: "k_scan_m4rm4", 8: "k_scan_m4rm_q", 9: "k_scan_m4rm6"}.get(xp.last_scan_kernel(), "?"),
         "unit": "Tops/s (32-bit masked-XOR lane ops)",
         "achieved": achieved / 1e12,
         "peak": peaks["lop3_per_s"] / 1e12,
@@ -434,8 +449,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            rate, threads, desc, kind = cpu_reference_sample(target_s=15.0)
-            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": desc}
+            rate, threads, desc, kind, one = cpu_reference_sample(target_s=15.0)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "sample": desc,
+                   "single_thread_value": one,
+                   "single_thread_sample": "4 of the config-4 requests, one thread (answer_batch as shipped)"}
         except Exception as ex:  # the oracle is optional on the measuring host
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex!r}"}
@@ -451,6 +468,7 @@ def main():
             "reduce": ("none" if sh is None else
                        "fused peer epilogue (tile fix-up)" if sh.fused else "IPC xor reduce-scatter"),
             "parity": parity,
+            **({"peer_bytes": peer_bytes} if peer_bytes else {}),
             "effective_scan_GBps": B * N_BUCKETS * BUCKET_BYTES / (ms_per_step * 1e-3) / 1e9,
             "gpu_launches": launches,
             "roofline": roof,

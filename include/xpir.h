@@ -148,7 +148,7 @@ int xpir_xor_reduce_dev(int device, uint8_t* d_dst, const uint8_t* const* d_srcs
 typedef struct {
     int kernel;        /* 0 = auto, 1 = direct select-XOR, 2 = M4RM byte tables (auto variant),
                           4 = M4RM register accumulators, 5 = M4RM half-TMEM accumulators,
-                          6 = warp-private nibble tables, 7 = M4RM nibble tables,
+                          7 = M4RM nibble tables,
                           8 = M4RM quad-interleaved 32-byte-column tables with full-TMEM
                               accumulators (auto for B >= 2048, S % 32 == 0),
                           9 = M4RM 6-bucket tables (64 rows per 6 buckets) */

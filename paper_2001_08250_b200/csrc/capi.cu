@@ -327,30 +327,15 @@ uint64_t xpir_query_window_bytes(const xpir_store* st) {
 // queries), 1 = direct select-XOR (S % 16 == 0; row-major query window),
 // 3 = byte-granular (any S).
 // ---------------------------------------------------------------------------
-// Batch-size crossovers from the config-5 sweep: the byte-table
-// M4RM kernels from 128 requests; below, the direct kernel. The warp-private
-// nibble-table kernel (6) measured slower than direct at every B in [8, 128)
-// (latency-bound), so it is selectable but not chosen automatically.
-static uint32_t g_nib_min_batch = 0xffffffffu;
-static uint32_t g_k4_min_batch = 24;   // nibble-table M4RM (kernel 7) from here
-static uint32_t g_m4_min_batch = 257;  // byte-table M4RM (kernels 2/5) from here
-static uint32_t g_q_min_batch = 2048;  // quad-table full-TMEM M4RM (kernel 8) from here
-// 6-bucket-table M4RM (kernel 9) for B in [129, 256]: 6-15% faster than the
-// nibble tables there (1 GiB store, S = 1024/4096: B = 256 1.96 vs 2.30 ms);
-// past 256 its request tiles split and the byte tables win
-static uint32_t g_k6_min_batch = 129;
-static uint32_t g_k6_max_batch = 256;
-// XPIR_K9_RANGE="min,max" overrides that range (A/B runs; "1,0" disables kernel 9)
-static const bool g_k6_env = [] {
-    if (const char* e = std::getenv("XPIR_K9_RANGE")) {
-        unsigned a = 0, b = 0;
-        if (std::sscanf(e, "%u,%u", &a, &b) == 2) {
-            g_k6_min_batch = a;
-            g_k6_max_batch = b;
-        }
-    }
-    return true;
-}();
+// Batch-size crossovers from the config-5 sweep: below 24 the direct
+// kernel, nibble tables (7) from 24, 6-bucket tables (9) for 129..256 (6-15% faster
+// than the nibble tables there: 1 GiB store, S = 1024/4096, B = 256 1.96 vs 2.30 ms;
+// past 256 its request tiles split), byte tables (2/5) from 257, quad tables (8) or
+// half-TMEM byte tables (5) by the calibrated cost model from 2048.
+static const uint32_t g_k4_min_batch = 24;
+static const uint32_t g_k6_min_batch = 129, g_k6_max_batch = 256;
+static const uint32_t g_m4_min_batch = 257;
+static const uint32_t g_q_min_batch = 2048;
 
 static int choose_kernel(const xpir_store* st, uint32_t B) {
     int k;
@@ -371,9 +356,10 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
         }
         k = !m4_ok ? 1
             : (B >= g_k6_min_batch && B <= g_k6_max_batch) ? 9
-            : B >= g_m4_min_batch ? 2 : B >= g_k4_min_batch ? 7 : B >= g_nib_min_batch ? 6 : 1;
+            : B >= g_m4_min_batch ? 2 : B >= g_k4_min_batch ? 7 : 1;
     }
-    if ((k == 2 || k == 6 || k == 7 || k == 9) && !m4_ok) k = 1;
+    if (k == 6) k = 1;  // (the warp-private nibble kernel was retired in round 2)
+    if ((k == 2 || k == 7 || k == 9) && !m4_ok) k = 1;
     if (k == 8 && !q_ok) k = 1;
     return k;
 }
@@ -429,15 +415,6 @@ static int run_rows(xpir_store* st, int kernel, const uint8_t* qwin, uint64_t st
         XCK(launch_scan_bytes(a));
         count_launches(1);
         g_last_kernel = 3;
-        return XPIR_OK;
-    }
-    if (kernel == 6) {
-        cudaEvent_t ev;
-        timing_begin(s, &ev);
-        XCK(launch_scan_nib(a, num_sms(st->device)));
-        timing_end(s, ev);
-        count_launches(1);
-        g_last_kernel = 6;
         return XPIR_OK;
     }
     // direct: CTAs XOR their partials straight into `out` (no partial buffer)

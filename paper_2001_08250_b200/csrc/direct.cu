@@ -23,6 +23,12 @@ namespace xpir {
 using ptx::red_xor64;
 
 constexpr int DIRECT_NT = 256;
+// requests per tile that select through the FMA pipe (split-pipe step below):
+// measured on a 1 GiB store (profiles/r02_direct_split_pipe.txt) — one of eight
+// wins 6-7% at B = 16-32; more lose to register pressure and issue slots
+#ifndef XPIR_DIRECT_NI
+#define XPIR_DIRECT_NI(r) ((r) == 8 ? 1 : 0)
+#endif
 
 template <int RPT, int W>
 __global__ void __launch_bounds__(DIRECT_NT)
@@ -80,12 +86,78 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
         }
     };
 
+    // Split-pipe pair step (B > 4): the dense masked XOR is ALU-bound (LOP3 and
+    // SHF issue on the ALU pipe only), so NI of the RPT requests take their
+    // selection through the FMA pipe instead — the bit b in {0,1} is the top bit of
+    // the request's bit-reversed word, read with IMAD.HI(qr, 2) and stepped with
+    // IMAD (qr * 2), and the selected word is IMAD(v, b) — leaving one 3-input
+    // LOP3 per word for two buckets (acc ^ v_a*b_a ^ v_b*b_b). The other requests
+    // keep the predicated XOR (one predicate per request x bucket). Per request x
+    // 2 buckets x 8 words the FMA path costs 20 FMA + 8 ALU instructions, the
+    // predicated path 18 ALU; the pipe model says ~5 of 8 requests, but the kernel
+    // is latency-bound at 2 CTAs/SM and the extra instructions and registers cost
+    // more than the ALU relief beyond NI = 1 (measured, XPIR_DIRECT_NI).
+    constexpr int NI = kMask ? 0 : XPIR_DIRECT_NI(RPT);
+    auto fma_sel = [](uint32_t v, uint32_t b) -> uint32_t {
+        uint32_t r;
+        asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(v), "r"(b));
+        return r;
+    };
+    auto fma_top = [](uint32_t x) -> uint32_t {  // x >> 31, on the FMA pipe
+        uint32_t r;
+        asm("mul.hi.u32 %0, %1, 2;" : "=r"(r) : "r"(x));
+        return r;
+    };
+    auto fma_dbl = [](uint32_t x) -> uint32_t {  // x << 1, on the FMA pipe
+        uint32_t r;
+        asm("mul.lo.u32 %0, %1, 2;" : "=r"(r) : "r"(x));
+        return r;
+    };
+    auto step2 = [&](const uint4 (&va)[W], const uint4 (&vb)[W], uint32_t (&qw)[RPT], uint32_t (&qr)[RPT],
+                     uint32_t bit) {
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            if (i < NI) {
+                const uint32_t ba = fma_top(qr[i]);
+                const uint32_t q1 = fma_dbl(qr[i]);
+                const uint32_t bb = fma_top(q1);
+                qr[i] = fma_dbl(q1);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    acc[i][w].x ^= fma_sel(va[w].x, ba) ^ fma_sel(vb[w].x, bb);
+                    acc[i][w].y ^= fma_sel(va[w].y, ba) ^ fma_sel(vb[w].y, bb);
+                    acc[i][w].z ^= fma_sel(va[w].z, ba) ^ fma_sel(vb[w].z, bb);
+                    acc[i][w].w ^= fma_sel(va[w].w, ba) ^ fma_sel(vb[w].w, bb);
+                }
+            } else {
+                if (qw[i] & bit) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        acc[i][w].x ^= va[w].x;
+                        acc[i][w].y ^= va[w].y;
+                        acc[i][w].z ^= va[w].z;
+                        acc[i][w].w ^= va[w].w;
+                    }
+                }
+                if (qw[i] & (bit << 1)) {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        acc[i][w].x ^= vb[w].x;
+                        acc[i][w].y ^= vb[w].y;
+                        acc[i][w].z ^= vb[w].z;
+                        acc[i][w].w ^= vb[w].w;
+                    }
+                }
+            }
+        }
+    };
+
     if (active) {
         const uint4* col = reinterpret_cast<const uint4*>(db) + uint64_t(c) * W;
         const uint64_t stride = S / 16;
         for (uint32_t jc = jb; jc < je; jc += 32) {
             const uint32_t n = min(32u, je - jc);
-            uint32_t qw[RPT];
+            uint32_t qw[RPT], qr[RPT];
 #pragma unroll
             for (int i = 0; i < RPT; ++i) {
                 uint32_t w = 0;
@@ -97,8 +169,20 @@ k_scan_direct(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uin
                 }
                 if (n < 32) w &= (1u << n) - 1u;
                 qw[i] = kMask ? __brev(w) : w;  // bucket jc+jj -> bit jj (pir.hpp:25); bit 31-jj reversed
+                qr[i] = __brev(w);
             }
-            if (n == 32) {
+            if (n == 32 && NI > 0) {
+#pragma unroll 4
+                for (uint32_t jj = 0; jj < 32; jj += 2) {
+                    uint4 va[W], vb[W];
+#pragma unroll
+                    for (int w = 0; w < W; ++w) {
+                        va[w] = __ldcs(col + uint64_t(jc + jj) * stride + w);
+                        vb[w] = __ldcs(col + uint64_t(jc + jj + 1) * stride + w);
+                    }
+                    step2(va, vb, qw, qr, 1u << jj);
+                }
+            } else if (n == 32) {
 #pragma unroll 8
                 for (uint32_t jj = 0; jj < 32; ++jj) {
                     uint4 v[W];

@@ -77,7 +77,6 @@ cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byt
                                uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4 = false);
 cudaError_t launch_scan_direct(const ScanArgs& a, int num_sms, uint32_t* nsplit_out);
 cudaError_t launch_scan_bytes(const ScanArgs& a);
-cudaError_t launch_scan_nib(const ScanArgs& a, int num_sms);  // nib.cu, S % 128 == 0
 cudaError_t launch_init_out(uint8_t* out, uint32_t B, uint32_t S, const uint8_t* mask_seeds,
                             bool xor_into, cudaStream_t s);
 cudaError_t launch_expand(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,

@@ -119,8 +119,7 @@ __global__ void k_interest(Id16 id, const uint64_t* __restrict__ seqs, uint64_t 
         w0 |= uint64_t(id.b[i]) << (8 * i);
         w1 |= uint64_t(id.b[8 + i]) << (8 * i);
     }
-    // grid-stride: the grid holds a few blocks per SM, so a concurrent write-round
-    // chain (the cooperative placement kernel, the payload scatter) finds room
+    // grid-stride over (write, hash index) pairs
     const uint64_t total = n * h, stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += stride) {
         const uint64_t w = t / h;
@@ -573,15 +572,10 @@ cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint
     if (!t) return cudaSuccess;
     Id16 id;
     std::memcpy(id.b, id16_host, 16);
-    static const uint32_t per_sm = [] {  // XPIR_INTEREST_CTAS_PER_SM (A/B runs), default 16 = full occupancy
-        const char* e = std::getenv("XPIR_INTEREST_CTAS_PER_SM");
-        const int v = e ? std::atoi(e) : 16;
-        return uint32_t(v > 0 ? v : 16);
-    }();
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const uint64_t want = (t + 127) / 128, cap = uint64_t(sms) * per_sm;
+    const uint64_t want = (t + 127) / 128, cap = uint64_t(sms) * 16;  // a full wave, grid-stride beyond
     k_interest<<<uint32_t(want < cap ? want : cap), 128, 0, s>>>(id, seqs, n, h, m_bits, pos_out, words);
     return cudaGetLastError();
 }

@@ -50,7 +50,7 @@ def test_full_retrieval_every_target(xp, port, cuda):
             assert np.array_equal(np.bitwise_xor.reduce(ans, axis=0), db.reshape(N, S)[beta])
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 6, 7, 9])
+@pytest.mark.parametrize("kernel", [1, 2, 7, 9])
 @pytest.mark.parametrize("N,S,B", [
     (8, 128, 1), (9, 128, 3), (1000, 256, 97), (1024, 4096, 64), (777, 512, 130),
     (4096, 128, 1), (2048, 1024, 513), (4000, 2048, 1025), (256, 32768, 40), (12345, 128, 300),
