@@ -219,6 +219,9 @@ struct xpir_table {
     DevBuf in_b1, in_b2, in_payload, in_reports, gather, chk, in_pack;
     PinnedBuf stage;              // host inputs of xpir_table_insert_batch, packed for one H2D
     PinnedBuf state_h;            // pinned mirror of the walk state (async H2D / D2H)
+    cudaGraphExec_t g1 = nullptr; // one host write as a graph (xpir_table_insert_batch, n = 1)
+    PinnedBuf g1_stage;           // its packed write + report, pinned
+    DevBuf g1_dev;                //   and on device
     bool walked = false;          // a walk kernel ran this batch (pre-existing items may have moved)
     bool async_pending = false;   // xpir_table_insert_batch_async issued, xpir_table_finish not yet called
     struct {

@@ -30,6 +30,10 @@ static void table_free_all(xpir_table* t) {
     t->in_pack.release();
     t->stage.release();
     t->state_h.release();
+    if (t->g1) cudaGraphExecDestroy(t->g1);
+    t->g1 = nullptr;
+    t->g1_stage.release();
+    t->g1_dev.release();
     t->par.release();
     if (t->stream) cudaStreamDestroy(t->stream);
 }
@@ -129,8 +133,33 @@ static int sync_state(xpir_table* t, cudaStream_t s) {
     XCK(cudaMemcpyAsync(t->state_h.p, t->dstate, sizeof(CuckooState), cudaMemcpyDeviceToHost, s));
     XCK(cudaStreamSynchronize(s));
     std::memcpy(&t->h, t->state_h.p, sizeof(CuckooState));
-    t->state_on_device = false;
-    if (t->h.status == 2) return fail(XPIR_ESTATE, "table_insert: FIFO ring overflow");
+    t->state_on_device = false;  // status 1 (draws) / 2 (FIFO ring full): the caller resumes the walk
+    return XPIR_OK;
+}
+
+// The FIFO ring (stamp -> slot, replacing the reference's std::map, cuckoo.hpp:79)
+// holds the stamps [fifo_head, next_stamp); live items that are never GC'd keep
+// fifo_head back while stamps grow (capacity == slots with failing chains), so the
+// ring doubles and is refilled from the live slots instead of failing.
+static int grow_fifo(xpir_table* t, cudaStream_t s) {
+    uint64_t cap = t->d.fifo_cap * 2;
+    while (t->h.next_stamp + 4096 - t->h.fifo_head >= cap) cap *= 2;
+    int64_t* ring = nullptr;
+    XCK(cudaStreamSynchronize(s));
+    XCK(cudaMalloc(&ring, cap * 8));
+    cudaError_t e = launch_fifo_rebuild(t->d, ring, cap, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        cudaFree(ring);
+        XCK(e);
+    }
+    cudaFree(t->d.fifo);
+    t->d.fifo = ring;
+    t->d.fifo_cap = cap;
+    if (t->g1) {  // the single-write graph holds the old ring in its kernel parameters
+        cudaGraphExecDestroy(t->g1);
+        t->g1 = nullptr;
+    }
     return XPIR_OK;
 }
 
@@ -158,11 +187,14 @@ static int walk_loop(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2, 
         t->walked = true;
         XCK(cudaMemcpyAsync(&t->h, t->dstate, sizeof(CuckooState), cudaMemcpyDeviceToHost, s));
         XCK(cudaStreamSynchronize(s));
-        if (t->h.status == 2) return fail(XPIR_ESTATE, "table_insert: FIFO ring overflow");
-        if (t->h.resume_at <= i && t->h.status != 1)
+        if (t->h.status == 2) {  // the FIFO ring is full: grow it, resume at the same insert
+            if (int rc = grow_fifo(t, s)) return rc;
+        } else if (t->h.resume_at <= i && t->h.status != 1) {
             return fail(XPIR_ESTATE, "table_insert: walk made no progress");
+        }
         i = t->h.resume_at;
         if (t->h.status == 1) t->h.draw_count = 0;  // force a refill
+        t->h.status = 0;
     }
     return XPIR_OK;
 }
@@ -202,9 +234,13 @@ static int finish_walk(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2
     if (rc) return rc;
     *n_ok = t->h.limit < n ? t->h.limit : n;
     t->h.limit = ~0ull;
-    if (t->h.status == 1) {
+    if (t->h.status == 1 || t->h.status == 2) {  // the walk paused (draws / FIFO ring): resume
+        if (t->h.status == 2) {
+            if (int rc2 = grow_fifo(t, s)) return rc2;
+        } else {
+            t->h.draw_count = 0;  // refill, then resume
+        }
         t->h.status = 0;
-        t->h.draw_count = 0;  // refill, then resume
         return walk_loop(t, d_b1, d_b2, t->h.resume_at, *n_ok, d_reports, s);
     }
     return push_state(t, s);  // the device copy stays authoritative
@@ -329,9 +365,13 @@ static int insert_impl(xpir_table* t, const uint32_t* d_b1, const uint32_t* d_b2
         t->h.limit = ~0ull;
         if (status == 0) {
             done = true;
-        } else if (status == 1) {  // the walk paused: refill and finish it from resume_at
+        } else if (status == 1 || status == 2) {  // the walk paused (draws / FIFO ring): resume it
             t->h.status = 0;
-            t->h.draw_count = 0;
+            if (status == 2) {
+                if ((rc = grow_fifo(t, s))) return rc;
+            } else {
+                t->h.draw_count = 0;
+            }
             if ((rc = walk_loop(t, d_b1, d_b2, t->h.resume_at, *n_ok, d_reports, s))) return rc;
         } else {  // 3: gather staging too small; the walk is complete
             t->h.status = 0;
@@ -414,8 +454,12 @@ int xpir_table_finish(xpir_table* t, uint64_t* n_applied) {
     t->h.limit = ~0ull;
     t->h.status = 0;
     if (status != 0) {
-        if (status == 1) {  // the walk paused for draws: refill and finish it from resume_at
-            t->h.draw_count = 0;
+        if (status == 1 || status == 2) {  // the walk paused (draws / FIFO ring): resume it
+            if (status == 2) {
+                if ((rc = grow_fifo(t, s))) return rc;
+            } else {
+                t->h.draw_count = 0;
+            }
             if ((rc = walk_loop(t, a.b1, a.b2, t->h.resume_at, ok, a.reports, s))) return rc;
         }
         const ShardMap none{};
@@ -485,6 +529,95 @@ int xpir_table_shard(const xpir_table* t, uint32_t* lo, uint32_t* hi) {
     return XPIR_OK;
 }
 
+}  // extern "C"
+
+// One host write (ServerCore::apply_write through the drop-in) as a replayed CUDA
+// graph: [inputs H2D from the pinned stage, state H2D from the pinned mirror, the
+// global-map walk, payload gather, payload scatter, reports D2H, state D2H] —
+// one graph launch and one synchronisation per write instead of ~12 runtime
+// calls. Captured once per table (its buffers are fixed once reserved); the host
+// only packs the write, advances its state mirror and checks the result.
+static int insert_one_graph(xpir_table* t, uint32_t b1, uint32_t b2, const uint8_t* payload, uint32_t* report) {
+    cudaStream_t s = t->stream;
+    const uint64_t item = t->d.item;
+    const uint64_t o2 = 16, op = 32, orep = op + round16(item), total = orep + 16;
+    if (!t->g1) {
+        // fixed buffers: packed write + report (device and pinned), state mirror, gather staging
+        XCK(t->g1_stage.ensure(total));
+        XCK(t->g1_dev.ensure(total));
+        XCK(t->state_h.ensure(sizeof(CuckooState)));
+        XCK(t->gather.ensure(502 * item));
+        t->d.gather = t->gather.as<uint8_t>();
+        uint8_t* dp = t->g1_dev.as<uint8_t>();
+        cudaGraph_t graph = nullptr;
+        XCK(cudaStreamSynchronize(s));
+        XCK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        cudaError_t e = cudaMemcpyAsync(dp, t->g1_stage.p, orep, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(t->dstate, t->state_h.p, sizeof(CuckooState), cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = launch_cuckoo_walk(t->d, t->dstate, reinterpret_cast<const uint32_t*>(dp),
+                                   reinterpret_cast<const uint32_t*>(dp + o2), 0, 1,
+                                   reinterpret_cast<uint32_t*>(dp + orep), s);
+        const ShardMap none{};
+        if (e == cudaSuccess)
+            e = launch_cuckoo_gather_sharded(t->d, &t->h, t->lo, t->hi, t->data, none, s, t->dstate, 502, 502);
+        if (e == cudaSuccess)
+            e = launch_cuckoo_scatter_sharded(t->d, &t->h, t->lo, t->hi, t->data, dp + op, s, t->dstate, 502);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(t->g1_stage.p + orep, dp + orep, 16, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(t->state_h.p, t->dstate, sizeof(CuckooState), cudaMemcpyDeviceToHost, s);
+        const cudaError_t e2 = cudaStreamEndCapture(s, &graph);
+        if (e == cudaSuccess) e = e2;
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&t->g1, graph, 0);
+        if (graph) cudaGraphDestroy(graph);
+        if (e != cudaSuccess) {
+            t->g1 = nullptr;
+            cudaGetLastError();
+            return fail(XPIR_ECUDA, std::string("table_insert: single-write graph: ") + cudaGetErrorString(e));
+        }
+    }
+    std::memcpy(t->g1_stage.p, &b1, 4);
+    std::memcpy(t->g1_stage.p + o2, &b2, 4);
+    std::memcpy(t->g1_stage.p + op, payload, item);
+    // the batch starts on the host mirror (as walk_impl's small path), the graph
+    // pushes it, walks, moves the payloads and brings the state back
+    t->h.batch_id += 1;
+    t->h.n_touched = 0;
+    t->h.walked = 0;
+    t->h.limit = ~0ull;
+    t->h.status = 0;
+    t->walked = true;
+    int rc = refill_draws(t, 2048, s);
+    if (rc) return rc;
+    XCK(t->state_h.ensure(sizeof(CuckooState)));  // no earlier async copy still reads the mirror
+    std::memcpy(t->state_h.p, &t->h, sizeof(CuckooState));
+    XCK(cudaGraphLaunch(t->g1, s));
+    count_launches(3);
+    XCK(cudaStreamSynchronize(s));
+    std::memcpy(&t->h, t->state_h.p, sizeof(CuckooState));
+    if (t->h.status != 0) {  // the walk paused (draws / FIFO ring): finish on the host-driven path
+        const uint32_t st0 = t->h.status;
+        t->h.status = 0;
+        if (st0 == 2) {
+            if ((rc = grow_fifo(t, s))) return rc;
+        } else {
+            t->h.draw_count = 0;
+        }
+        uint8_t* dp = t->g1_dev.as<uint8_t>();
+        if ((rc = walk_loop(t, reinterpret_cast<const uint32_t*>(dp), reinterpret_cast<const uint32_t*>(dp + o2),
+                            t->h.resume_at, 1, reinterpret_cast<uint32_t*>(dp + orep), s)))
+            return rc;
+        const ShardMap none{};
+        if ((rc = gather_impl(t, none, s)) || (rc = scatter_impl(t, dp + op, s))) return rc;
+        XCK(cudaMemcpyAsync(t->g1_stage.p + orep, dp + orep, 16, cudaMemcpyDeviceToHost, s));
+        XCK(cudaStreamSynchronize(s));
+        if ((rc = push_state(t, s))) return rc;
+    }
+    if (report) std::memcpy(report, t->g1_stage.p + orep, 16);
+    return XPIR_OK;
+}
+
+extern "C" {
+
 int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b2,
                             const uint8_t* payload, uint64_t n, uint32_t* reports) {
     if (!t) return fail(XPIR_EINVAL, "table_insert: null table");
@@ -503,7 +636,9 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b
     std::lock_guard<std::mutex> lk(t->mu);
     DeviceGuard g(t->device);
     cudaStream_t s = t->stream;
-    if (ok > 0) {
+    if (ok == 1 && !t->state_on_device && 256 < t->slots() && walk_w_supported(t->d)) {
+        if (int rc = insert_one_graph(t, b1[0], b2[0], payload, reports)) return rc;
+    } else if (ok > 0) {
         // [beta1 | beta2 | payload | reports] packed: one pinned staging buffer, one H2D
         const uint64_t o2 = round16(4 * ok), op = o2 + round16(4 * ok), orep = op + round16(ok * t->d.item);
         const uint64_t total = orep + 16 * ok;

@@ -104,9 +104,13 @@ k_par_solve(CuckooDev d, CuckooState* st, uint64_t n, const uint32_t* __restrict
     volatile unsigned long long* vf = flags;
     const uint32_t NB = d.buckets;
     // the batch's starting state (read by every thread before thread 0 changes it)
-    const uint64_t live0 = st->live, next_stamp = st->next_stamp;
+    const uint64_t live0 = st->live, next_stamp = st->next_stamp, head = st->fifo_head;
     const uint32_t batch_id = st->batch_id + 1;
-    const uint64_t room = d.capacity > live0 ? d.capacity - live0 : 0;
+    // no FIFO GC within the prefix, and every new stamp must fit the FIFO ring
+    const uint64_t span = next_stamp - head;
+    const uint64_t ring_room = d.fifo_cap > span ? d.fifo_cap - span : 0;
+    uint64_t room = d.capacity > live0 ? d.capacity - live0 : 0;
+    if (room > ring_room) room = ring_room;
     // P0 (cnt and cur are all zero on entry)
     for (uint64_t i = tid; i < n; i += nthr) {
         const uint32_t x1 = b1[i], x2 = b2[i];

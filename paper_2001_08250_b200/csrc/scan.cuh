@@ -184,6 +184,8 @@ __device__ __forceinline__ bool walk_prologue(CuckooState* gst, uint64_t& i0, ui
     return true;
 }
 
+// refill a FIFO ring of `cap` entries (a power of two) from the live slots' stamps
+cudaError_t launch_fifo_rebuild(const CuckooDev& d, int64_t* ring, uint64_t cap, cudaStream_t s);
 cudaError_t launch_cuckoo_walk(const CuckooDev& d, CuckooState* st, const uint32_t* beta1,
                                const uint32_t* beta2, uint64_t i0, uint64_t n, uint32_t* reports,
                                cudaStream_t s);

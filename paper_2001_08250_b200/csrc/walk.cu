@@ -176,6 +176,16 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                     return false;
                 }
             }
+            // FIFO ring room for this insert's stamp, checked before any state changes
+            // (stamps of dead entries at the head never matter again: skip them); on
+            // overflow the host grows the ring and resumes at this insert
+            if (s.next_stamp - s.fifo_head >= d.fifo_cap) {
+                while (s.fifo_head < s.next_stamp && d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
+                if (s.next_stamp - s.fifo_head >= d.fifo_cap) {
+                    s.status = 2;
+                    return false;
+                }
+            }
             uint32_t stored = 0, dropped = 0, gc = 0, disp = 0;
             // both buckets' occupancy in one round trip, together with the FIFO head
             // reads below (re-read when the GC frees a slot)
@@ -188,15 +198,7 @@ k_cuckoo_walk_w(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 m1 = free_mask(b1);
                 m2 = free_mask(b2);
             }
-            const uint64_t stamp = s.next_stamp++;  // :71
-            // stamps of dead entries at the head never matter again: skip them
-            while (s.fifo_head < stamp && d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
-            if (stamp - s.fifo_head >= d.fifo_cap) {
-                s.writes--;
-                s.next_stamp--;
-                s.status = 2;
-                return false;
-            }
+            const uint64_t stamp = s.next_stamp++;  // :71 (ring room checked above)
             if (m1) m2 = 0;  // :73-84 (bucket 2 only when bucket 1 is full)
             if (m1 | m2) {
                 const uint32_t b = m1 ? b1 : b2;

@@ -439,6 +439,15 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                     return false;
                 }
             }
+            // FIFO ring room for this insert's stamp, checked before any state changes
+            if (s.next_stamp - s.fifo_head >= d.fifo_cap) {
+                drain();  // pending chains write FIFO entries
+                while (s.fifo_head < s.next_stamp && d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
+                if (s.next_stamp - s.fifo_head >= d.fifo_cap) {
+                    s.status = 2;
+                    return false;
+                }
+            }
             uint32_t dropped = 0, gc = 0, disp = 0;
             s.writes++;                     // :62
             if (s.live == d.capacity) {     // :64-69 FIFO GC of the oldest entry
@@ -457,17 +466,7 @@ k_cuckoo_walk_x(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __re
                 gc = 1;
                 __syncwarp();
             }
-            const uint64_t stamp = s.next_stamp++;  // :71
-            if (stamp - s.fifo_head >= d.fifo_cap) {  // dead entries at the head never matter again
-                drain();
-                while (s.fifo_head < stamp && d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
-            }
-            if (stamp - s.fifo_head >= d.fifo_cap) {
-                s.writes--;
-                s.next_stamp--;
-                s.status = 2;
-                return false;
-            }
+            const uint64_t stamp = s.next_stamp++;  // :71 (ring room checked above)
             const uint32_t m1 = free_mask(b1);  // :73-84
             const uint32_t m2 = m1 ? 0u : free_mask(b2);
             if (m1 | m2) {

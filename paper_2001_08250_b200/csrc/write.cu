@@ -9,6 +9,7 @@
 //   k_draws           DetRng::next_u64 of consecutive fill calls (rng.hpp:31-37)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -303,6 +304,15 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
                     *stop = 1;
                     break;
                 }
+                // FIFO ring room for this insert's stamp, before any state changes
+                if (s.next_stamp - s.fifo_head >= d.fifo_cap) {
+                    while (s.fifo_head < s.next_stamp && d.fifo[s.fifo_head & fmask] < 0) s.fifo_head++;
+                    if (s.next_stamp - s.fifo_head >= d.fifo_cap) {
+                        s.status = 2;
+                        *stop = 1;
+                        break;
+                    }
+                }
                 uint32_t stored = 0, dropped = 0, gc = 0, disp = 0;
                 s.writes++;                                 // :62
                 if (s.live == d.capacity) {                 // :64-69 FIFO GC of the oldest entry
@@ -310,12 +320,7 @@ k_cuckoo_walk(CuckooDev d, CuckooState* __restrict__ gst, const uint32_t* __rest
                     clear(uint32_t(d.fifo[s.fifo_head & fmask]));
                     gc = 1;
                 }
-                const uint64_t stamp = s.next_stamp++;     // :71
-                if (stamp - s.fifo_head >= d.fifo_cap) {
-                    s.status = 2;
-                    *stop = 1;
-                    break;
-                }
+                const uint64_t stamp = s.next_stamp++;     // :71 (ring room checked above)
                 int fs = free_slot(b1);                     // :73-84
                 if (fs >= 0) {
                     place(b1 * d.depth + fs, b1, b2, stamp, int64_t(i));
@@ -608,6 +613,21 @@ __global__ void k_absorb_all(const uint32_t* __restrict__ pos, uint64_t n, unsig
 cudaError_t launch_absorb_unchecked(const uint32_t* pos, uint64_t n, unsigned long long* words, cudaStream_t s) {
     if (!n) return cudaSuccess;
     k_absorb_all<<<uint32_t((n + 255) / 256), 256, 0, s>>>(pos, n, words);
+    return cudaGetLastError();
+}
+
+// FIFO ring growth: every live slot re-entered at stamp & (new_cap - 1)
+__global__ void k_fifo_rebuild(CuckooDev d, int64_t* __restrict__ ring, uint64_t cap_mask) {
+    const uint64_t slots = uint64_t(d.buckets) * d.depth;
+    for (uint64_t f = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; f < slots; f += uint64_t(gridDim.x) * blockDim.x)
+        if (d.used[f]) ring[d.stamp[f] & cap_mask] = int64_t(f);
+}
+
+cudaError_t launch_fifo_rebuild(const CuckooDev& d, int64_t* ring, uint64_t cap, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(ring, 0xff, cap * 8, s);  // -1: no entry
+    if (e != cudaSuccess) return e;
+    const uint64_t slots = uint64_t(d.buckets) * d.depth;
+    k_fifo_rebuild<<<uint32_t(std::min<uint64_t>((slots + 255) / 256, 148 * 8)), 256, 0, s>>>(d, ring, cap - 1);
     return cudaGetLastError();
 }
 

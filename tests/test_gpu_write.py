@@ -322,3 +322,34 @@ def test_payload_shards_match_whole_table(xp, port, cuda, G, nb, depth, item, lo
         shards[0].state_digest()  # needs the whole table
     with pytest.raises(xp.InvalidArgument):
         shards[0].insert_batch([0], [0], np.zeros(item, np.uint8))  # the one-call path is whole-table only
+
+
+@pytest.mark.parametrize("single", [False, True])
+def test_fifo_ring_grows_instead_of_failing(xp, port, cuda, single):
+    """with capacity == buckets*depth, failing eviction chains keep live
+    below capacity, so FIFO GC never runs while old items in untouched buckets stay
+    live and stamps keep growing past the ring (2,048 entries for 128 slots). The
+    reference's std::map keeps going; the device ring now doubles and is refilled
+    from the live slots (bit-exact vs the oracle throughout)."""
+    nb, depth, item = 32, 4, 8
+    cap = nb * depth
+    g = np.random.default_rng(99 + single)
+    seed = g.integers(0, 256, 32, dtype=np.uint8).tobytes()
+    T, P = xp.Table(nb, depth, cap, item, seed), port.table(nb, depth, cap, item, seed)
+    b1 = g.integers(0, nb, cap).astype(np.uint32)
+    b2 = g.integers(0, nb, cap).astype(np.uint32)
+    pl = g.integers(0, 256, (cap, item), dtype=np.uint8)
+    assert np.array_equal(T.insert_batch(b1, b2, pl), P.insert_batch(b1, b2, pl))
+    n = 2600  # > 2,048 stamps while buckets 8..31 keep their first items
+    b1 = g.integers(0, 8, n).astype(np.uint32)
+    b2 = g.integers(0, 8, n).astype(np.uint32)
+    pl = g.integers(0, 256, (n, item), dtype=np.uint8)
+    step = 1 if single else 200
+    for a in range(0, n, step):
+        if single and a % 100:
+            T.insert_batch(b1[a:a + 1], b2[a:a + 1], pl[a:a + 1])
+            P.insert_batch(b1[a:a + 1], b2[a:a + 1], pl[a:a + 1])
+            continue
+        assert np.array_equal(T.insert_batch(b1[a:a + step], b2[a:a + step], pl[a:a + step]),
+                              P.insert_batch(b1[a:a + step], b2[a:a + step], pl[a:a + step])), a
+    assert T.state_digest() == P.state_digest()
