@@ -15,7 +15,7 @@ Prints ONE JSON line on rank 0 (bench contract in the task statement):
   value        whole-job requests/s with seeds + store resident in HBM
   e2e          the same metric through the C-ABI host call xpir_answer_batch_seeded
                (host seeds in, host answers out, copies inside the timed region)
-  roofline     dominant kernel k_scan_m4rm vs the dense-LOP3 ALU bound
+  roofline     dominant kernel (k_scan_m4rm_q9 at config 4) vs the dense-LOP3 ALU bound
   cpu_baseline the reference's pir::answer_batch (oracle/_ref) on the host cores
 """
 from __future__ import annotations
@@ -212,8 +212,8 @@ def traffic_from_profile(n_buckets, batch, world, kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
     kernel from the committed ncu capture of this same workload (profiles/),
     or None when the capture does not match the configuration being run."""
-    name = {5: "m4rm_tmem", 8: "m4rm_q"}.get(kernel)
-    path = os.path.join(ROOT, "profiles", f"r01_traffic_{name}.json")
+    name = {5: "r01_traffic_m4rm_tmem", 8: "r02_traffic_m4rm_q9"}.get(kernel)
+    path = os.path.join(ROOT, "profiles", f"{name}.json")
     if name is None or world != 1 or n_buckets != 1 << 20 or batch != BATCH or not os.path.exists(path):
         return None
     with open(path) as f:
@@ -405,7 +405,7 @@ def main():
                "d2h_bytes_per_step": (r1 - r0) * BUCKET_BYTES * world,
                "path": "per-rank seeds H2D + owned answer rows D2H"}
 
-    # roofline of the dominant kernel (k_scan_m4rm) on this rank's shard
+    # roofline of the dominant kernel (k_scan_m4rm_q9 at config 4) on this rank's shard
     peaks = xp.measure_peaks(local)
     nb = hi - lo
     per_launch_ms = scan_ms / max(scan_launches, 1)
@@ -419,29 +419,36 @@ def main():
             peak_src = "MEASURED_PEAKS.json"
     except Exception:
         peak_src = "fallback 6545 GB/s"
-    lookups = B * (nb // 8) * (BUCKET_BYTES // 4)  # M4RM: one 4-byte table word per (request, group, word)
+    kernel = xp.last_scan_kernel()
+    # shared-memory lookup bytes of the table kernel that ran: 32 B per (request,
+    # table, 32-byte column); kernel 8's tables cover 9 buckets (2 sets of 4 tables
+    # per 72 buckets), the byte tables 8
+    n_tables = 8 * ((nb + 71) // 72) if kernel == 8 else nb // 8
+    lookup_bytes = B * n_tables * BUCKET_BYTES
     roof = {
         "bound": "alu",
         "kernel": {1: "k_scan_direct", 2: "k_scan_m4rm", 5: "k_scan_m4rm_tmem",
-                   7: "k_scan_m4rm4", 8: "k_scan_m4rm_q", 9: "k_scan_m4rm6"}.get(xp.last_scan_kernel(), "?"),
+                   7: "k_scan_m4rm4", 8: "k_scan_m4rm_q9", 9: "k_scan_m4rm6"}.get(kernel, "?"),
         "unit": "Tops/s (32-bit masked-XOR lane ops)",
         "achieved": achieved / 1e12,
         "peak": peaks["lop3_per_s"] / 1e12,
         "frac": achieved / peaks["lop3_per_s"],
         "peak_source": "measured live: k_lop3_peak (acc ^= w & m, 148 SMs)",
-        "traffic": traffic_from_profile(N_BUCKETS, B, world, xp.last_scan_kernel()),
+        "traffic": traffic_from_profile(N_BUCKETS, B, world, kernel),
         "algorithmic_ops_per_launch": work_lop3,
         "launch_ms": per_launch_ms,
-        "note": ("W = B*N_g*S/4 dense GF(2) select-XOR ops; the M4RM kernel does B*N_g*S/32 table "
-                 "lookups instead (8 buckets per lookup), so frac > 1 is expected and is not a "
-                 "measurement error; smem_bound below is the ceiling of the algorithm actually run"),
-        "smem_bound": {"achieved_GBps": lookups * 4 / (per_launch_ms * 1e-3) / 1e9,
+        "note": ("W = B*N_g*S/4 dense GF(2) select-XOR ops; the M4RM kernel does one 32-byte table "
+                 "lookup per (request, 9 buckets, 32-byte column) instead (8 buckets for the byte-table "
+                 "kernels), so frac > 1 is expected and is not a measurement error; smem_bound below "
+                 "is the ceiling of the algorithm actually run"),
+        "smem_bound": {"achieved_GBps": lookup_bytes / (per_launch_ms * 1e-3) / 1e9,
                        "peak_GBps": peaks["smem_bytes_per_s"] / 1e9,
-                       "frac": lookups * 4 / (per_launch_ms * 1e-3) / peaks["smem_bytes_per_s"]},
+                       "frac": lookup_bytes / (per_launch_ms * 1e-3) / peaks["smem_bytes_per_s"],
+                       "lookup_bytes_per_launch": lookup_bytes},
         "hbm": {"achieved_GBps": hbm_bytes / (per_launch_ms * 1e-3) / 1e9, "peak_GBps": hbm_peak,
                 "peak_source": peak_src, "frac": hbm_bytes / (per_launch_ms * 1e-3) / 1e9 / hbm_peak,
                 "bytes_per_launch": hbm_bytes},
-        "traffic_source": "profiles/r01_traffic_<kernel>.json (ncu dram__bytes_read+write of this kernel "
+        "traffic_source": "profiles/r0N_traffic_<kernel>.json (ncu dram__bytes_read+write of this kernel "
                           "on this workload; algorithmic bytes per launch = hbm.bytes_per_launch)",
         "kernel_share_of_step": (scan_ms / args.steps) / ms_per_step,
     }

@@ -360,7 +360,7 @@ static int choose_kernel(const xpir_store* st, uint32_t B) {
     }
     if (k == 6) k = 1;  // (the warp-private nibble kernel was retired in round 2)
     if ((k == 2 || k == 7 || k == 9) && !m4_ok) k = 1;
-    if (k == 8 && !q_ok) k = 1;
+    if ((k == 8 ) && !q_ok) k = 1;
     return k;
 }
 
@@ -374,7 +374,7 @@ static int run_m4(xpir_store* st, const uint8_t* qT, uint64_t qstride, uint32_t 
     }
     M4Args a{st->data, st->nb(), st->S, qT, qstride, B, d_out, s};
     cudaEvent_t ev;
-    if (kernel == 8) {  // quad-interleaved 32-byte-column tables, full-TMEM accumulators
+    if (kernel == 8) {  // quad-interleaved 9-bucket tables, full-TMEM accumulators
         timing_begin(s, &ev);
         XCK(launch_scan_m4rm_q(a, num_sms(st->device)));
         timing_end(s, ev);
@@ -436,11 +436,11 @@ static int scan_rows(xpir_store* st, const uint8_t* rows, uint64_t stride, uint3
     if (B == 0) return XPIR_OK;
     const int k = choose_kernel(st, B);
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
-    if (k != 2 && k != 7 && k != 8 && k != 9) return run_rows(st, k, rows + blo, stride, B, d_out, s);
+    if (k != 2 && k != 7 && k != 8 && k != 9 && k != 10) return run_rows(st, k, rows + blo, stride, B, d_out, s);
     const uint64_t qs = m4rm_qstride(B);
     DevBuf& qw = st->qwin_for(s);
     XCK(qw.ensure(m4rm_qrows(nbw) * qs));
-    XCK(launch_transpose_q(rows, stride, blo, nbw, B, qw.as<uint8_t>(), qs, s, k == 8));
+    XCK(launch_transpose_q(rows, stride, blo, nbw, B, qw.as<uint8_t>(), qs, s, m4rm_layout(k)));
     count_launches(1);
     return run_m4(st, qw.as<uint8_t>(), qs, B, d_out, s, k);
 }
@@ -476,7 +476,7 @@ int xpir_answer_batch_seeded_dev(xpir_store* st, const uint8_t* d_seeds, uint32_
         const uint64_t qs = m4rm_qstride(B);
         DevBuf& qw = st->qwin_for(s);
         XCK(qw.ensure(m4rm_qrows(nbw) * qs));
-        XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s, k == 8));
+        XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s, m4rm_layout(k)));
         count_launches(1);
         return run_m4(st, qw.as<uint8_t>(), qs, B, d_out, s, k);
     }
@@ -520,7 +520,7 @@ int xpir_answer_batch(xpir_store* st, const uint8_t* q, uint64_t q_stride, uint3
     if (k == 2 || k == 7 || k == 8 || k == 9) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
-        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s, k == 8));
+        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s, m4rm_layout(k)));
         count_launches(1);
         rc = run_m4(st, st->qwin.as<uint8_t>(), qs, B, dout, s, k);
     } else {
@@ -588,7 +588,7 @@ int xpir_answer_batch_mixed(xpir_store* st, uint32_t B, const uint8_t* is_seed, 
     if (k == 2 || k == 7 || k == 8 || k == 9) {
         const uint64_t qs = m4rm_qstride(B);
         XCK(st->qwin.ensure(m4rm_qrows(nbw) * qs));
-        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s, k == 8));
+        XCK(launch_transpose_q(st->q.as<uint8_t>(), ws, 0, nbw, B, st->qwin.as<uint8_t>(), qs, s, m4rm_layout(k)));
         count_launches(1);
         rc = run_m4(st, st->qwin.as<uint8_t>(), qs, B, dout, s, k);
     } else {
@@ -654,7 +654,7 @@ int xpir_answer_batch_seeded_peer_dev(xpir_store* st, const uint8_t* d_seeds, ui
     XCK(zeroed(st->peer_stats, 16));
     DevBuf& qw = st->qwin_for(s);
     XCK(qw.ensure(m4rm_qrows(nbw) * qs));
-    XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s, true));  // the fused path always runs kernel 8
+    XCK(launch_expand_T(d_seeds, B, blo, nbw, qw.as<uint8_t>(), qs, s, m4rm_layout(8)));  // the fused path always runs kernel 8
     M4Args a{st->data, st->nb(), st->S, qw.as<uint8_t>(), qs, B, out_ptrs[0], s};
     a.peers.n = n_ranks;
     a.peers.self = self_rank;

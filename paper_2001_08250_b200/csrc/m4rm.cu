@@ -234,16 +234,19 @@ k_scan_m4rm(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8
 //   so each of the 64 byte stores per thread is a coalesced 32-byte warp store.
 // k_transpose_q: rows q[r*q_stride + byte_lo + k] -> qT (32x32 smem tiles).
 // ---------------------------------------------------------------------------
-// set4: the set-interleaved layout of k_scan_m4rm_q instead — byte k of request r
-// at (k >> 2) * 4 * qstride + 4 r + (k & 3), i.e. the four query bytes of a set
-// of four groups are one 32-bit word per request.
-__device__ __forceinline__ uint64_t qidx(uint64_t k, uint32_t r, uint64_t qstride, bool set4) {
-    return set4 ? (k >> 2) * 4 * qstride + uint64_t(r) * 4 + (k & 3) : k * qstride + r;
+// layout 2 (k_scan_m4rm_q9, kernel 8): byte k = 9p + b of pair p; b < 8 goes to
+// byte b & 3 of the 32-bit word of set 2p + b/4 (one word per request and set,
+// [set][request]), b = 8 (the pair's ninth index bits) to the plane after the
+// words: hi_off + p * qstride + r.
+__device__ __forceinline__ uint64_t qidx(uint64_t k, uint32_t r, uint64_t qstride, int layout, uint64_t hi_off) {
+    if (layout == 0) return k * qstride + r;
+    const uint64_t p = k / 9, b = k - 9 * p;
+    return b < 8 ? (2 * p + (b >> 2)) * 4 * qstride + uint64_t(r) * 4 + (b & 3) : hi_off + p * qstride + r;
 }
 
 __global__ void __launch_bounds__(128)
 k_expand_T(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
-           uint8_t* __restrict__ qT, uint64_t qstride, bool set4) {
+           uint8_t* __restrict__ qT, uint64_t qstride, int layout, uint64_t hi_off) {
     const uint64_t blk_lo = byte_lo / 64;
     const uint64_t nblk = (byte_lo + nbytes + 63) / 64 - blk_lo;
     const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -257,22 +260,76 @@ k_expand_T(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t byte_lo, uint
     uint32_t ks[16];
     chacha20_block(key, blk, ks);
     const int64_t base = int64_t(blk * 64) - int64_t(byte_lo);
-    if (set4 && (base & 3) == 0 && base >= 0 && uint64_t(base) + 64 <= nbytes) {
-        // 16 whole sets: one coalesced 32-bit store each
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-            *reinterpret_cast<uint32_t*>(qT + qidx(uint64_t(base) + 4 * j, r, qstride, true)) = ks[j];
-        return;
-    }
 #pragma unroll
     for (int j = 0; j < 64; ++j) {
         const int64_t k = base + j;
-        if (k >= 0 && uint64_t(k) < nbytes) qT[qidx(uint64_t(k), r, qstride, set4)] = uint8_t(ks[j >> 2] >> (8 * (j & 3)));
+        if (k >= 0 && uint64_t(k) < nbytes)
+            qT[qidx(uint64_t(k), r, qstride, layout, hi_off)] = uint8_t(ks[j >> 2] >> (8 * (j & 3)));
+    }
+}
+
+// Layout 2 straight from the keystream: a thread owns request r and a chunk of
+// 576 window bytes (64 pairs = 9 ChaCha blocks, the period where pairs and blocks
+// realign). Whole chunks of a 64-byte-aligned window write each set's 32-bit word
+// with one funnel shift (the word straddling a block boundary takes the previous
+// block's last word) and each pair's ninth-bit byte; the rest go byte by byte.
+__global__ void __launch_bounds__(128)
+k_expand_q9(const uint8_t* __restrict__ seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
+            uint8_t* __restrict__ qT, uint64_t qstride, uint64_t hi_off) {
+    const uint64_t nch = (nbytes + 575) / 576;
+    const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t Bp = (B + 31) & ~31u;
+    if (t >= Bp * nch) return;
+    const uint64_t c = t / Bp;
+    const uint32_t r = uint32_t(t - c * Bp);
+    if (r >= B) return;
+    ChaChaKey key = chacha_key(seeds + uint64_t(r) * 32, 0);
+    const uint64_t k0 = 576 * c;
+    if ((byte_lo & 63) == 0 && k0 + 576 <= nbytes) {
+        const uint64_t blk0 = (byte_lo + k0) / 64;
+        uint8_t* const lo_base = qT + uint64_t(128 * c) * 4 * qstride + uint64_t(r) * 4;
+        uint8_t* const hi_base = qT + hi_off + uint64_t(64 * c) * qstride + r;
+        uint32_t prev = 0;
+#pragma unroll
+        for (int b = 0; b < 9; ++b) {
+            uint32_t ks[16];
+            chacha20_block(key, blk0 + b, ks);
+#pragma unroll
+            for (int s = 0; s < 128; ++s) {
+                const int o = 9 * (s >> 1) + 4 * (s & 1), w = o >> 2, sh = 8 * (o & 3);
+                const int wl = w + (sh ? 1 : 0);  // last keystream word the set needs
+                if (wl / 16 != b) continue;
+                const uint32_t a = (w / 16 == b) ? ks[w & 15] : prev;
+                const uint32_t v = sh ? __funnelshift_r(a, ks[wl & 15], sh) : a;
+                *reinterpret_cast<uint32_t*>(lo_base + uint64_t(s) * 4 * qstride) = v;
+            }
+#pragma unroll
+            for (int p = 0; p < 64; ++p) {
+                const int o = 9 * p + 8, w = o >> 2;
+                if (w / 16 != b) continue;
+                hi_base[uint64_t(p) * qstride] = uint8_t(ks[w & 15] >> (8 * (o & 3)));
+            }
+            prev = ks[15];
+        }
+        return;
+    }
+    const uint64_t k1 = k0 + 576 < nbytes ? k0 + 576 : nbytes;
+    for (uint64_t blk = (byte_lo + k0) / 64; blk * 64 < byte_lo + k1; ++blk) {
+        uint32_t ks[16];
+        chacha20_block(key, blk, ks);
+        const int64_t base = int64_t(blk * 64) - int64_t(byte_lo);
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+            const int64_t k = base + j;
+            if (k >= int64_t(k0) && uint64_t(k) < k1)
+                qT[qidx(uint64_t(k), r, qstride, 2, hi_off)] = uint8_t(ks[j >> 2] >> (8 * (j & 3)));
+        }
     }
 }
 
 __global__ void k_transpose_q(const uint8_t* __restrict__ q, uint64_t q_stride, uint64_t byte_lo,
-                              uint64_t nbytes, uint32_t B, uint8_t* __restrict__ qT, uint64_t qstride, bool set4) {
+                              uint64_t nbytes, uint32_t B, uint8_t* __restrict__ qT, uint64_t qstride, int layout,
+                              uint64_t hi_off) {
     __shared__ uint8_t tile[32][33];
     const uint64_t k0 = uint64_t(blockIdx.x) * 32;  // byte (group) tile
     const uint32_t r0 = blockIdx.y * 32;            // request tile
@@ -285,7 +342,7 @@ __global__ void k_transpose_q(const uint8_t* __restrict__ q, uint64_t q_stride, 
     for (int y = threadIdx.y; y < 32; y += blockDim.y) {
         const uint64_t k = k0 + y;
         const uint32_t r = r0 + threadIdx.x;
-        if (k < nbytes && r < B) qT[qidx(k, r, qstride, set4)] = tile[threadIdx.x][y];
+        if (k < nbytes && r < B) qT[qidx(k, r, qstride, layout, hi_off)] = tile[threadIdx.x][y];
     }
 }
 
@@ -322,22 +379,39 @@ uint64_t m4rm_qstride(uint32_t B) { return (uint64_t(B) + 15) & ~uint64_t(15); }
 // chunks of the nibble kernel, the 12-byte chunks of the 6-bucket kernel and
 // the 4-byte sets of the quad kernel (rows past the vector are never selected:
 // they map to zero-filled buckets)
-uint64_t m4rm_qrows(uint64_t n_groups) { return (n_groups + 47) / 48 * 48; }
+uint64_t m4rm_qrows(uint64_t n_groups) {
+    const uint64_t r48 = (n_groups + 47) / 48 * 48;
+    const uint64_t r9 = (n_groups + 8) / 9 * 9;  // layout 2: whole pairs
+    return r48 > r9 ? r48 : r9;
+}
+
+static uint64_t hi_offset(int layout, uint64_t nbytes, uint64_t qstride) {
+    return layout == 2 ? (nbytes + 8) / 9 * 8 * qstride : 0;
+}
 
 cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
-                            uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4) {
+                            uint8_t* qT, uint64_t qstride, cudaStream_t s, int layout) {
+    if (layout == 2) {
+        const uint64_t n = uint64_t((B + 31) & ~31u) * ((nbytes + 575) / 576);
+        if (n == 0) return cudaSuccess;
+        k_expand_q9<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qT, qstride,
+                                                               hi_offset(layout, nbytes, qstride));
+        return cudaGetLastError();
+    }
     const uint64_t nblk = (byte_lo + nbytes + 63) / 64 - byte_lo / 64;
     const uint64_t n = uint64_t((B + 31) & ~31u) * nblk;
     if (n == 0) return cudaSuccess;
-    k_expand_T<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qT, qstride, set4);
+    k_expand_T<<<uint32_t((n + 127) / 128), 128, 0, s>>>(seeds, B, byte_lo, nbytes, qT, qstride, layout,
+                                                          hi_offset(layout, nbytes, qstride));
     return cudaGetLastError();
 }
 
 cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
-                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4) {
+                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s, int layout) {
     if (!B || !nbytes) return cudaSuccess;
     dim3 grid(uint32_t((nbytes + 31) / 32), (B + 31) / 32);
-    k_transpose_q<<<grid, dim3(32, 8), 0, s>>>(q, q_stride, byte_lo, nbytes, B, qT, qstride, set4);
+    k_transpose_q<<<grid, dim3(32, 8), 0, s>>>(q, q_stride, byte_lo, nbytes, B, qT, qstride, layout,
+                                               hi_offset(layout, nbytes, qstride));
     return cudaGetLastError();
 }
 

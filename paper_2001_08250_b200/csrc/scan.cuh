@@ -25,7 +25,7 @@ struct ScanArgs {
 // Fused cross-GPU reduction target: answer row r belongs to the rank g with
 // bound[g] <= r < bound[g+1]; every rank's buffer holds all B rows at the same
 // offsets (only the owner's rows are meaningful). n == 0: no peers.
-// Fused cross-GPU reduce of the quad-table scan (m4rm_q.cu): rank g owns answer
+// Fused cross-GPU reduce of the quad-table scan (m4rm_q9.cu): rank g owns answer
 // rows [bound[g], bound[g+1]) in its buffer ptr[g] (CUDA-IPC peer pointers).
 // Segment partials of one (request tile, column tile) accumulate in this GPU's
 // `partial` buffer; the last segment to arrive (tile_cnt) pushes the tile's rows
@@ -62,19 +62,24 @@ struct M4Args {
 };
 cudaError_t launch_scan_m4rm(const M4Args& a, int ctas_per_sm, int num_sms, int variant);
 cudaError_t launch_scan_m4rm_tmem(const M4Args& a, int num_sms);
-// quad-interleaved 32-byte-column tables, full-TMEM accumulators (m4rm_q.cu); S % 32 == 0
+// quad-interleaved 9-bucket tables over 32-byte columns, full-TMEM accumulators
+// (m4rm_q9.cu, kernel 8); S % 32 == 0; queries in layout 2
 cudaError_t launch_scan_m4rm_q(const M4Args& a, int num_sms);
 int m4rm_q_tile(uint32_t B);
+uint64_t m4rm_q9_hi_offset(uint32_t nb, uint64_t qstride);
 double m4rm_q_cost(uint32_t B, int* tile);  // vs the half-TMEM kernel: ceil(B/2048)*2048/3.0
 cudaError_t launch_scan_m4rm4(const M4Args& a, int num_sms);  // nibble tables (m4rm4.cu)
 cudaError_t launch_scan_m4rm6(const M4Args& a, int num_sms);  // 6-bucket tables (m4rm6.cu)
 uint64_t m4rm_qstride(uint32_t B);
 uint64_t m4rm_qrows(uint64_t n_groups);  // rows to allocate (staging reads 16-row chunks)
-// set4 = true: the set-interleaved layout of k_scan_m4rm_q (kernel 8)
+// layout: see m4rm_layout below (k_expand_T runs k_expand_q9 for layout 2)
 cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, uint64_t nbytes,
-                            uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4 = false);
+                            uint8_t* qT, uint64_t qstride, cudaStream_t s, int layout = 0);
 cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
-                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s, bool set4 = false);
+                               uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s, int layout = 0);
+// query layout each M4RM kernel reads: 0 group-major bytes (kernels 2/5/7/9),
+// 2 pairs of 9-bucket sets (kernel 8)
+inline int m4rm_layout(int kernel) { return kernel == 8 ? 2 : 0; }
 cudaError_t launch_scan_direct(const ScanArgs& a, int num_sms, uint32_t* nsplit_out);
 cudaError_t launch_scan_bytes(const ScanArgs& a);
 cudaError_t launch_init_out(uint8_t* out, uint32_t B, uint32_t S, const uint8_t* mask_seeds,
