@@ -156,6 +156,16 @@ typedef struct {
     int reserved[6];
 } xpir_scan_opts;
 int xpir_set_scan_opts(const xpir_scan_opts* o);
+/* How host threads wait for the device in this process (all devices): 0 = the
+   CUDA runtime's default (spin while there are more cores than contexts),
+   1 = spin, 2 = yield, 3 = blocking (threads sleep on an OS primitive). The
+   environment variable XPIR_SYNC = spin | yield | blocking sets it at the
+   library's first device call. Measured through the reference drop-ins
+   (profiles/r02_production_path.jsonl): blocking cuts the real-time cluster's
+   mean delivery latency (acceptance criterion 5's replay) from 776 to 590-611 ms
+   but makes every synchronous write 4-6x slower (ServerCore::apply_write
+   41 -> 178-267 us), so the default stays the runtime's. */
+int xpir_set_host_sync(int mode);
 /* Which kernel the last scan used (the ids above; 3 = byte-granular, 5 = M4RM half-TMEM). */
 int xpir_last_scan_kernel(void);
 /* When enabled, CUDA events bracket every scan-kernel launch on its own stream;

@@ -8,6 +8,8 @@
 //                                              server::answer_share on one sealed snapshot
 //   bench_read writes   capacity writes_per_seal epochs
 //                                              ServerCore::apply_write x k + seal_epoch (server.cpp:58-81)
+//   bench_read delivery                        acceptance.cpp criterion 5's first replay (replay.cpp:222):
+//                                              a real-time 3-server cluster, 8 chat users, 500 messages
 //
 // Each prints one JSON object per measurement on stdout.
 #include <atomic>
@@ -155,11 +157,46 @@ static int writes(int argc, char** argv) {
     return 0;
 }
 
+// The cluster and chat workload of acceptance criterion 5 (acceptance.cpp:247-290,
+// delivery_config), timed alone: wall-clock delivery latency through the nodes.
+static int delivery(int, char**) {
+    DetRng rng(555);
+    Config cfg = make_local_config(3, rng);
+    cfg.capacity_n = 4096;
+    cfg.depth_d = 4;
+    cfg.message_z = 256;
+    cfg.write_interval_ms = 200;
+    cfg.read_interval_ms = 100;
+    cfg.jitter_ms = 0;
+    cfg.get_updates_every = 2;
+    cfg.giv_rotate_writes = 16;
+    cfg.window_deltas = 100;
+    cfg.epoch_seal_writes = 64;
+    cfg.epoch_seal_interval_ms = 50;
+    cfg.rate_limit = false;
+    harness::ChatGenSpec spec;
+    spec.users = 8;
+    spec.channels = 1;
+    spec.messages = 500;
+    spec.interval_ms = 300;
+    spec.seed = 11;
+    auto msgs = harness::generate_chat(spec);
+    auto t0 = clk::now();
+    auto rep = harness::replay_workload(msgs, cfg, 7, 30000);
+    std::printf("{\"bench\": \"delivery\", \"delivered\": %zu, \"expected\": %zu, \"latency_mean_ms\": %.1f, "
+                "\"latency_p50_ms\": %.1f, \"latency_p95_ms\": %.1f, \"latency_max_ms\": %.1f, "
+                "\"server_reads_per_s\": %.1f, \"wall_s\": %.1f}\n",
+                rep.deliveries, rep.expected_deliveries, rep.latency_mean_ms, rep.latency_p50_ms,
+                rep.latency_p95_ms, rep.latency_max_ms, rep.server_reads_per_sec, since_us(t0) * 1e-6);
+    return 0;
+}
+
 int main(int argc, char** argv) {
     const std::string mode = argc > 1 ? argv[1] : "process";
     if (mode == "process") return process(argc, argv);
     if (mode == "concurrent") return concurrent(argc, argv);
     if (mode == "writes") return writes(argc, argv);
-    std::fprintf(stderr, "usage: bench_read process|concurrent|writes ...\n");
+    if (mode == "delivery") return delivery(argc, argv);
+    std::fprintf(stderr, "usage: bench_read process|concurrent|writes|delivery ...\n");
     return 2;
 }

@@ -72,6 +72,7 @@ _SIGS = {
     "xpir_version": ([], C.c_int),
     "xpir_launch_count": ([], C.c_uint64),
     "xpir_set_scan_opts": ([_vp], C.c_int),
+    "xpir_set_host_sync": ([C.c_int], C.c_int),
     "xpir_last_scan_kernel": ([], C.c_int),
     "xpir_scan_timing": ([C.c_int], C.c_int),
     "xpir_scan_timing_collect": ([C.POINTER(C.c_double), _u32p], C.c_int),

@@ -55,6 +55,14 @@ int xpir_set_scan_opts(const xpir_scan_opts* o) {
 }
 int xpir_last_scan_kernel(void) { return g_last_kernel.load(); }
 
+int xpir_set_host_sync(int mode) {
+    static const unsigned flags[4] = {cudaDeviceScheduleAuto, cudaDeviceScheduleSpin, cudaDeviceScheduleYield,
+                                      cudaDeviceScheduleBlockingSync};
+    if (mode < 0 || mode > 3) return fail(XPIR_EINVAL, "set_host_sync: mode 0..3");
+    set_sync_flags(flags[mode]);
+    return XPIR_OK;
+}
+
 }  // extern "C"
 
 // Scan-kernel event timing (bench.py's roofline.achieved denominator).

@@ -42,9 +42,35 @@ namespace capi {
             return fail(XPIR_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Host wait policy for this process's CUDA contexts (xpir_set_host_sync; the
+// environment variable XPIR_SYNC = spin | yield | blocking applies it once, at
+// the library's first device call).
+inline void set_sync_flags(unsigned f) {
+    int n = 0, cur = 0;
+    cudaGetDeviceCount(&n);
+    cudaGetDevice(&cur);
+    for (int d = 0; d < n; ++d) {
+        cudaSetDevice(d);
+        cudaSetDeviceFlags(f);
+    }
+    cudaSetDevice(cur);
+    cudaGetLastError();
+}
+inline bool apply_sync_policy() {
+    const char* e = getenv("XPIR_SYNC");
+    if (!e) return false;
+    set_sync_flags(!strcmp(e, "blocking") ? cudaDeviceScheduleBlockingSync
+                   : !strcmp(e, "yield")  ? cudaDeviceScheduleYield
+                   : !strcmp(e, "spin")   ? cudaDeviceScheduleSpin
+                                          : cudaDeviceScheduleAuto);
+    return true;
+}
+
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
+        static const bool policy = apply_sync_policy();
+        (void)policy;
         cudaGetDevice(&prev);
         if (prev != dev) cudaSetDevice(dev);
     }

@@ -7,6 +7,7 @@ for arm in b200 ref; do
   timeout 600 ./bench_read_$arm concurrent 100000 64 8 | sed "s/^{/{\"arm\": \"$arm\", /" >> $OUT
   timeout 600 ./bench_read_$arm writes 131072 500 8 | sed "s/^{/{\"arm\": \"$arm\", /" >> $OUT
   timeout 600 ./bench_read_$arm writes 32768 64 16 | sed "s/^{/{\"arm\": \"$arm\", /" >> $OUT
+  timeout 400 ./bench_read_$arm delivery | sed "s/^{/{\"arm\": \"$arm\", /" >> $OUT
 done
 echo "host: $(nproc) cores, $(grep -m1 'model name' /proc/cpuinfo)" >> ../../../gpurun_out/prod_path_host.txt
 timeout 1200 ./acceptance_b200 > ../../../gpurun_out/acceptance_b200.txt 2>&1
