@@ -346,6 +346,41 @@ __global__ void k_transpose_q(const uint8_t* __restrict__ q, uint64_t q_stride, 
     }
 }
 
+// Layout 2 from caller rows: a block transposes 32 pairs (288 query bytes) of 32
+// requests through shared memory and writes whole 32-bit set words (one coalesced
+// 128-byte store per set and warp) and the pairs' ninth-bit bytes. Row stride 292
+// bytes = 73 words: the column reads of the write phase are bank-conflict-free.
+__global__ void __launch_bounds__(256)
+k_transpose_q9(const uint8_t* __restrict__ q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes, uint32_t B,
+               uint8_t* __restrict__ qT, uint64_t qstride, uint64_t hi_off) {
+    __shared__ uint8_t tile[32][292];
+    const uint64_t k0 = uint64_t(blockIdx.x) * 288;
+    const uint32_t r0 = blockIdx.y * 32;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int idx = tid; idx < 32 * 288; idx += 256) {
+        const int row = idx / 288, k = idx - row * 288;
+        const uint32_t r = r0 + row;
+        tile[row][k] = (r < B && k0 + k < nbytes) ? q[uint64_t(r) * q_stride + byte_lo + k0 + k] : uint8_t(0);
+    }
+    __syncthreads();
+    const uint64_t n_pairs = (nbytes + 8) / 9;
+    const uint32_t tx = threadIdx.x, r = r0 + tx;
+    if (r >= B) return;
+    for (int s = threadIdx.y; s < 64; s += 8) {
+        const int c = 9 * (s >> 1) + 4 * (s & 1);
+        const uint64_t gp = uint64_t(blockIdx.x) * 32 + (s >> 1);
+        if (gp >= n_pairs) break;
+        const uint32_t w = uint32_t(tile[tx][c]) | uint32_t(tile[tx][c + 1]) << 8 | uint32_t(tile[tx][c + 2]) << 16 |
+                           uint32_t(tile[tx][c + 3]) << 24;
+        *reinterpret_cast<uint32_t*>(qT + (2 * gp + (s & 1)) * 4 * qstride + uint64_t(r) * 4) = w;
+    }
+    for (int p = threadIdx.y; p < 32; p += 8) {
+        const uint64_t gp = uint64_t(blockIdx.x) * 32 + p;
+        if (gp >= n_pairs) break;
+        qT[hi_off + gp * qstride + r] = tile[tx][9 * p + 8];
+    }
+}
+
 // ---------------------------------------------------------------------------
 template <int NT, int RPT>
 static cudaError_t launch_m4(const M4Args& a, int ctas_per_sm, int num_sms) {
@@ -409,6 +444,12 @@ cudaError_t launch_expand_T(const uint8_t* seeds, uint32_t B, uint64_t byte_lo, 
 cudaError_t launch_transpose_q(const uint8_t* q, uint64_t q_stride, uint64_t byte_lo, uint64_t nbytes,
                                uint32_t B, uint8_t* qT, uint64_t qstride, cudaStream_t s, int layout) {
     if (!B || !nbytes) return cudaSuccess;
+    if (layout == 2) {
+        dim3 grid9(uint32_t((nbytes + 287) / 288), (B + 31) / 32);
+        k_transpose_q9<<<grid9, dim3(32, 8), 0, s>>>(q, q_stride, byte_lo, nbytes, B, qT, qstride,
+                                                     hi_offset(layout, nbytes, qstride));
+        return cudaGetLastError();
+    }
     dim3 grid(uint32_t((nbytes + 31) / 32), (B + 31) / 32);
     k_transpose_q<<<grid, dim3(32, 8), 0, s>>>(q, q_stride, byte_lo, nbytes, B, qT, qstride, layout,
                                                hi_offset(layout, nbytes, qstride));

@@ -335,9 +335,11 @@ def test_m4rm_variants_match_oracle(xp, port, cuda, kernel, N, S, B):
     (64, 128, 6000), (5000, 160, 8192), (131, 4096, 9000), (100003, 32, 2049), (40, 32, 16385),
 ])
 def test_m4rm_quad_tables_match_oracle(xp, port, cuda, N, S, B):
-    """Quad-interleaved 32-byte-column tables with full-TMEM accumulators (8), forced
-    at any batch size: partial 2048/4096/8192-request tiles, bucket counts that end
-    mid-group and mid-set, bucket sizes that are multiples of 32 but not of 128."""
+    """Quad-interleaved 9-bucket tables over 32-byte columns with full-TMEM
+    accumulators (8), forced at any batch size: partial 2048/4096/8192-request
+    tiles, bucket counts that end mid-table, mid-set and mid-pair (72 buckets),
+    bucket sizes that are multiples of 32 but not of 128, caller rows through the
+    shared-memory layout-2 transposition (whole 288-byte tiles and a tail)."""
     g = np.random.default_rng(N * 5 + S + B)
     db = rand(g, N * S)
     q = rand(g, B, (N + 7) // 8)
