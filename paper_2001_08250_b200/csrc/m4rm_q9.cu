@@ -21,13 +21,14 @@
 //    ([pair][request] bytes, four requests per 32-bit load).
 //  * Four 512-row tables of a set interleave per 128-byte bank line exactly as in
 //    K1q (row x of table t at x*128 + 32t): one set = 64 KiB, double-buffered
-//    128 KiB, each buffer 64 KiB-aligned in the shared window so the ninth index
-//    bit is OR-ed into the address as bit 15 (one LOP3).
+//    128 KiB. The 9-bit index is one PRMT of the set word and the request's ninth
+//    bits spread to one byte per table (IMAD by 0x204081 + LOP3, once per
+//    request and set).
 //  * Shared-memory wavefronts per set (Rc = 8192): 8192 lookups + 512 table
 //    stores + 72 bucket-word reads + 256 + 32 index loads + ~10 staging fills
 //    = 9074 per 36 buckets, against K1q's 8776 per 32 buckets: 8% fewer per
-//    bucket. The index ALU work rises from 2 to 4 instructions per lookup
-//    (PRMT, IMAD, SHF, LOP3), well inside the ALU pipe's slack.
+//    bucket. The index costs what the byte tables' did (PRMT + IMAD per lookup)
+//    plus three instructions per request and set.
 //
 // Unchanged from the byte-table version:
 //  * One lane owns one request and its full 32-byte slice (two 16-byte halves).
@@ -70,10 +71,10 @@ constexpr int R_STG = 36 * 32;    // 36 buckets x 32 B per staged set
 template <int NQ>
 struct RCfg {
     static constexpr int RC = R_NT * 4 * NQ;  // requests per tile
-    // offsets from the 64 KiB-aligned base: two table buffers, staging ring, TMEM slot
+    // two table buffers, staging ring, TMEM slot
     static constexpr int OFF_STG = 2 * R_TAB;
     static constexpr int OFF_ADDR = OFF_STG + R_NST * R_STG;
-    static constexpr int SMEM = 65535 + OFF_ADDR + 16;  // + worst-case alignment slack
+    static constexpr int SMEM = OFF_ADDR + 16;
     static constexpr int TCOLS = 128 * NQ;
     static_assert(SMEM <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
@@ -142,10 +143,8 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
                uint32_t n_ctiles, uint32_t n_pairs, uint32_t n_seg, PeerOut peers) {
     using C = RCfg<NQ>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    const uint32_t sraw = smem_u32(smem);
-    const uint32_t skew = (65536u - (sraw & 65535u)) & 65535u;
-    const uint32_t sbase = sraw + skew;  // 64 KiB-aligned: table rows 256..511 set address bit 15
-    uint8_t* const sgen = smem + skew;
+    const uint32_t sbase = smem_u32(smem);
+    uint8_t* const sgen = smem;
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int i8 = lane & 7, lp = i8 >> 1;
@@ -162,16 +161,15 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
     const uint32_t tbase = *reinterpret_cast<const uint32_t*>(sgen + C::OFF_ADDR);
     const uint32_t tcol = tbase + (uint32_t((warp & 3) * 32) << 16) + uint32_t(warp >> 2) * (32 * NQ);
 
-    // lookup constants: step kk reads table t = (lp + kk) & 3, own half first; low
-    // index bits = byte t of the set word (PRMT 0x4440 | t), ninth bit = bit t of
-    // the request's nibble, shifted to bit 15 (<< (15 - t))
-    uint32_t toff[4], bsel[4], hsh[4];
+    // lookup constants: step kk reads table t = (lp + kk) & 3, own half first
+    uint32_t toff[4], bsel[4];
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {
         const uint32_t t = uint32_t(lp + kk) & 3u;
         toff[kk] = 32 * t + 16 * uint32_t(i8 & 1);
-        bsel[kk] = 0x4440u | t;
-        hsh[kk] = 15u - t;
+        // 9-bit index in one PRMT: byte 0 = low byte t of the set word, byte 1 =
+        // byte t of the spread ninth bits (0/1), bytes 2-3 = sign of that byte (0)
+        bsel[kk] = t | ((4u + t) << 4) | ((12u + t) << 8) | ((12u + t) << 12);
     }
     const uint32_t dhalf = (i8 & 1) ? 0xfffffff0u : 16u;
     // build constants: lane -> (table bt, 32-bit word bw); warp -> index bits 4..6
@@ -263,11 +261,14 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
                     const uint32_t ta = tcol + 8 * (4 * q + k);
                     uint32_t m[8];
                     tm_ld8(ta, m);
-                    const uint32_t hk = hq[q] >> (8 * k + hshift);
+                    // ninth bits of the request's four tables -> bytes 0..3 (bit t -> bit 8t)
+                    const uint32_t hx = (((hq[q] >> (8 * k + hshift)) & 15u) * 0x204081u) & 0x01010101u;
                     uint4 v0[4], v1[4];
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        const uint32_t a0 = (__byte_perm(wk[k], 0, bsel[kk]) * 128 + tk[kk]) | ((hk << hsh[kk]) & 0x8000u);
+                        uint32_t i9;  // PTX prmt (not __byte_perm): selector bit 3 = sign-replicate
+                        asm("prmt.b32 %0, %1, %2, %3;" : "=r"(i9) : "r"(wk[k]), "r"(hx), "r"(bsel[kk]));
+                        const uint32_t a0 = i9 * 128 + tk[kk];
                         v0[kk] = lds128(a0);
                         v1[kk] = lds128(a0 + dhalf);
                     }
