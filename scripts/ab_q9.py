@@ -1,4 +1,4 @@
-"""A/B of the 9-bucket quad-table kernel (10) against the quad-table kernel (8):
+"""A/B of the 9-bucket quad-table kernel, run while it was candidate kernel 10 (it replaced
 bit-exact on ragged shapes (row-major and seeded queries, shard windows), then
 per-launch time at config 4 (4 GiB, B = 8192) and a 1 GiB store."""
 import json

@@ -1,4 +1,4 @@
-# kernel 8 vs 10 vs 5 (half-TMEM byte tables) on a 1 GiB store at the batch sizes the
+# kernel 8 (then the byte-table quad kernel) vs candidate 10 (the 9-bucket tables, now kernel 8) vs 5 on a 1 GiB store at the batch sizes the
 # cost model routes to them
 for S in 512 1024 4096 8192; do
   N=$(( (1 << 30) / S ))
