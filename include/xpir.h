@@ -149,8 +149,9 @@ typedef struct {
     int kernel;        /* 0 = auto, 1 = direct select-XOR, 2 = M4RM byte tables (auto variant),
                           4 = M4RM register accumulators, 5 = M4RM half-TMEM accumulators,
                           7 = M4RM nibble tables,
-                          8 = M4RM quad-interleaved 32-byte-column tables with full-TMEM
-                              accumulators (auto for B >= 2048, S % 32 == 0),
+                          8 = M4RM 9-bucket tables, four interleaved per 32-byte column,
+                              full-TMEM accumulators (auto for B = 4096 and >= 8192,
+                              S % 32 == 0),
                           9 = M4RM 6-bucket tables (64 rows per 6 buckets) */
     int ctas_per_sm;   /* 0 = auto */
     int reserved[6];
