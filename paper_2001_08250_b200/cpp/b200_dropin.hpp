@@ -2,6 +2,7 @@
 // (pir_b200.cpp, server_b200.cpp). Not part of the reference's headers.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 
 #include "oblog/pir.hpp"
@@ -28,5 +29,14 @@ xpir_store* registered_store(const pir::Snapshot& snap);
 // read batcher (answer_share's server step, server.cpp:122-123): the scan and
 // the pad are fused, concurrent callers are coalesced into one batch.
 bytes answer_masked(const pir::Snapshot& snap, const pir::QueryVector& q, const crypto::Seed& seed);
+
+// Opt-in wall-clock trace of the drop-in entry points (XPIR_DROPIN_TRACE=1):
+// calls, total and max time per entry, printed to stderr at process exit.
+struct Trace {
+    explicit Trace(const char* name);
+    ~Trace();
+    const char* name;
+    std::chrono::steady_clock::time_point t0;
+};
 
 }  // namespace oblog::b200

@@ -23,6 +23,8 @@
 // read, from node.cpp's session and link threads concurrently) go through one
 // read batcher per snapshot geometry (xpir_batcher_*), so concurrent reads are
 // coalesced into one device scan; a lone caller is scanned at once.
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <list>
 #include <map>
@@ -37,6 +39,45 @@
 #include "xpir.h"
 
 namespace oblog::b200 {
+
+namespace {
+struct TraceStat {
+    uint64_t calls = 0;
+    double total_us = 0, max_us = 0;
+};
+struct TraceTable {
+    std::mutex mu;
+    std::map<std::string, TraceStat> stats;
+    ~TraceTable() {
+        if (stats.empty()) return;
+        std::fprintf(stderr, "drop-in trace: entry, calls, total ms, mean us, max us\n");
+        for (const auto& [k, v] : stats)
+            std::fprintf(stderr, "  %-28s %9llu %10.1f %9.1f %9.1f\n", k.c_str(), (unsigned long long)v.calls,
+                         v.total_us * 1e-3, v.total_us / double(v.calls), v.max_us);
+    }
+};
+TraceTable* trace_table() {
+    static const bool on = [] {
+        const char* e = std::getenv("XPIR_DROPIN_TRACE");
+        return e && *e && *e != '0';
+    }();
+    if (!on) return nullptr;
+    static TraceTable t;
+    return &t;
+}
+}  // namespace
+
+Trace::Trace(const char* n) : name(n), t0(std::chrono::steady_clock::now()) {}
+Trace::~Trace() {
+    TraceTable* t = trace_table();
+    if (!t) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    std::lock_guard<std::mutex> lk(t->mu);
+    TraceStat& st = t->stats[name];
+    st.calls += 1;
+    st.total_us += us;
+    if (us > st.max_us) st.max_us = us;
+}
 
 void check(int rc, const char* what) {
     if (rc == XPIR_OK) return;
@@ -197,6 +238,7 @@ xpir_store* registered_store(const pir::Snapshot& snap) {
 }
 
 bytes answer_masked(const pir::Snapshot& snap, const pir::QueryVector& q, const crypto::Seed& seed) {
+    Trace tr("pir.answer_masked");
     if (q.bit_count != snap.bucket_count) throw std::invalid_argument("answer: query length mismatch");
     return scan_one(snap, q, seed.data());
 }
@@ -226,6 +268,7 @@ std::vector<QueryVector> gen_queries(uint32_t beta, uint32_t bucket_count, uint3
 }
 
 std::vector<bytes> answer_batch(const Snapshot& snap, const std::vector<QueryVector>& qs) {
+    b200::Trace tr("pir.answer_batch");
     for (const QueryVector& q : qs)
         if (q.bit_count != snap.bucket_count) throw std::invalid_argument("answer_batch: query length mismatch");
     std::vector<bytes> out(qs.size(), bytes(snap.bucket_size, 0));
@@ -242,6 +285,7 @@ std::vector<bytes> answer_batch(const Snapshot& snap, const std::vector<QueryVec
 }
 
 bytes answer(const Snapshot& snap, const QueryVector& q) {
+    b200::Trace tr("pir.answer");
     if (q.bit_count != snap.bucket_count) throw std::invalid_argument("answer: query length mismatch");
     return scan_one(snap, q, nullptr);
 }

@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -54,6 +55,10 @@ struct CoreState {
     xpir_window* window = nullptr;
     uint32_t buckets = 0, bucket_size = 0;
     size_t item = 0;
+    // encoded frozen deltas by absolute delta number (Window::base() + index): a
+    // frozen delta never changes again, so each is encoded once, not at every freeze
+    std::mutex enc_mu;
+    std::map<uint64_t, bytes> enc_cache;
     CoreState() = default;
     CoreState(const CoreState&) = delete;
     CoreState& operator=(const CoreState&) = delete;
@@ -175,22 +180,32 @@ ServerCore::ServerCore(const Config& cfg, uint32_t index)
 }
 
 WindowFreeze ServerCore::make_freeze() const {  // server.cpp:45-56, from the device window
+    b200::Trace tr("server.make_freeze");
     auto cs = state_in(epochs_);
     WindowFreeze f;
     uint64_t count = 0;
     f.digest.resize(32);
     check(xpir_server_freeze(cs->sv, &f.base, &f.newest, f.digest.data(), &count), "server: freeze");
+    // deltas 0..count-1 are frozen (server.cpp:46-48); the reference re-encodes all
+    // of them every freeze, here only the ones not encoded before (one per rotation)
+    std::lock_guard<std::mutex> lk(cs->enc_mu);
+    cs->enc_cache.erase(cs->enc_cache.begin(), cs->enc_cache.lower_bound(f.base));
     for (uint64_t k = 0; k < count; ++k) {
-        uint64_t len = 0;
-        check(xpir_window_encode_delta(cs->window, k, nullptr, 0, &len), "server: encode_delta");
-        bytes enc(len);
-        check(xpir_window_encode_delta(cs->window, k, enc.data(), len, &len), "server: encode_delta");
-        f.deltas.push_back(std::move(enc));
+        auto it = cs->enc_cache.find(f.base + k);
+        if (it == cs->enc_cache.end()) {
+            uint64_t len = 0;
+            check(xpir_window_encode_delta(cs->window, k, nullptr, 0, &len), "server: encode_delta");
+            bytes enc(len);
+            check(xpir_window_encode_delta(cs->window, k, enc.data(), len, &len), "server: encode_delta");
+            it = cs->enc_cache.emplace(f.base + k, std::move(enc)).first;
+        }
+        f.deltas.push_back(it->second);
     }
     return f;
 }
 
 ServerCore::ApplyResult ServerCore::apply_write(const logproto::WriteRequest& w, bool seal_after) {
+    b200::Trace tr("server.apply_write");
     auto cs = state_in(epochs_);
     // server.cpp:60-61, then Table::insert's own size check (cuckoo.cpp:59-60)
     if (w.beta1 >= cs->buckets || w.beta2 >= cs->buckets)
@@ -218,6 +233,7 @@ ServerCore::ApplyResult ServerCore::apply_write(const logproto::WriteRequest& w,
 }
 
 uint64_t ServerCore::seal_epoch() {
+    b200::Trace tr("server.seal_epoch");
     auto cs = state_in(epochs_);
     // The epoch that falls off the ring (server.cpp:79) is released before the
     // device seal, so its image is re-sealed in place unless a reader still holds it.
@@ -234,6 +250,7 @@ uint64_t ServerCore::seal_epoch() {
 }
 
 std::shared_ptr<const pir::Snapshot> ServerCore::snapshot_at(uint64_t epoch) const {
+    b200::Trace tr("server.snapshot_at");
     if (epoch == kSentinel) return nullptr;
     auto it = epochs_.find(epoch);
     if (it == epochs_.end()) return nullptr;
@@ -242,11 +259,15 @@ std::shared_ptr<const pir::Snapshot> ServerCore::snapshot_at(uint64_t epoch) con
 
 std::shared_ptr<const pir::Snapshot> ServerCore::latest_snapshot() const { return snapshot_at(latest_epoch_); }
 
-crypto::Signature ServerCore::sign_current_freeze() const { return sign_freeze(sign_seed_, freeze_); }
+crypto::Signature ServerCore::sign_current_freeze() const {
+    b200::Trace tr("server.sign_current_freeze");
+    return sign_freeze(sign_seed_, freeze_);
+}
 
 // server.cpp:95-113: every field the replicas must agree on; the table, the
 // window and each sealed epoch's bytes are digested from the device state.
 bytes ServerCore::state_digest() const {
+    b200::Trace tr("server.state_digest");
     auto cs = state_in(epochs_);
     crypto::Hasher h(32);
     h.update(to_bytes("server-state-v1"));
@@ -285,6 +306,7 @@ bytes ServerCore::state_digest() const {
 // blob earns a random block from the caller's rng, never an error.
 ShareAnswer answer_share(const pir::Snapshot& snap, const crypto::BoxKeyPair& keys, byte_view blob,
                          uint32_t buckets, Rng& rng, ServerMetrics* metrics) {
+    b200::Trace tr("server.answer_share");
     ShareAnswer out;
     if (auto plain = crypto::pk_open(keys, blob)) {
         auto share = wire::decode_read_share(*plain, buckets);

@@ -280,8 +280,9 @@ struct xpir_window {
     std::deque<unsigned long long*> deltas;
     cudaStream_t stream = nullptr;
     DevBuf pos, seqs, scratch, enc;
-    PinnedBuf stage;  // host positions of xpir_window_absorb_prechecked
-    std::mutex mu;
+    PinnedBuf stage;           // host positions of xpir_window_absorb_prechecked
+    mutable PinnedBuf dstage;  // deltas staged for a digest (xpir_window_digest_n)
+    mutable std::mutex mu;
 };
 
 // Window::absorb of positions already checked against m_bits on the host: one

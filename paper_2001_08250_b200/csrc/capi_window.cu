@@ -67,6 +67,7 @@ int xpir_window_destroy(xpir_window* win) {
     win->scratch.release();
     win->enc.release();
     win->stage.release();
+    win->dstage.release();
     cudaStreamDestroy(win->stream);
     delete win;
     return XPIR_OK;
@@ -191,6 +192,16 @@ int xpir_window_digest(const xpir_window* win, uint8_t out[32]) {  // notify.cpp
 int xpir_window_digest_n(const xpir_window* win, uint64_t count, uint8_t out[32]) {  // Window::digest(count)
     if (!win || !out) return fail(XPIR_EINVAL, "window_digest: null argument");
     if (count > win->deltas.size()) return fail(XPIR_EINVAL, "Window::digest: count too large");  // notify.cpp:92
+    // every delta in one batch of async copies into pinned memory, one sync (a
+    // freeze digests the whole window: round 1 paid a sync + copy per delta)
+    std::lock_guard<std::mutex> lk(win->mu);
+    DeviceGuard g(win->device);
+    const size_t row = 8 * win->words;
+    XCK(win->dstage.ensure(count ? row * count : 1));
+    for (uint64_t i = 0; i < count; ++i)
+        XCK(cudaMemcpyAsync(win->dstage.p + i * row, win->deltas[i], row, cudaMemcpyDeviceToHost, win->stream));
+    XCK(win->dstage.release_after(win->stream));
+    XCK(cudaStreamSynchronize(win->stream));
     HostBlake2b h(32);
     const char* tag = "interest-window-v1";
     h.update(reinterpret_cast<const uint8_t*>(tag), std::strlen(tag));
@@ -199,12 +210,7 @@ int xpir_window_digest_n(const xpir_window* win, uint64_t count, uint8_t out[32]
     h.update_u64be(win->w);
     h.update_u64be(win->base);
     h.update_u64be(count);
-    std::vector<uint64_t> words(win->words);
-    for (uint64_t i = 0; i < count; ++i) {
-        int rc = xpir_window_delta(win, i, words.data());
-        if (rc) return rc;
-        h.update(reinterpret_cast<const uint8_t*>(words.data()), 8 * words.size());  // LE words
-    }
+    for (uint64_t i = 0; i < count; ++i) h.update(win->dstage.p + i * row, row);  // LE words
     h.final(out);
     return XPIR_OK;
 }
