@@ -13,6 +13,10 @@
 // (qT) exactly as for k_scan_m4rm; work units are dealt round-robin with the
 // column tile fastest (shared L2 reuse of staged chunks); accumulators are
 // flushed with 64-bit atomicXor per unit. Bit-exact pir::answer_batch.
+// B <= 32 (round 2): each request's lookups are dealt over 2/4/8 quarter-warp
+// slots (template SPLIT, no per-lookup branch), so all 16 warps look up instead
+// of B/4; B = 32 rose from 0.72-0.76 to 0.80 of the dense roofline, and the
+// branch-free loop lifted B = 48..256 by 4-12% (profiles/r02_nibble_split.jsonl).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -29,16 +33,20 @@ constexpr int K4_NT = 512;
 constexpr int K4_NW = K4_NT / 32;
 constexpr int K4_CHUNK_BUCKETS = 128;                // 16 query bytes per request
 constexpr int K4_TAB = 16 * 128;                     // one 16-row table
-constexpr int K4_PHASE_TABS = 16 * K4_TAB;           // 16 tables = 64 buckets
 constexpr int K4_DBS = K4_CHUNK_BUCKETS * 128;       // 16 KiB
 
-template <int RPT>
+// PT tables per phase (16: 64 buckets, two phases per chunk; 32: the whole chunk);
+// NST staged chunks in flight (the prefetch distance: a small batch finishes a
+// chunk faster than HBM latency, so it needs more than double buffering)
+template <int RPT, int PT, int NST>
 struct K4Layout {
     static constexpr int Rc = K4_NW * 4 * RPT;
     static constexpr int QS = 16 * Rc;               // 16 qT rows of the chunk
-    static constexpr int OFF_QS = 2 * K4_PHASE_TABS;
-    static constexpr int OFF_DBS = OFF_QS + 2 * QS;
-    static constexpr int SMEM = OFF_DBS + 2 * K4_DBS;
+    static constexpr int PHASE_TABS = PT * K4_TAB;
+    static constexpr int OFF_QS = 2 * PHASE_TABS;
+    static constexpr int OFF_DBS = OFF_QS + NST * QS;
+    static constexpr int SMEM = OFF_DBS + NST * K4_DBS;
+    static_assert(SMEM <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
 
 template <int RPT>
@@ -56,18 +64,25 @@ __device__ __forceinline__ uint32_t load_bytes(uint32_t a) {
 }
 }  // namespace
 
-template <int RPT>
+template <int RPT, int PT, int NST, int SPLIT>
 __global__ void __launch_bounds__(K4_NT, 1)
 k_scan_m4rm4(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ qT,
              uint64_t qstride, uint32_t B, uint8_t* __restrict__ out, uint32_t n_ctiles, uint32_t n_chunks,
              uint32_t n_seg) {
-    using L = K4Layout<RPT>;
+    using L = K4Layout<RPT, PT, NST>;
+    constexpr int JB = PT / 2;  // query bytes per phase
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sbase = smem_u32(smem);
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int qq = lane >> 3, l8 = lane & 7;
-    const int slot0 = (warp * 4 + qq) * RPT;
+    // SPLIT > 1 (RPT = 1, B <= 32): the 64 quarter-warp slots hold 64 / SPLIT
+    // requests, each request's lookups of a phase dealt to SPLIT slots (query byte
+    // j to part j % SPLIT), so every warp looks up; the parts' partial answers
+    // meet in the red.xor flush
+    constexpr int PER = 64 / SPLIT;  // requests per tile when split
+    const int part = (warp * 4 + qq) / PER;
+    const int slot0 = SPLIT > 1 ? (warp * 4 + qq) - part * PER : (warp * 4 + qq) * RPT;
     const uint32_t n_rtiles = (B + L::Rc - 1) / L::Rc;
     const uint64_t units = uint64_t(n_ctiles) * n_rtiles * n_seg;
 
@@ -80,7 +95,7 @@ k_scan_m4rm4(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint
         if (kc0 >= kc1) continue;
         const uint32_t r_base = rt * L::Rc;
         const uint32_t nvalid = min(uint32_t(L::Rc), B - r_base);
-        const bool active = uint32_t(warp * 4 * RPT) < nvalid;
+        const bool active = SPLIT > 1 ? uint32_t(slot0) < nvalid : uint32_t(warp * 4 * RPT) < nvalid;
 
         uint4 acc[RPT];
 #pragma unroll
@@ -106,29 +121,30 @@ k_scan_m4rm4(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint
             }
         };
 
-        stage(kc0, 0);
-        cp_async_commit();
+#pragma unroll
+        for (int p = 0; p < NST - 1; ++p) {
+            if (kc0 + p < kc1) stage(kc0 + p, p);
+            cp_async_commit();
+        }
         int tb = 0;
         for (uint32_t kc = kc0; kc < kc1; ++kc) {
-            const int b = (kc - kc0) & 1;
-            if (kc + 1 < kc1) {
-                stage(kc + 1, b ^ 1);
-                cp_async_commit();
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
-            }
+            const int b = int((kc - kc0) % NST);
+            if (kc + NST - 1 < kc1) stage(kc + NST - 1, int((kc - kc0 + NST - 1) % NST));
+            cp_async_commit();
+            cp_async_wait<NST - 1>();  // chunk kc landed (one group per chunk, empty past the end)
             __syncthreads();
             const uint32_t qbuf = sbase + L::OFF_QS + b * L::QS;
             const uint32_t dbuf = sbase + L::OFF_DBS + b * K4_DBS;
 #pragma unroll 1
-            for (int ph = 0; ph < 2; ++ph) {
-                const uint32_t tabs = sbase + tb * K4_PHASE_TABS;
-                {   // warp w builds the table of buckets 64*ph + 4w .. +3
-                    const uint32_t src = dbuf + (64 * ph + 4 * warp) * 128 + lane * 4;
+            for (int ph = 0; ph < 32 / PT; ++ph) {
+                const uint32_t tabs = sbase + tb * L::PHASE_TABS;
+#pragma unroll
+                for (int u = 0; u < PT / 16; ++u) {  // warp w builds table t = w + 16u: buckets 4t .. 4t+3
+                    const int t16 = warp + 16 * u;
+                    const uint32_t src = dbuf + (4 * PT * ph + 4 * t16) * 128 + lane * 4;
                     const uint32_t b0 = lds32(src), b1 = lds32(src + 128), b2 = lds32(src + 256),
                                    b3 = lds32(src + 384);
-                    const uint32_t t = tabs + warp * K4_TAB + lane * 4;
+                    const uint32_t t = tabs + t16 * K4_TAB + lane * 4;
                     uint32_t h = 0;
                     sts32(t + 0 * 128, h);
                     h ^= b0; sts32(t + 1 * 128, h);
@@ -151,8 +167,9 @@ k_scan_m4rm4(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint
                 if (active) {
                     const uint32_t rows = tabs + l8 * 16;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {  // query byte 8*ph + j: tables 2j (low) and 2j+1 (high)
-                        const uint32_t qb = load_bytes<RPT>(qbuf + (8 * ph + j) * L::Rc + slot0);
+                    for (int jj = 0; jj < JB / SPLIT; ++jj) {  // query byte JB*ph + j: tables 2j, 2j+1
+                        const int j = part + jj * SPLIT;
+                        const uint32_t qb = load_bytes<RPT>(qbuf + (JB * ph + j) * L::Rc + slot0);
 #pragma unroll
                         for (int i = 0; i < RPT; ++i) {
                             const uint32_t x = (qb >> (8 * i)) & 0xffu;
@@ -183,10 +200,11 @@ k_scan_m4rm4(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint
     }
 }
 
-template <int RPT>
+template <int RPT, int SPLIT = 1>
 static cudaError_t launch_k4(const M4Args& a, int num_sms) {
-    using L = K4Layout<RPT>;
-    cudaError_t e = cudaFuncSetAttribute(k_scan_m4rm4<RPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+    constexpr int PT = 16, NST = 2;  // 32 tables per phase / deeper staging: measured no faster
+    using L = K4Layout<RPT, PT, NST>;
+    cudaError_t e = cudaFuncSetAttribute(k_scan_m4rm4<RPT, PT, NST, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
     if (e != cudaSuccess) return e;
     const uint32_t n_ctiles = a.S / 128;
     const uint32_t n_rtiles = (a.B + L::Rc - 1) / L::Rc;
@@ -196,12 +214,17 @@ static cudaError_t launch_k4(const M4Args& a, int num_sms) {
     uint64_t n_seg = (16 * grid + pairs - 1) / pairs;  // ~16 units per CTA
     if (n_seg > n_chunks) n_seg = n_chunks;
     if (n_seg < 1) n_seg = 1;
-    k_scan_m4rm4<RPT><<<uint32_t(grid), K4_NT, L::SMEM, a.stream>>>(a.db, a.nb, a.S, a.qT, a.qstride, a.B, a.out,
-                                                                  n_ctiles, n_chunks, uint32_t(n_seg));
+    k_scan_m4rm4<RPT, PT, NST, SPLIT><<<uint32_t(grid), K4_NT, L::SMEM, a.stream>>>(
+        a.db, a.nb, a.S, a.qT, a.qstride, a.B, a.out, n_ctiles, n_chunks, uint32_t(n_seg));
     return cudaGetLastError();
 }
 
 cudaError_t launch_scan_m4rm4(const M4Args& a, int num_sms) {
+    // B <= 32: each request's lookups spread over 64 / B' slots (B' = B rounded up
+    // to a power of two >= 8), so all 16 warps look up
+    if (a.B <= 8) return launch_k4<1, 8>(a, num_sms);
+    if (a.B <= 16) return launch_k4<1, 4>(a, num_sms);
+    if (a.B <= 32) return launch_k4<1, 2>(a, num_sms);
     if (a.B <= 64) return launch_k4<1>(a, num_sms);
     if (a.B <= 128) return launch_k4<2>(a, num_sms);
     return launch_k4<4>(a, num_sms);

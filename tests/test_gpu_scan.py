@@ -69,6 +69,22 @@ def test_scan_matches_oracle(xp, port, cuda, kernel, N, S, B):
         assert xp.last_scan_kernel() == 2
 
 
+@pytest.mark.parametrize("B", [5, 8, 9, 13, 16, 17, 24, 31, 32, 33])
+def test_nibble_tables_split_lookups(xp, port, cuda, B):
+    """Nibble tables (7) at B <= 32 deal each request's lookups over 2/4/8
+    quarter-warp slots whose partial answers meet in the red.xor flush; every
+    split (and the unsplit B = 33) against the oracle, ragged bucket counts."""
+    N, S = 5000 + B, 256
+    g = np.random.default_rng(B * 31 + 7)
+    db = rand(g, N * S)
+    q = rand(g, B, (N + 7) // 8)
+    xp.set_scan_opts(7)
+    st = xp.Store(N, S)
+    st.upload(db)
+    assert np.array_equal(st.answer_batch(q), port.answer_batch(db, N, S, q, B))
+    assert xp.last_scan_kernel() == 7
+
+
 @pytest.mark.parametrize("S", [96, 512])
 def test_direct_every_small_batch(xp, port, cuda, S):
     """The direct kernel's request tiling (tiles of 1/2/4/6/8 requests, partial
