@@ -639,23 +639,29 @@ int xpir_table_insert_batch(xpir_table* t, const uint32_t* b1, const uint32_t* b
     if (ok == 1 && !t->state_on_device && 256 < t->slots() && walk_w_supported(t->d)) {
         if (int rc = insert_one_graph(t, b1[0], b2[0], payload, reports)) return rc;
     } else if (ok > 0) {
-        // [beta1 | beta2 | payload | reports] packed: one pinned staging buffer, one H2D
+        // [beta1 | beta2 | payload | reports] packed: one pinned staging buffer, one H2D.
+        // Large payloads go straight from the caller's memory instead (the driver
+        // pipelines pageable copies; one host memcpy of 16 MB into the stage first
+        // cost ~2 ms per config-3-sized round)
         const uint64_t o2 = round16(4 * ok), op = o2 + round16(4 * ok), orep = op + round16(ok * t->d.item);
         const uint64_t total = orep + 16 * ok;
-        XCK(t->stage.ensure(total));
+        const bool pack_payload = ok * t->d.item <= (uint64_t(1) << 18);
+        const uint64_t hrep = pack_payload ? orep : op;  // host offset of the reports
+        XCK(t->stage.ensure(hrep + 16 * ok));
         std::memcpy(t->stage.p, b1, 4 * ok);
         std::memcpy(t->stage.p + o2, b2, 4 * ok);
-        std::memcpy(t->stage.p + op, payload, ok * t->d.item);
+        if (pack_payload) std::memcpy(t->stage.p + op, payload, ok * t->d.item);
         XCK(t->in_pack.ensure(total));
         uint8_t* dp = t->in_pack.as<uint8_t>();
-        XCK(cudaMemcpyAsync(dp, t->stage.p, orep, cudaMemcpyHostToDevice, s));
+        XCK(cudaMemcpyAsync(dp, t->stage.p, pack_payload ? orep : op, cudaMemcpyHostToDevice, s));
+        if (!pack_payload) XCK(cudaMemcpyAsync(dp + op, payload, ok * t->d.item, cudaMemcpyHostToDevice, s));
         uint64_t applied = ok;
         int rc = insert_impl(t, reinterpret_cast<const uint32_t*>(dp), reinterpret_cast<const uint32_t*>(dp + o2),
-                             dp + op, ok, reinterpret_cast<uint32_t*>(dp + orep), s, t->stage.p + orep, true,
+                             dp + op, ok, reinterpret_cast<uint32_t*>(dp + orep), s, t->stage.p + hrep, true,
                              &applied);
         XCK(t->stage.release_after(s));
         if (rc) return rc;
-        if (reports) std::memcpy(reports, t->stage.p + orep, 16 * ok);
+        if (reports) std::memcpy(reports, t->stage.p + hrep, 16 * ok);
     }
     if (ok < n) return fail(XPIR_EINVAL, "cuckoo: bucket index out of range");
     return XPIR_OK;
@@ -673,8 +679,10 @@ int xpir_table_reserve(xpir_table* t, uint64_t max_batch) {
     XCK(t->in_b2.ensure(4 * max_batch));
     XCK(t->in_reports.ensure(16 * max_batch));
     // the packed host-input staging of xpir_table_insert_batch, pinned, for max_batch writes
+    // (payloads above 256 KiB are copied from the caller's memory, not staged)
     const uint64_t pack = 2 * round16(4 * max_batch) + round16(max_batch * t->d.item) + 16 * max_batch;
-    XCK(t->stage.ensure(pack));
+    const bool pack_payload = max_batch * t->d.item <= (uint64_t(1) << 18);
+    XCK(t->stage.ensure(pack_payload ? pack : 2 * round16(4 * max_batch) + 16 * max_batch));
     XCK(t->in_pack.ensure(pack));
     XCK(cuckoo_reserve(t->par, max_batch, t->d.buckets, t->stream));  // parallel-prefix scratch
     // a full draw window, so a round's eviction walk rarely has to pause for draws
