@@ -11,15 +11,15 @@ import paper_2001_08250_b200 as xp  # noqa: E402
 
 peaks = xp.measure_peaks(0)
 cs = torch.cuda.current_stream()
-for S in (4096,):
+for S in (4096, 512, 1024):
     N = (1 << 30) // S
     st = xp.Store(N, S)
     st.fill_keystream(bytes(32), 0)
     res = {}
-    for B in (8, 12, 16, 20, 24, 32, 48, 64, 128, 256):
+    for B in (8, 12, 16, 20, 24, 32, 48, 64, 128, 144, 192, 256):
         q = torch.randint(0, 256, (B, N // 8), dtype=torch.uint8, device="cuda")
         outs, fr = {}, {}
-        for k in (1, 7):
+        for k in ((1, 7, 9) if B >= 128 else (1, 7)):
             xp.set_scan_opts(k)
             o = torch.empty((B, S), dtype=torch.uint8, device="cuda")
             for _ in range(2):
@@ -36,7 +36,8 @@ for S in (4096,):
             t_hbm = (N * S + B * N / 8 + B * S) / 6.5345e12 * 1e3
             fr[k] = round(max(t_alu, t_hbm) / ms, 3)
             outs[k] = o
-        res[B] = {"direct": fr[1], "nibble": fr[7], "same": bool(torch.equal(outs[1], outs[7]))}
+        res[B] = {"direct": fr[1], "nibble": fr[7], **({"six": fr[9]} if 9 in fr else {}),
+                  "same": all(bool(torch.equal(outs[1], o)) for o in outs.values())}
     print(json.dumps({"S": S, "res": res}), flush=True)
     st.close()
 xp.set_scan_opts(0)
