@@ -444,7 +444,7 @@ static int scan_rows(xpir_store* st, const uint8_t* rows, uint64_t stride, uint3
     if (B == 0) return XPIR_OK;
     const int k = choose_kernel(st, B);
     const uint64_t blo = st->byte_lo(), nbw = st->nbytes_window();
-    if (k != 2 && k != 7 && k != 8 && k != 9 && k != 10) return run_rows(st, k, rows + blo, stride, B, d_out, s);
+    if (k != 2 && k != 7 && k != 8 && k != 9) return run_rows(st, k, rows + blo, stride, B, d_out, s);
     const uint64_t qs = m4rm_qstride(B);
     DevBuf& qw = st->qwin_for(s);
     XCK(qw.ensure(m4rm_qrows(nbw) * qs));
