@@ -1,4 +1,4 @@
-"""A/B: direct kernel on the head of the store and nibble tables on the tail,
+"""Historical A/B (round 2; the kernel-11 dispatch path it drove was removed after it lost): direct kernel on the head of the store and nibble tables on the tail,
 launched concurrently on two streams (kernel 11, XPIR_HYB2_F = head fraction in
 thousandths) against each alone; 1 GiB store, S = 4096, explicit rows."""
 import json
