@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -580,9 +581,22 @@ cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint
     // One thread per (write, hash): short-lived blocks, so the write round's table
     // chain (its cooperative prefix on a higher-priority stream) takes SMs as they
     // retire instead of waiting for a resident grid-stride wave to drain (config 3
-    // round as one graph: 0.157 -> 0.128 ms). Grid-stride only past 2^31 blocks.
+    // round as one graph: 0.157 -> 0.127 ms). 56 KiB of (unused) dynamic shared
+    // memory per block caps the kernel at 4 blocks per SM, leaving thread slots for
+    // the chain from the start: 0.127 -> 0.119 ms; alone the hashes take ~100 us
+    // instead of ~97 (ALU-bound at 16 warps per SM either way).
+    constexpr int kOccupancyCapSmem = 56 * 1024;
+    static std::atomic<uint64_t> attr_set{0};  // per device (the attribute is per context)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !((attr_set.load() >> dev) & 1)) {
+        cudaError_t e = cudaFuncSetAttribute(k_interest, cudaFuncAttributeMaxDynamicSharedMemorySize, kOccupancyCapSmem);
+        if (e != cudaSuccess) return e;
+        attr_set.fetch_or(uint64_t(1) << dev);
+    }
     const uint64_t want = (t + 127) / 128, cap = 0x7fffffffull;
-    k_interest<<<uint32_t(want < cap ? want : cap), 128, 0, s>>>(id, seqs, n, h, m_bits, pos_out, words);
+    k_interest<<<uint32_t(want < cap ? want : cap), 128, kOccupancyCapSmem, s>>>(id, seqs, n, h, m_bits, pos_out,
+                                                                                 words);
     return cudaGetLastError();
 }
 
