@@ -254,7 +254,9 @@ def launch_count() -> int:
 
 
 def last_scan_kernel() -> int:
-    """1 = direct select-XOR, 2 = M4RM byte tables, 3 = byte-granular."""
+    """Kernel of the last scan: 1 direct select-XOR, 2 M4RM byte tables (register
+    accumulators), 3 byte-granular, 5 byte tables with half-TMEM accumulators,
+    7 nibble tables, 8 9-bucket quad tables (full TMEM), 9 6-bucket tables."""
     return lib().xpir_last_scan_kernel()
 
 

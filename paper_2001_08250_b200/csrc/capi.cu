@@ -338,7 +338,7 @@ uint64_t xpir_query_window_bytes(const xpir_store* st) {
 // Batch-size crossovers from the config-5 sweep: below 24 the direct
 // kernel, nibble tables (7) from 24, 6-bucket tables (9) for 129..256 (6-15% faster
 // than the nibble tables there: 1 GiB store, S = 1024/4096, B = 256 1.96 vs 2.30 ms;
-// past 256 its request tiles split), byte tables (2/5) from 257, quad tables (8) or
+// past 256 its request tiles split), byte tables (2/5) from 257, 9-bucket quad tables (8) or
 // half-TMEM byte tables (5) by the calibrated cost model from 2048.
 static const uint32_t g_k4_min_batch = 24;
 static const uint32_t g_k6_min_batch = 129, g_k6_max_batch = 256;

@@ -11,7 +11,7 @@ exchange is our own: every rank maps its peers' partial buffers through CUDA IPC
 (reduce-scatter: rank g owns requests [g*B/G, (g+1)*B/G)). The mask pad (K3) is
 applied exactly once, after the reduce, by the owner.
 
-Fused mode (B >= 2048, the quad-table M4RM kernel 8): the reduce disappears
+Fused mode (B >= 2048, the 9-bucket quad-table M4RM kernel 8): the reduce disappears
 into the scan. Every owner first initialises its rows (mask pad or zero); then
 each rank's scan kernel accumulates the segment partials of every (request
 tile, column tile) in a local buffer and the tile's last segment pushes the
