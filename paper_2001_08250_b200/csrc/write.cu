@@ -112,9 +112,56 @@ struct Id16 {
     uint8_t b[16];
 };
 
+// BLAKE2b for the interest hashes (prims.cuh blake2b_compress, crypto.cpp:146-166
+// via bloom_positions), the G function's rotate-left-by-1 moved to the FMA pipe:
+// the compression is ALU-bound (XOR / funnel shift / 64-bit add all issue on the
+// ALU pipe), so lo' = lo*2 + hi>>31 and hi' = hi*2 + lo>>31 are IMADs with a
+// multiplier the compiler cannot fold (`two`, a kernel argument). Bit-identical.
+// Measured (config 3 round as one graph): 0.119 -> 0.116 ms, the hashes alone
+// 100 -> 96 us. Moving the rotations by 24 and 16 too (MUL.HI + IMAD pairs) was
+// no faster (98.5 us) or slower (108 us): the longer dependency chain costs more.
+__device__ __forceinline__ uint64_t rotl1_fma(uint64_t x, uint32_t two) {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    uint32_t tl, th, nl, nh;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(tl) : "r"(lo), "r"(two));   // lo >> 31
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(th) : "r"(hi), "r"(two));   // hi >> 31
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(nl) : "r"(lo), "r"(two), "r"(th));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(nh) : "r"(hi), "r"(two), "r"(tl));
+    return (uint64_t(nh) << 32) | nl;
+}
+
+__device__ __forceinline__ uint64_t blake2b64_interest(uint64_t w0, uint64_t w1, uint64_t w2, uint32_t i,
+                                                       uint32_t two) {
+    const uint64_t m[16] = {w0, w1, w2, uint64_t(i), 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    uint64_t v[16];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        v[k] = b2_iv(k);
+        v[8 + k] = b2_iv(k);
+    }
+    v[0] ^= 0x01010000ULL ^ 8ULL;  // parameter block: outlen 8, fanout 1, depth 1
+    const uint64_t h0 = v[0];
+    v[12] ^= 28;  // t0 = message length
+    v[14] = ~v[14];
+#define XP_GI(r, i, a, b, c, d)                                         \
+    a = a + b + m[b2_sigma(r, 2 * i)]; d = rotr64(d ^ a, 32);           \
+    c = c + d; b = rotr64(b ^ c, 24);                                   \
+    a = a + b + m[b2_sigma(r, 2 * i + 1)]; d = rotr64(d ^ a, 16);       \
+    c = c + d; b = rotl1_fma(b ^ c, two)
+#pragma unroll
+    for (int r = 0; r < 12; ++r) {
+        XP_GI(r, 0, v[0], v[4], v[8], v[12]); XP_GI(r, 1, v[1], v[5], v[9], v[13]);
+        XP_GI(r, 2, v[2], v[6], v[10], v[14]); XP_GI(r, 3, v[3], v[7], v[11], v[15]);
+        XP_GI(r, 4, v[0], v[5], v[10], v[15]); XP_GI(r, 5, v[1], v[6], v[11], v[12]);
+        XP_GI(r, 6, v[2], v[7], v[8], v[13]); XP_GI(r, 7, v[3], v[4], v[9], v[14]);
+    }
+#undef XP_GI
+    return h0 ^ v[0] ^ v[8];
+}
+
 __global__ void k_interest(Id16 id, const uint64_t* __restrict__ seqs, uint64_t n, uint32_t h,
                            uint32_t m_bits, uint32_t* __restrict__ pos_out,
-                           unsigned long long* __restrict__ words) {
+                           unsigned long long* __restrict__ words, uint32_t two) {
     uint64_t w0 = 0, w1 = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -130,7 +177,7 @@ __global__ void k_interest(Id16 id, const uint64_t* __restrict__ seqs, uint64_t 
         const uint64_t sq = seqs[w];
         const uint64_t w2 = __byte_perm(uint32_t(sq >> 32), 0, 0x0123) |
                             uint64_t(__byte_perm(uint32_t(sq), 0, 0x0123)) << 32;
-        const uint32_t pos = bloom_position_interest(w0, w1, w2, k, m_bits);
+        const uint32_t pos = uint32_t(__umul64hi(blake2b64_interest(w0, w1, w2, k, two), uint64_t(m_bits)));
         if (pos_out) pos_out[t] = pos;
         if (words) atomicOr(words + (pos >> 6), 1ull << (pos & 63));
     }
@@ -583,8 +630,7 @@ cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint
     // retire instead of waiting for a resident grid-stride wave to drain (config 3
     // round as one graph: 0.157 -> 0.127 ms). 56 KiB of (unused) dynamic shared
     // memory per block caps the kernel at 4 blocks per SM, leaving thread slots for
-    // the chain from the start: 0.127 -> 0.119 ms; alone the hashes take ~100 us
-    // instead of ~97 (ALU-bound at 16 warps per SM either way).
+    // the chain from the start: 0.127 -> 0.119 ms (ALU-bound at 16 warps per SM).
     constexpr int kOccupancyCapSmem = 56 * 1024;
     static std::atomic<uint64_t> attr_set{0};  // per device (the attribute is per context)
     int dev = 0;
@@ -596,7 +642,7 @@ cudaError_t launch_interest(const uint8_t* id16_host, const uint64_t* seqs, uint
     }
     const uint64_t want = (t + 127) / 128, cap = 0x7fffffffull;
     k_interest<<<uint32_t(want < cap ? want : cap), 128, kOccupancyCapSmem, s>>>(id, seqs, n, h, m_bits, pos_out,
-                                                                                 words);
+                                                                                 words, 2u);
     return cudaGetLastError();
 }
 
