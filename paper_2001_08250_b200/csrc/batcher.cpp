@@ -22,6 +22,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -39,6 +40,14 @@ namespace {
 
 enum class BState { Idle, Forming, Sealed, InFlight, Done };
 constexpr int NBUF = 3;
+
+// Batches in flight before a forming one waits (adaptive sealing). 1 (default):
+// closed-loop 381k requests/s at 512 callers; 2 (XPIR_BATCHER_INFLIGHT=2): lower
+// open-loop latency (250k/s offered: p50 290 vs 469 us) for 6% less peak (359k).
+static size_t inflight_cap() {
+    static const size_t cap = getenv("XPIR_BATCHER_INFLIGHT") ? size_t(atoi(getenv("XPIR_BATCHER_INFLIGHT"))) : 1;
+    return cap;
+}
 
 struct BBuf {
     uint8_t* rows = nullptr;   // pinned
@@ -106,7 +115,8 @@ struct xpir_batcher {
             // caller pays no batching delay); while a batch is in flight it keeps forming
             // until it is full, max_wait_us have passed, or the device goes idle.
             const auto deadline = b->first + std::chrono::microseconds(max_wait_us);
-            cv_work.wait_until(lk, deadline, [&] { return stop.load() || b->count >= max_batch || inflight.empty(); });
+            cv_work.wait_until(lk, deadline,
+                               [&] { return stop.load() || b->count >= max_batch || inflight.size() < inflight_cap(); });
             b->state = BState::Sealed;  // no more joins
             const uint32_t B = b->count;
             const bool masked = b->masked;
@@ -167,7 +177,7 @@ struct xpir_batcher {
             inflight.pop_front();
             publish(b, e == cudaSuccess ? XPIR_OK : XPIR_ECUDA,
                     e == cudaSuccess ? std::string() : std::string("batcher: ") + cudaGetErrorString(e));
-            if (inflight.empty()) cv_work.notify_one();  // a forming batch may go now
+            if (inflight.size() < inflight_cap()) cv_work.notify_one();  // a forming batch may go now
         }
     }
 };
