@@ -48,12 +48,14 @@
 //    local partial buffer whose last-arriving segment pushes each finished row to
 //    its owner rank over NVLink (red.relaxed.sys).
 //
-// Decoupled pipeline (DEC, full 8192-request tiles): instead of one CTA barrier
-// per set, two mbarriers per table buffer — full[b] (the 8 builder warps have
-// built a set into b) and empty[b] (all 16 warps have finished its lookups) — and
-// a builder-only named barrier for the staged bucket slices. Warps 8-15, which
-// do not build, run ahead into the next set's lookups instead of waiting at the
-// barrier for the builders' tail (config 4: 128.4-129.0 -> 127.1 ms).
+// Pipeline without CTA barriers: every warp builds 32 of a set's 512 table rows
+// and then looks up its own requests. Per table buffer two mbarriers — full[b]
+// (all 16 warps have written their rows of the set in b) and empty[b] (all 16
+// have finished its lookups) — and per staging slot one mbarrier that the
+// cp.async copies of the bucket slices arrive on as they land. A warp waits only
+// for what it reads next, so warps drift up to a set apart instead of meeting at
+// a barrier per set (config 4: 128.4 ms with a barrier per set -> 123.3 ms; the
+// 2048/4096-request tiles 5% / 3% faster).
 //
 // TMEM map (one CTA per SM): warp w uses lanes 32*(w%4)..+31 and columns
 // 128*(w/4) + 8*s for its request slot s < 4*NQ.
@@ -81,8 +83,8 @@ struct RCfg {
     // two table buffers, staging ring, TMEM slot
     static constexpr int OFF_STG = 2 * R_TAB;
     static constexpr int OFF_ADDR = OFF_STG + R_NST * R_STG;
-    static constexpr int OFF_MBAR = OFF_ADDR + 16;  // full[2], empty[2] (decoupled pipeline)
-    static constexpr int SMEM = OFF_MBAR + 32;
+    static constexpr int OFF_MBAR = OFF_ADDR + 16;  // full[2], empty[2], staged[R_NST]
+    static constexpr int SMEM = OFF_MBAR + 32 + 8 * R_NST;
     static constexpr int TCOLS = 128 * NQ;
     static_assert(SMEM <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
@@ -141,6 +143,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// the mbarrier counts this thread's prior cp.async copies as they land (.noinc:
+// the barrier's expected count, set at init, already includes them)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint32_t a) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];\n" ::"r"(a) : "memory");
+}
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
@@ -156,7 +163,7 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
 
 // qT: low index bytes, set-interleaved ([set][request] 32-bit words, 2 sets per
 // pair); qH: ninth-bit bytes ([pair][request]). Both qstride requests wide.
-template <int NQ, bool DEC>
+template <int NQ>
 __global__ void __launch_bounds__(R_NT, 1)
 k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const uint8_t* __restrict__ qT,
                const uint8_t* __restrict__ qH, uint64_t qstride, uint32_t B, uint8_t* __restrict__ out,
@@ -179,19 +186,18 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tbase = *reinterpret_cast<const uint32_t*>(sgen + C::OFF_ADDR);
-    // decoupled pipeline: full[b] completes when the 8 builder warps have built a
-    // set into table buffer b, empty[b] when all 16 warps have finished its lookups
-    const uint32_t mb_full = sbase + C::OFF_MBAR, mb_empty = sbase + C::OFF_MBAR + 16;
-    if (DEC) {
-        if (tid == 0) {
-            mbar_init(mb_full, 8);
-            mbar_init(mb_full + 8, 8);
-            mbar_init(mb_empty, 16);
-            mbar_init(mb_empty + 8, 16);
+    // mbarriers: full[b] / empty[b] per table buffer (16 warp arrivals each),
+    // staged[k] per staging slot (72 copying threads' cp.async completions)
+    const uint32_t mb_full = sbase + C::OFF_MBAR, mb_empty = sbase + C::OFF_MBAR + 16,
+                   mb_stg = sbase + C::OFF_MBAR + 32;
+    if (tid == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(mb_full + 8 * b, 16);
+            mbar_init(mb_empty + 8 * b, 16);
         }
-        __syncthreads();
+        for (int b = 0; b < R_NST; ++b) mbar_init(mb_stg + 8 * b, 72);
     }
-    const bool builder = warp < 8;
+    __syncthreads();
     const uint32_t tcol = tbase + (uint32_t((warp & 3) * 32) << 16) + uint32_t(warp >> 2) * (32 * NQ);
 
     // lookup constants: step kk reads table t = (lp + kk) & 3, own half first
@@ -205,9 +211,10 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
         bsel[kk] = t | ((4u + t) << 4) | ((12u + t) << 8) | ((12u + t) << 12);
     }
     const uint32_t dhalf = (i8 & 1) ? 0xfffffff0u : 16u;
-    // build constants: lane -> (table bt, 32-bit word bw); warp -> index bits 4..6
+    // build constants: lane -> (table bt, 32-bit word bw); warp -> index bits 4..7
     const int bt = lane >> 3, bw = lane & 7;
-    const uint32_t hm0 = 0u - (warp & 1u), hm1 = 0u - ((warp >> 1) & 1u), hm2 = 0u - ((warp >> 2) & 1u);
+    const uint32_t hm0 = 0u - (warp & 1u), hm1 = 0u - ((warp >> 1) & 1u), hm2 = 0u - ((warp >> 2) & 1u),
+                   hm3 = 0u - ((warp >> 3) & 1u);
 
     const uint32_t n_rtiles = (B + C::RC - 1) / C::RC;
     const uint64_t units = uint64_t(n_ctiles) * n_rtiles * n_seg;
@@ -242,6 +249,7 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
                 const bool ok = bucket < nb;
                 const uint8_t* src = db + (ok ? uint64_t(bucket) * S : 0) + uint64_t(c) * 32 + part * 16;
                 cp_async16_ef(dst + tid * 16, src, ok ? 16u : 0u, spol);
+                cp_async_mbar_arrive(mb_stg + 8 * buf);
             }
         };
         auto load_q = [&](uint32_t j, uint4 (&w)[NQ]) {
@@ -262,18 +270,18 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
         // Warps 0-7 build: warp w writes the rows whose index bits 4..6 equal w, for
         // the four values of bits 7..8 (16 Gray-code rows over buckets 0..3 each).
         // (All 16 warps building two blocks each measured no faster.)
+        // warp w writes the rows whose index bits 4..7 equal w, for both values of
+        // bit 8 (two 16-row Gray-code blocks over buckets 0..3)
         auto build = [&](int buf, int tb) {
-            if (warp >= 8) return;
             const uint32_t src = sbase + C::OFF_STG + buf * R_STG + bt * 32 + bw * 4;
             uint32_t b[9];
 #pragma unroll
             for (int i = 0; i < 9; ++i) b[i] = lds32(src + i * 128);
-            const uint32_t h = (b[4] & hm0) ^ (b[5] & hm1) ^ (b[6] & hm2);
+            const uint32_t h = (b[4] & hm0) ^ (b[5] & hm1) ^ (b[6] & hm2) ^ (b[7] & hm3);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t row0 =
-                    sbase + tb * R_TAB + uint32_t((warp + 8 * u) << 4) * 128 + bt * 32 + bw * 4;
-                uint32_t x = h ^ ((u & 1) ? b[7] : 0u) ^ ((u & 2) ? b[8] : 0u);
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t row0 = sbase + tb * R_TAB + uint32_t((warp + 16 * u) << 4) * 128 + bt * 32 + bw * 4;
+                uint32_t x = h ^ (u ? b[8] : 0u);
                 sts32(row0, x);
 #pragma unroll
                 for (int m = 1; m < 16; ++m) {
@@ -319,33 +327,19 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
             }
         };
 
-        // prologue: sets s0 .. s0+2 in flight, T(s0) built, words of s0 and pair p0 loading
+        // prologue: sets s0 .. s0+2 in flight, words of s0 and pair p0 loading, T(s0) built
         uint4 wn[NQ];
         uint32_t hn[NQ], hc[NQ];
         load_q(s0, wn);
         load_h(p0, hn);
 #pragma unroll
-        for (int p = 0; p < R_NST - 1; ++p) {
+        for (int p = 0; p < R_NST - 1; ++p)
             if (s0 + p < s1) stage(s0 + p, seq0 + p);
-            cp_async_commit();
-        }
-        if (DEC) {
-            // builders: staging of s0 landed (group s0; s0+1, s0+2 may pend), buffer 0
-            // free (its previous use consumed), build, publish
-            if (builder) {
-                cp_async_wait<R_NST - 2>();
-                asm volatile("bar.sync 1, 256;\n" ::: "memory");
-                if (seq0) mbar_wait(mb_empty, ((seq0 >> 1) - 1) & 1);
-                build(int(seq0 % R_NST), 0);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(mb_full);
-            }
-        } else {
-            cp_async_wait<R_NST - 3>();
-            __syncthreads();
-            build(int(seq0 % R_NST), 0);
-            __syncthreads();
-        }
+        mbar_wait(mb_stg + 8 * (seq0 % R_NST), (seq0 / R_NST) & 1);
+        if (seq0) mbar_wait(mb_empty, ((seq0 >> 1) - 1) & 1);
+        build(int(seq0 % R_NST), 0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mb_full);
 #pragma unroll 1
         for (uint32_t jp = s0; jp < s1; jp += 2) {
 #pragma unroll
@@ -363,38 +357,24 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
                     load_q(j + 1, wn);
                     if (h == 1) load_h((j + 1) >> 1, hn);
                 }
-                if (DEC) {
-                    if (builder) {
-                        if (j + R_NST - 1 < s1) stage(j + R_NST - 1, sq + R_NST - 1);
-                        cp_async_commit();
-                        if (j + 1 < s1) {
-                            cp_async_wait<R_NST - 2>();  // set j+1 landed (j+2, j+3 may pend)
-                            asm volatile("bar.sync 1, 256;\n" ::: "memory");
-                            const uint32_t sb = sq + 1;  // buffer sb & 1 = h ^ 1, use sb >> 1
-                            mbar_wait(mb_empty + 8 * (h ^ 1), ((sb >> 1) - 1) & 1);
-                            build(int(sb % R_NST), h ^ 1);
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(mb_full + 8 * (h ^ 1));
-                        }
-                    }
-                    mbar_wait(mb_full + 8 * h, (sq >> 1) & 1);
-                    lookups(wc, hc, 4u * uint32_t(h), h);
-                    tm_wait_st();
+                if (j + R_NST - 1 < s1) stage(j + R_NST - 1, sq + R_NST - 1);
+                if (j + 1 < s1) {  // this warp's rows of set j+1, once its slices landed and buffer h^1 is free
+                    const uint32_t sb = sq + 1;
+                    mbar_wait(mb_stg + 8 * (sb % R_NST), (sb / R_NST) & 1);
+                    mbar_wait(mb_empty + 8 * (h ^ 1), ((sb >> 1) - 1) & 1);
+                    build(int(sb % R_NST), h ^ 1);
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(mb_empty + 8 * h);
-                } else {
-                    if (j + R_NST - 1 < s1) stage(j + R_NST - 1, sq + R_NST - 1);
-                    cp_async_commit();
-                    if (j + 1 < s1) build(int((sq + 1) % R_NST), h ^ 1);
-                    lookups(wc, hc, 4u * uint32_t(h), h);
-                    tm_wait_st();
-                    cp_async_wait<R_NST - 3>();
-                    __syncthreads();
+                    if (lane == 0) mbar_arrive(mb_full + 8 * (h ^ 1));
                 }
+                mbar_wait(mb_full + 8 * h, (sq >> 1) & 1);  // set j built by every warp
+                lookups(wc, hc, 4u * uint32_t(h), h);
+                tm_wait_st();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(mb_empty + 8 * h);
             }
         }
         seq0 += s1 - s0;
-        if (DEC) __syncthreads();  // the next unit restages and rebuilds
+        __syncthreads();  // the next unit restages and rebuilds
 
         // flush (K1q's): straight to the rows, or through the local partial buffer
         // and the tile's last segment when the fused cross-GPU reduce is on
@@ -469,10 +449,10 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
 
 namespace {
 
-template <int NQ, bool DEC>
+template <int NQ>
 cudaError_t launch_q9(const M4Args& a, int num_sms) {
     using C = RCfg<NQ>;
-    cudaError_t e = cudaFuncSetAttribute(k_scan_m4rm_q9<NQ, DEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_scan_m4rm_q9<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     const uint32_t n_ctiles = a.S / 32;
     const uint32_t n_rtiles = (a.B + C::RC - 1) / C::RC;
@@ -500,7 +480,7 @@ cudaError_t launch_q9(const M4Args& a, int num_sms) {
     if (n_seg < want) n_seg = step <= want ? (want + step - 1) / step * step : want;
     if (n_seg < 1) n_seg = 1;
     const uint8_t* qH = a.qT + m4rm_q9_hi_offset(a.nb, a.qstride);
-    k_scan_m4rm_q9<NQ, DEC><<<dim3(uint32_t(grid)), R_NT, C::SMEM, a.stream>>>(
+    k_scan_m4rm_q9<NQ><<<dim3(uint32_t(grid)), R_NT, C::SMEM, a.stream>>>(
         a.db, a.nb, a.S, a.qT, qH, a.qstride, a.B, a.out, n_ctiles, n_pairs, uint32_t(n_seg), a.peers);
     return cudaGetLastError();
 }
@@ -537,12 +517,10 @@ uint64_t m4rm_q9_hi_offset(uint32_t nb, uint64_t qstride) { return uint64_t((nb 
 
 cudaError_t launch_scan_m4rm_q(const M4Args& a, int num_sms) {
     if (a.S % 32 != 0) return cudaErrorInvalidValue;
-    // decoupled build/lookup pipeline for full tiles (config 4: 128.4-129.0 ->
-    // 127.1 ms); the 4096-request tile measured 1.3% slower with it (17.44 vs 17.67 ms)
     switch (m4rm_q_tile(a.B)) {
-        case 8192: return launch_q9<4, true>(a, num_sms);
-        case 4096: return launch_q9<2, false>(a, num_sms);
-        default: return launch_q9<1, false>(a, num_sms);
+        case 8192: return launch_q9<4>(a, num_sms);
+        case 4096: return launch_q9<2>(a, num_sms);
+        default: return launch_q9<1>(a, num_sms);
     }
 }
 
