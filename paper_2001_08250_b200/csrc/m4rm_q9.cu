@@ -5,8 +5,8 @@
 // Same math as every M4RM kernel: T[x] = XOR of the buckets selected by the bits
 // of x, the answer slice of request r is the XOR over tables of T[index_r]
 // (bit-exact pir::answer_batch, pir.cpp:41-52). Round 1's K1q used 8-bucket
-// (byte) tables; round 2 replaced it with this kernel (profiles/r02_quad9_ab.txt:
-// 130 against 137 ms per config-4 launch, bit-exact). What changed:
+// (byte) tables; round 2 replaced it with this kernel (profiles/r02_ncu_m4rm_q9_summary.txt:
+// 123.3 against 136.8 ms per config-4 launch, bit-exact). What changed:
 //
 //  * A table covers 9 buckets (512 rows of 32 bytes), so one lookup serves 9
 //    buckets instead of 8: the lookup wavefronts per bucket drop by 1/9.
@@ -25,8 +25,8 @@
 //    bits spread to one byte per table (IMAD by 0x204081 + LOP3, once per
 //    request and set).
 //  * Shared-memory wavefronts per set (Rc = 8192): 8192 lookups + 512 table
-//    stores + 72 bucket-word reads + 256 + 32 index loads + ~10 staging fills
-//    = 9074 per 36 buckets, against K1q's 8776 per 32 buckets: 8% fewer per
+//    stores + 144 bucket-word reads + 256 + 32 index loads + ~10 staging fills
+//    = 9146 per 36 buckets, against K1q's 8776 per 32 buckets: 7% fewer per
 //    bucket. The index costs what the byte tables' did (PRMT + IMAD per lookup)
 //    plus three instructions per request and set.
 //
@@ -41,8 +41,8 @@
 //    requests per tile (templated 2048 / 4096 / 8192).
 //  * Index words are read straight from L2 into registers one set ahead (LDG with
 //    an L2 evict_last policy), bucket slices staged by cp.async (zero-fill past the
-//    shard, evict_first), one __syncthreads per set (the build of set j+1 overlaps
-//    the lookups of set j).
+//    shard, evict_first) three sets ahead; the build of set j+1 overlaps the
+//    lookups of set j (double-buffered tables).
 //  * Segment partials XOR into the answer rows (red.xor with an evict_last policy,
 //    so DRAM sees each answer row once), or, for the fused cross-GPU reduce, into a
 //    local partial buffer whose last-arriving segment pushes each finished row to
