@@ -498,11 +498,11 @@ cudaError_t launch_q9(const M4Args& a, int num_sms) {
 // Modelled time of a batch (arbitrary units: padded requests / measured
 // efficiency) for each tile size; the efficiencies are measured fractions of the
 // dense-ALU roofline at full tiles on a 1 GiB store, S = 4096 (scripts/time_scan.py):
-// 2048 -> 2.96, 4096 -> 3.46, 8192 -> 3.80 (the half-TMEM 128-byte-column kernel:
+// 2048 -> 2.98, 4096 -> 3.54, 8192 -> 3.82 (the half-TMEM 128-byte-column kernel:
 // 3.0, still 1-2% faster at B = 2048 and 6144).
 double m4rm_q_cost(uint32_t B, int* tile) {
     static const int rcs[3] = {2048, 4096, 8192};
-    static const double eff[3] = {2.96, 3.46, 3.80};
+    static const double eff[3] = {2.98, 3.54, 3.82};
     double best = 1e300;
     int best_rc = 2048;
     for (int k = 0; k < 3; ++k) {
