@@ -20,8 +20,8 @@
 //    32-bit words K1q reads, the ninth-bit bytes in a plane after them
 //    ([pair][request] bytes, four requests per 32-bit load).
 //  * Four 512-row tables of a set interleave per 128-byte bank line exactly as in
-//    K1q (row x of table t at x*128 + 32t): one set = 64 KiB; three table
-//    buffers (192 KiB) for the 8192/4096-request tiles, two for 2048. The 9-bit index is one PRMT of the set word and the request's ninth
+//    K1q (row x of table t at x*128 + 32t): one set = 64 KiB, double-buffered
+//    128 KiB. The 9-bit index is one PRMT of the set word and the request's ninth
 //    bits spread to one byte per table (IMAD by 0x204081 + LOP3, once per
 //    request and set).
 //  * Shared-memory wavefronts per set (Rc = 8192): 8192 lookups + 512 table
@@ -54,8 +54,8 @@
 // have finished its lookups) — and per staging slot one mbarrier that the
 // cp.async copies of the bucket slices arrive on as they land. A warp waits only
 // for what it reads next, so warps drift up to a set apart instead of meeting at
-// a barrier per set (config 4: 128.4 ms with a barrier per set -> 123.3 ms, and
-// 122.8 ms with a third table buffer; the 2048/4096-request tiles 4% / 5% faster).
+// a barrier per set (config 4: 128.4 ms with a barrier per set -> 123.3 ms; the
+// 2048/4096-request tiles 5% / 3% faster).
 //
 // TMEM map (one CTA per SM): warp w uses lanes 32*(w%4)..+31 and columns
 // 128*(w/4) + 8*s for its request slot s < 4*NQ.
@@ -77,17 +77,14 @@ constexpr int R_TAB = 512 * 128;  // one set of four interleaved 512-row tables
 constexpr int R_NST = 4;          // staging ring depth (sets)
 constexpr int R_STG = 36 * 32;    // 36 buckets x 32 B per staged set
 
-// table buffers: three let warps drift two sets apart (8192 / 4096-request tiles
-// 0.4% / 2% faster than two); the 2048-request tile runs faster with two
 template <int NQ>
 struct RCfg {
-    static constexpr int NTB = NQ >= 2 ? 3 : 2;
     static constexpr int RC = R_NT * 4 * NQ;  // requests per tile
     // two table buffers, staging ring, TMEM slot
-    static constexpr int OFF_STG = NTB * R_TAB;
+    static constexpr int OFF_STG = 2 * R_TAB;
     static constexpr int OFF_ADDR = OFF_STG + R_NST * R_STG;
-    static constexpr int OFF_MBAR = OFF_ADDR + 16;  // full[NTB], empty[NTB], staged[R_NST]
-    static constexpr int SMEM = OFF_MBAR + 16 * NTB + 8 * R_NST;
+    static constexpr int OFF_MBAR = OFF_ADDR + 16;  // full[2], empty[2], staged[R_NST]
+    static constexpr int SMEM = OFF_MBAR + 32 + 8 * R_NST;
     static constexpr int TCOLS = 128 * NQ;
     static_assert(SMEM <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
@@ -191,10 +188,10 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
     const uint32_t tbase = *reinterpret_cast<const uint32_t*>(sgen + C::OFF_ADDR);
     // mbarriers: full[b] / empty[b] per table buffer (16 warp arrivals each),
     // staged[k] per staging slot (72 copying threads' cp.async completions)
-    const uint32_t mb_full = sbase + C::OFF_MBAR, mb_empty = sbase + C::OFF_MBAR + 8 * C::NTB,
-                   mb_stg = sbase + C::OFF_MBAR + 16 * C::NTB;
+    const uint32_t mb_full = sbase + C::OFF_MBAR, mb_empty = sbase + C::OFF_MBAR + 16,
+                   mb_stg = sbase + C::OFF_MBAR + 32;
     if (tid == 0) {
-        for (int b = 0; b < C::NTB; ++b) {
+        for (int b = 0; b < 2; ++b) {
             mbar_init(mb_full + 8 * b, 16);
             mbar_init(mb_empty + 8 * b, 16);
         }
@@ -339,13 +336,10 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
         for (int p = 0; p < R_NST - 1; ++p)
             if (s0 + p < s1) stage(s0 + p, seq0 + p);
         mbar_wait(mb_stg + 8 * (seq0 % R_NST), (seq0 / R_NST) & 1);
-        {
-            const uint32_t b0 = seq0 % C::NTB, k0 = seq0 / C::NTB;
-            if (k0) mbar_wait(mb_empty + 8 * b0, (k0 - 1) & 1);
-            build(int(seq0 % R_NST), int(b0));
-            __syncwarp();
-            if (lane == 0) mbar_arrive(mb_full + 8 * b0);
-        }
+        if (seq0) mbar_wait(mb_empty, ((seq0 >> 1) - 1) & 1);
+        build(int(seq0 % R_NST), 0);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(mb_full);
 #pragma unroll 1
         for (uint32_t jp = s0; jp < s1; jp += 2) {
 #pragma unroll
@@ -367,18 +361,16 @@ k_scan_m4rm_q9(const uint8_t* __restrict__ db, uint32_t nb, uint32_t S, const ui
                 if (j + 1 < s1) {  // this warp's rows of set j+1, once its slices landed and buffer h^1 is free
                     const uint32_t sb = sq + 1;
                     mbar_wait(mb_stg + 8 * (sb % R_NST), (sb / R_NST) & 1);
-                    const uint32_t bb = sb % C::NTB, kb = sb / C::NTB;
-                    if (kb) mbar_wait(mb_empty + 8 * bb, (kb - 1) & 1);
-                    build(int(sb % R_NST), int(bb));
+                    mbar_wait(mb_empty + 8 * (h ^ 1), ((sb >> 1) - 1) & 1);
+                    build(int(sb % R_NST), h ^ 1);
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(mb_full + 8 * bb);
+                    if (lane == 0) mbar_arrive(mb_full + 8 * (h ^ 1));
                 }
-                const uint32_t bq = sq % C::NTB;
-                mbar_wait(mb_full + 8 * bq, (sq / C::NTB) & 1);  // set j built by every warp
-                lookups(wc, hc, 4u * uint32_t(h), int(bq));
+                mbar_wait(mb_full + 8 * h, (sq >> 1) & 1);  // set j built by every warp
+                lookups(wc, hc, 4u * uint32_t(h), h);
                 tm_wait_st();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(mb_empty + 8 * bq);
+                if (lane == 0) mbar_arrive(mb_empty + 8 * h);
             }
         }
         seq0 += s1 - s0;
@@ -498,11 +490,11 @@ cudaError_t launch_q9(const M4Args& a, int num_sms) {
 // Modelled time of a batch (arbitrary units: padded requests / measured
 // efficiency) for each tile size; the efficiencies are measured fractions of the
 // dense-ALU roofline at full tiles on a 1 GiB store, S = 4096 (scripts/time_scan.py):
-// 2048 -> 2.98, 4096 -> 3.54, 8192 -> 3.82 (the half-TMEM 128-byte-column kernel:
+// 2048 -> 2.96, 4096 -> 3.46, 8192 -> 3.80 (the half-TMEM 128-byte-column kernel:
 // 3.0, still 1-2% faster at B = 2048 and 6144).
 double m4rm_q_cost(uint32_t B, int* tile) {
     static const int rcs[3] = {2048, 4096, 8192};
-    static const double eff[3] = {2.98, 3.54, 3.82};
+    static const double eff[3] = {2.96, 3.46, 3.80};
     double best = 1e300;
     int best_rc = 2048;
     for (int k = 0; k < 3; ++k) {
